@@ -1,0 +1,385 @@
+"""Benchmark: 4D Vlasov DOF-updates/s per Strang step on B200 (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2]
+                    [--impl vpb|reference] [--no-e2e] [--no-cpu-baseline]
+
+One "step" is one ``strang_step(field, tau, consume=True)`` through the
+public API -- six sweeps, density, field solve, v-shift tables, and the
+per-step non-finite check (one D2H + sync) -- exactly what the reference's
+``bench_step`` times (/root/reference/pkg/src/slvp/bench.py:54-68).  The
+default workload is BASELINE config 2 (Landau 4D, 64^4 cells, degree 2 =
+192^4 = 1.36e9 dofs, 10.9 GB per copy of f, dt = 0.05), the configuration
+the metric is quoted on that fits one GPU.
+
+Timing: W untimed warm-up steps, then exactly K steps bracketed by a
+barrier + torch.cuda.synchronize(), timed with CUDA events on the launching
+stream; max over ranks.  The field (10.9 GB) is ~87x the 126 MB L2, so no
+explicit L2 flush is needed.  SM clocks / throttle reasons are sampled with
+nvidia-smi during the timed region.
+
+``e2e``: the same steps with f resident in pinned HOST memory, i.e. each
+step copies f host->device, runs the step, and copies f back (what a
+reference user holding f on the host sees).
+
+``roofline``: the dominant kernel (most device time per step) measured by
+CUDA events around its launches in the timed steps; algorithmic bytes = 16
+B per dof per sweep (one fp64 read + one write).
+
+``cpu_baseline`` / ``--impl reference``: the reference's own compiled line
+kernels (built into oracle/_ref from _kernels.pyx) driven like the
+reference's strang_step on every host thread, on a bounded scaled sample of
+the same configuration (oracle/refarm.py).
+
+Multi-GPU (torchrun, N > 1): each rank runs the full configuration on its
+own GPU as an independent replica (``scaling: weak``); the sharded strong
+scaling path lives in paper_1803_02143_b200.dist.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "4D Vlasov DOF-updates/s per Strang step at 1/2/4/8 B200; % of HBM roofline"
+UNIT = "DOF-updates/s"
+
+CONFIGS = {
+    # BASELINE.json configs (degree 2 == dg_order 3)
+    "cfg1": dict(problem="landau4d", method="dg", dofs=48, order=3, tau=0.1,
+                 label="BASELINE config 1: Landau 4D, 16^4 cells, degree 2 (48^4 dofs), dt=0.1"),
+    "cfg2": dict(problem="landau4d", method="dg", dofs=192, order=3, tau=0.05,
+                 label="BASELINE config 2: Landau 4D, 64^4 cells, degree 2 (192^4 = 1.36e9 dofs), dt=0.05"),
+    "cfg3": dict(problem="twostream4d_baseline", method="dg", dofs=128, order=2, tau=0.1,
+                 label="BASELINE config 3: two-stream 4D, 64^4 cells, degree 1 (128^4 dofs), dt=0.1"),
+    "cfg4": dict(problem="landau4d", method="spline", dofs=128, order=0, tau=0.1,
+                 label="BASELINE config 4: Landau 4D cubic spline, 128^4 points, dt=0.1"),
+    "cfg5": dict(problem="landau4d", method="dg", dofs=288, order=3, tau=0.05,
+                 label="BASELINE config 5: Landau 4D, 96^4 cells, degree 2 (288^4 = 6.9e9 dofs), dt=0.05"),
+}
+
+BYTES_PER_DOF_SWEEP = 16  # read + write one fp64 per dof
+
+
+def load_peaks() -> tuple[float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling
+# ---------------------------------------------------------------------------
+REASONS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+
+class ClockSampler:
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = Path(os.environ.get("TMPDIR", "/tmp")) / f"vpb_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        q = "clocks.sm,clocks.max.sm," + ",".join(f"clocks_event_reasons.{r}" for r in REASONS)
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self) -> dict | None:
+        if self.proc is None or not self.path.exists():
+            return None
+        sm, mx, active = [], [], set()
+        for line in self.path.read_text().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 2 + len(REASONS):
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for r, v in zip(REASONS, parts[2:]):
+                if v.lower().startswith("active"):
+                    active.add(r)
+        try:
+            self.path.unlink()
+        except OSError:
+            pass
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
+                "reasons": sorted(active), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+# ---------------------------------------------------------------------------
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def maybe_init(world: int, local: int, backend: str):
+    import torch
+    import torch.distributed as dist
+
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+    return dist if world > 1 else None
+
+
+def barrier(d, device=None):
+    if d is not None:
+        if device is not None:
+            d.barrier(device_ids=[device])
+        else:
+            d.barrier()
+
+
+def allreduce_max(d, value: float) -> float:
+    if d is None:
+        return value
+    import torch
+
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    d.all_reduce(t, op=d.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------
+def cpu_reference(cfg: dict) -> dict:
+    from oracle import refarm
+
+    return refarm.reference_step_rate(cfg["problem"], cfg["method"], cfg["dofs"], cfg["order"],
+                                      cfg["tau"])
+
+
+def run_reference_arm(args, cfg_name: str, cfg: dict) -> None:
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import core
+
+    samples = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_reference(cfg)
+        if i >= args.warmup:
+            samples.append(r)
+    vals = [s["dof_per_s"] for s in samples]
+    value = float(np.median(vals))
+    ms = float(np.median([s["step_s"] for s in samples])) * 1e3
+    last = samples[-1]
+    line = {
+        "impl": "reference",
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE initial condition, no dataset)",
+        "config": {"workload": cfg_name, "description": cfg["label"],
+                   "dofs": int(cfg["dofs"]) ** 4, "parallelism": "cpu-threads"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": last["threads"],
+                         "kind": last["kind"], "sample": last["sample"]},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "host_threads": core.host_threads(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_vpb(args, cfg_name: str, cfg: dict) -> None:
+    import torch
+
+    world, rank, local = dist_env()
+    d = maybe_init(world, local, "nccl")
+    torch.cuda.set_device(local)
+    import paper_1803_02143_b200 as vpb
+    from paper_1803_02143_b200 import driver
+
+    problem = vpb.problem_spec(cfg["problem"])
+    grid = vpb.make_grid(problem, cfg["method"], cfg["dofs"], dg_order=cfg["order"])
+    N = grid.total_dof
+    tau = cfg["tau"]
+    field = vpb.initialize(problem, grid)
+    st = driver.step_state(grid)
+    stream = torch.cuda.current_stream()
+
+    for _ in range(args.warmup):
+        driver.enqueue_step(field, tau, st)
+        driver.check_step(st, None)
+
+    # --- timed region: K public-API steps, events per step and per kernel group
+    labels: list = []
+    ev: list = []
+
+    def mark(label):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        ev.append(e)
+        labels.append(label)
+
+    barrier(d, local)
+    torch.cuda.synchronize()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        start.record(stream)
+        for _ in range(args.steps):
+            driver.enqueue_step(field, tau, st, timer=mark)
+            driver.check_step(st, None)
+        end.record(stream)
+        torch.cuda.synchronize()
+    barrier(d, local)
+    total_ms = start.elapsed_time(end)
+    total_ms = allreduce_max(d, total_ms)
+    ms_per_step = total_ms / args.steps
+    value = world * N * args.steps / (total_ms * 1e-3)
+
+    # per-group device time
+    groups: dict = {}
+    for i in range(len(ev) - 1):
+        if labels[i] is None:
+            continue
+        dt = ev[i].elapsed_time(ev[i + 1])
+        g = groups.setdefault(labels[i], [0.0, 0])
+        g[0] += dt
+        g[1] += 1
+    sweeps = {k: v for k, v in groups.items() if k.startswith("sweep_")}
+    dom = max(sweeps, key=lambda k: sweeps[k][0])
+    dom_avg_ms = sweeps[dom][0] / sweeps[dom][1]
+    peak, peak_kind = load_peaks()
+    achieved = BYTES_PER_DOF_SWEEP * N / (dom_avg_ms * 1e-3) / 1e9
+    step_gbs = 6 * BYTES_PER_DOF_SWEEP * N / (ms_per_step * 1e-3) / 1e9
+    per_kernel = {k: {"avg_ms": v[0] / v[1], "launch_groups": v[1],
+                      "share_of_step": v[0] / total_ms}
+                  for k, v in sorted(groups.items())}
+    for k, v in per_kernel.items():
+        if k.startswith("sweep_"):
+            v["achieved_gbs"] = BYTES_PER_DOF_SWEEP * N / (v["avg_ms"] * 1e-3) / 1e9
+            v["frac"] = v["achieved_gbs"] / peak
+
+    # --- e2e through the public API with host-resident f
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty(N, dtype=torch.float64, pin_memory=True)
+        host.copy_(field.data)
+        torch.cuda.synchronize()
+        k_e2e = max(1, min(args.steps, args.e2e_steps))
+        barrier(d, local)
+        torch.cuda.synchronize()
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(k_e2e):
+            field.data.copy_(host, non_blocking=True)
+            vpb.strang_step(field, tau, consume=True)
+            host.copy_(field.data, non_blocking=True)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = allreduce_max(d, s0.elapsed_time(s1))
+        e2e = {"value": world * N * k_e2e / (e2e_ms * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N, "steps": k_e2e,
+               "ms_per_step": e2e_ms / k_e2e,
+               "path": "pinned host f -> H2D -> strang_step -> D2H, every step"}
+        del host
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r = cpu_reference(cfg)
+        cpu = {"value": r["dof_per_s"], "unit": UNIT, "cores": r["threads"], "kind": r["kind"],
+               "sample": r["sample"]}
+
+    launches_per_step = {"dg": 6 + 2 + 2 + 5, "spline": 6 + 2 + 5}[cfg["method"]]
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": UNIT,
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_per_step,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (BASELINE initial condition on the named grid; no dataset)",
+            "config": {"workload": cfg_name, "description": cfg["label"], "dofs": N,
+                       "bytes_per_copy": 8 * N, "l2": "inputs (10.9 GB) >> 126 MB L2; no flush",
+                       "parallelism": "replicas" if world > 1 else "single-gpu"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": args.traffic, "kernel": dom,
+                         "peak_source": peak_kind,
+                         "algorithmic_bytes_per_launch": BYTES_PER_DOF_SWEEP * N,
+                         "step_frac": step_gbs / peak,
+                         "step_bytes": 6 * BYTES_PER_DOF_SWEEP * N},
+            "kernels": per_kernel,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": clocks.summary(),
+            "gpu_launches": launches_per_step * args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    if d is not None:
+        d.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="vpb", choices=["vpb", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="ncu dram bytes per launch of the dominant kernel (from profiles/)")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "vpb":
+        print("note: warmup raised to 3 (timing rules)", file=sys.stderr)
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference_arm(args, args.config, cfg)
+    else:
+        run_vpb(args, args.config, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,176 @@
+/*
+ * vpb200 — C ABI of the B200-native SLDG / cubic-spline Vlasov hot path.
+ *
+ * Every pointer argument is a DEVICE pointer (CUDA global memory) unless the
+ * comment says otherwise; `stream` is a cudaStream_t passed as void*.  Entry
+ * points return VPB_OK (0) or a nonzero status; vpb_last_error() gives the
+ * message of the calling thread's most recent failure.  No C++ exceptions
+ * cross this boundary and the library keeps no ownership of caller buffers
+ * (it caches only small per-size constant tables: the spline factors).
+ *
+ * Field layout for the *_axis entry points ("canonical"): f[v2][v1][x2][x1],
+ * row-major, x1 fastest; each axis holds cells*(order) dofs with the dG
+ * nodes innermost (reference: pkg/src/slvp/field.py:67-76, 246-251).
+ * dims[4] = dofs per axis in GRID order (x1, x2, v1, v2).  A 1x1v grid is
+ * dims = {nx, 1, nv, 1}.
+ *
+ * Reference interfaces replaced (all paths under /root/reference/pkg/src/slvp):
+ *   vpb_dg_sweep_contig      <- kernels.dg_sweep_contig      kernels.py:63-66, _kernels.pyx:202-225
+ *   vpb_dg_sweep_strided     <- kernels.dg_sweep_strided     kernels.py:69-72, _kernels.pyx:228-279
+ *   vpb_spline_sweep_contig  <- kernels.spline_sweep_contig  kernels.py:55-56, _kernels.pyx:126-149
+ *   vpb_spline_sweep_strided <- kernels.spline_sweep_strided kernels.py:59-60, _kernels.pyx:152-199
+ *   vpb_dg_tables            <- dg.projection_pairs          dg.py:99-152
+ *   vpb_dg_sweep_axis        <- field._sweep + DGAdvection   field.py:166-202, dg.py:178-209
+ *   vpb_spline_sweep_axis    <- field._sweep + SplineAdvection field.py:166-202, spline.py:91-110
+ *   vpb_density              <- poisson.compute_density      poisson.py:85-95
+ *   vpb_field_solve          <- poisson.solve_poisson        poisson.py:123-196
+ *   vpb_diagnostics          <- driver.diagnostics + poisson.electric_energy
+ *                                                           driver.py:279-316, poisson.py:199-217
+ *   vpb_electric_energy      <- poisson.electric_energy      poisson.py:199-217
+ *   vpb_fill_separable       <- driver.initialize (broadcast product) driver.py:182-198
+ *   vpb_halo_*               <- (new) x-axis halo pack/unpack for sharded fields
+ * The reference's `threads` / `block` arguments are CPU scheduling knobs and
+ * have no GPU meaning; they are dropped.
+ */
+#ifndef VPB200_H
+#define VPB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  VPB_OK = 0,
+  VPB_ERR_INVALID = 1,     /* bad argument (same cases the reference rejects with ValueError) */
+  VPB_ERR_CUDA = 2,        /* CUDA runtime / launch failure */
+  VPB_ERR_UNSUPPORTED = 3  /* valid but not implemented (e.g. order > 9) */
+};
+
+const char* vpb_version(void);
+const char* vpb_strerror(int code);
+const char* vpb_last_error(void);
+
+/* ------------------------------------------------------------------------
+ * Reference plugin API: the four line-kernel entry points.
+ * ---------------------------------------------------------------------- */
+
+/* lines/out: [nlines][n] C-contiguous, n = ncells*nloc.  idx[r] selects the
+ * table row (a,b: [ntable][nloc][nloc], q, alpha: [ntable]).  out is a
+ * separate buffer (the reference returns a new array). */
+int vpb_dg_sweep_contig(const double* lines, double* out, int64_t nlines, int64_t n,
+                        const int64_t* idx, const double* a, const double* b,
+                        const int64_t* q, const double* alpha, int64_t ntable,
+                        int32_t ncells, int32_t nloc, void* stream);
+
+/* view: 4-D strided array (element strides), last axis = the line; lines are
+ * enumerated in C order over shape[0..2].  Updated IN PLACE. */
+int vpb_dg_sweep_strided(double* view, const int64_t shape[4], const int64_t strides[4],
+                         const int64_t* idx, const double* a, const double* b,
+                         const int64_t* q, const double* alpha, int64_t ntable,
+                         int32_t ncells, int32_t nloc, void* stream);
+
+/* Cubic-spline advection: out_i = spline(line)(x_i - table[idx[r]]). */
+int vpb_spline_sweep_contig(const double* lines, double* out, int64_t nlines, int64_t n,
+                            const int64_t* idx, const double* table, int64_t ntable,
+                            double h, void* stream);
+int vpb_spline_sweep_strided(double* view, const int64_t shape[4], const int64_t strides[4],
+                             const int64_t* idx, const double* table, int64_t ntable,
+                             double h, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Device-resident hot path (canonical layout).
+ * ---------------------------------------------------------------------- */
+
+/* projection_pairs: shift[t] = values[t]*scale; s = shift/h; q = floor(s);
+ * alpha = s - q (carry alpha>=1 -> q+1, alpha=0); a,b = [ntable][order][order]. */
+int vpb_dg_tables(const double* values, int64_t ntable, double scale, double h, int32_t order,
+                  double* a, double* b, int64_t* q, double* alpha, void* stream);
+
+/* One dG sweep along `axis` (0=x1, 1=x2, 2=v1, 3=v2) from src to dst
+ * (distinct buffers).  Table row per line: x1 -> iv1, x2 -> iv2,
+ * v1/v2 -> ix2*dims[0]+ix1 (the device E layout).  *flag |= 1 if any output
+ * is non-finite (flag may be NULL). */
+int vpb_dg_sweep_axis(int32_t axis, const double* src, double* dst, const int64_t dims[4],
+                      int32_t order, const double* a, const double* b, const int64_t* q,
+                      const double* alpha, int32_t* flag, void* stream);
+
+/* One spline sweep along `axis`; shift of line = values[table row]*scale. */
+int vpb_spline_sweep_axis(int32_t axis, const double* src, double* dst, const int64_t dims[4],
+                          const double* values, double scale, double h, int32_t* flag,
+                          void* stream);
+
+/* rho[ix2*n1+ix1] = sum_v f * wv1[iv1] * wv2[iv2].  work: vpb_density_work_len doubles. */
+int64_t vpb_density_work_len(const int64_t dims[4]);
+int vpb_density(const double* f, const int64_t dims[4], const double* wv1, const double* wv2,
+                double* rho, double* work, void* stream);
+
+/* Spectral field solve on small dense transforms (all complex arrays are
+ * interleaved re,im, row-major):
+ *   rhohat = G1 * R * G2^T        (R[i1][i2] = rho[i2*n1+i1])
+ *   E_d    = Re(M1 * (K_d .* rhohat) * M2^T),  d = 0, 1
+ * E is written as e[d*n1*n2 + i2*n1 + i1].  stats[0] = weighted density mean
+ * (neutrality check, poisson.py:143-160).  *flag |= 1 if E is non-finite. */
+typedef struct {
+  int64_t n1, n2;       /* dofs along x1, x2 (n2 = 1 for 1x1v) */
+  int64_t c1, c2;       /* Fourier sizes (cells for dG, points for spline) */
+  int32_t ncomp;        /* field components: 2 for 2x2v, 1 for 1x1v */
+  const double* g1;     /* complex [c1][n1] */
+  const double* g2;     /* complex [c2][n2] */
+  const double* m1;     /* complex [n1][c1] */
+  const double* m2;     /* complex [n2][c2] */
+  const double* kmul;   /* complex [ncomp][c1][c2] */
+  const double* wx1;    /* [n1] quadrature weights */
+  const double* wx2;    /* [n2] */
+  double volume;        /* spatial measure */
+} vpb_field_geom;
+
+int64_t vpb_field_work_len(const vpb_field_geom* geom);
+int vpb_field_solve(const double* rho, const vpb_field_geom* geom, double* e, double* stats,
+                    double* work, int32_t* flag, void* stream);
+
+/* Diagnostics (driver.py:279-316): out[0..4] = mass, l1, l2^2, kinetic, EE.
+ * wx = [n1*n2] product weights wx1[ix1]*wx2[ix2] in device layout; e may be
+ * NULL (EE = 0).  work: vpb_diag_work_len doubles. */
+int64_t vpb_diag_work_len(const int64_t dims[4]);
+int vpb_diagnostics(const double* f, const int64_t dims[4], const double* wx,
+                    const double* wv1, const double* wv2, const double* v1sq,
+                    const double* v2sq, const double* e, int32_t ncomp, double* out,
+                    double* work, void* stream);
+
+/* out[0] = 0.5 * sum_d sum_x e[d*nx + x]^2 * wx[x]  (poisson.py:199-217). */
+int vpb_electric_energy(const double* e, int32_t ncomp, int64_t nx, const double* wx,
+                        double* out, void* stream);
+
+/* f[iv2][iv1][x] = (g2[iv2]*g1[iv1]) * space[x]  (x = ix2*n1+ix1). */
+int vpb_fill_separable(double* f, const int64_t dims[4], const double* g1, const double* g2,
+                       const double* space, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Sharded fields (multi-GPU layer): the local shard holds cells [c0, c0+cl)
+ * of the sharded x axis; halos are cell slabs of the full line geometry.
+ * ---------------------------------------------------------------------- */
+
+/* Pack `width` cells of every line along `axis` (0 or 1) starting at local
+ * cell `cell0` into a contiguous buffer [lines][width*order] (lines in C
+ * order over the transverse axes). */
+int vpb_halo_pack(int32_t axis, const double* f, const int64_t dims[4], int32_t order,
+                  int64_t cell0, int64_t width, double* buf, void* stream);
+
+/* dG sweep of a shard along a sharded x axis (axis 0 or 1).  Source cells
+ * outside the local range [0, cl) are read from the halo buffers (no
+ * periodic wrap inside the shard): `left` holds the wl cells just below the
+ * shard, `right` the wr cells just above it, both in the halo layout of
+ * vpb_halo_pack.  Requires wl >= max(q+1, 0) and wr >= max(-q, 0) over the
+ * table rows used. */
+int vpb_dg_sweep_axis_halo(int32_t axis, const double* src, double* dst, const int64_t dims[4],
+                           int32_t order, const double* left, int64_t wl, const double* right,
+                           int64_t wr, const double* a, const double* b, const int64_t* q,
+                           const double* alpha, int32_t* flag, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VPB200_H */

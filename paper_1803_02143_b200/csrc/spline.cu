@@ -1,0 +1,359 @@
+// Periodic cubic-spline sweeps for sm_100a.
+//
+// Reference arithmetic (pkg/src/slvp/_kernels.pyx:37-93, _kernels_py.py:16-77):
+//   solve  y = 6u; y_i -= mult_i*y_{i-1}; y_{n-1} /= denom_{n-1};
+//          y_i = (y_i - y_{i+1}) / denom_i; fac = (y_0 - 0.25 y_{n-1}) / sden;
+//          w_i = y_i - fac*z_i
+//   eval   s = shift/h; off = floor(-s); theta = -s - off (carry theta>=1);
+//          out_i = w0 om[j0+i] + w1 om[j0+i+1] + w2 om[j0+i+2] + w3 om[j0+i+3]
+//          with j0 = (off-1) mod n, summed left to right.
+// Every operation keeps the reference's order and rounding (no contraction).
+// The divisions by the constant denominators use the Markstein sequence
+//   q = y*r;  e = fma(-q, d, y);  q' = fma(e, r, q)      (r = RN(1/d))
+// which returns the correctly rounded y/d for all finite normal operands, so
+// the result is bitwise that of the reference's `/`.
+//
+// Kernel shape: a CTA owns a tile of T lines.  The tile is staged in shared
+// memory in [point][line] order, each thread runs the sequential Thomas
+// recurrence on its own line (the recurrence is latency bound, so the tile
+// is sized to keep several CTAs per SM), then the evaluation is remapped so
+// that stores are coalesced along the memory-contiguous direction.
+#include <algorithm>
+#include <map>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace vpb {
+
+constexpr int kSplineT = 32;  // lines per CTA
+
+struct SplineFactors {
+  int64_t n;
+  double* dev;  // [mult n][denom n][rden n][z n][sden, rsden]
+};
+
+// _factors(n) restated (pkg/src/slvp/_kernels_py.py:22-46), same operation
+// order; compiled with -ffp-contract=off so it rounds exactly like NumPy.
+static void host_factors(int64_t n, double* mult, double* denom, double* z, double* sden) {
+  const double gamma = -4.0;
+  double* diag = new double[n];
+  for (int64_t i = 0; i < n; ++i) diag[i] = 4.0;
+  diag[0] -= gamma;
+  diag[n - 1] -= 1.0 / gamma;
+  mult[0] = 0.0;
+  denom[0] = diag[0];
+  for (int64_t i = 1; i < n; ++i) {
+    mult[i] = 1.0 / denom[i - 1];
+    denom[i] = diag[i] - mult[i];
+  }
+  for (int64_t i = 0; i < n; ++i) z[i] = 0.0;
+  z[0] = gamma;
+  z[n - 1] = 1.0;
+  for (int64_t i = 1; i < n; ++i) z[i] -= mult[i] * z[i - 1];
+  z[n - 1] /= denom[n - 1];
+  for (int64_t i = n - 2; i >= 0; --i) {
+    z[i] -= z[i + 1];
+    z[i] /= denom[i];
+  }
+  *sden = 1.0 + z[0] - 0.25 * z[n - 1];
+  delete[] diag;
+}
+
+static int get_factors(int64_t n, const double** out) {
+  static std::mutex mu;
+  static std::map<std::pair<int, int64_t>, double*> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return check_launch("cudaGetDevice");
+  std::lock_guard<std::mutex> lock(mu);
+  auto key = std::make_pair(dev, n);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *out = it->second;
+    return VPB_OK;
+  }
+  double* h = new double[4 * n + 2];
+  double sden;
+  host_factors(n, h, h + n, h + 3 * n, &sden);
+  for (int64_t i = 0; i < n; ++i) h[2 * n + i] = 1.0 / h[n + i];
+  h[4 * n] = sden;
+  h[4 * n + 1] = 1.0 / sden;
+  double* d = nullptr;
+  if (cudaMalloc(&d, (4 * n + 2) * sizeof(double)) != cudaSuccess ||
+      cudaMemcpy(d, h, (4 * n + 2) * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) {
+    delete[] h;
+    return check_launch("spline factors upload");
+  }
+  delete[] h;
+  cache[key] = d;
+  *out = d;
+  return VPB_OK;
+}
+
+__device__ __forceinline__ double div_exact(double y, double d, double r) {
+  double q = __dmul_rn(y, r);
+  double e = __fma_rn(-q, d, y);
+  return __fma_rn(e, r, q);
+}
+
+// Line geometry of a tile.  Line L's point i sits at
+//   CONTIG:  src + L*n + i
+//   strided: src + (L / S) * S * n + (L % S) + i*S
+// Table row: idx ? idx[L] : (L / tdiv) % tmod.
+struct SplineTileArgs {
+  const double* src;
+  double* dst;
+  int64_t nlines;
+  int n;
+  int64_t S;
+  const int64_t* idx;
+  int64_t tdiv, tmod;
+  const double* values;
+  double scale, h;
+  const double* fac;
+  int32_t* flag;
+};
+
+template <bool CONTIG>
+__global__ void __launch_bounds__(kSplineT)
+    spline_tile_kernel(SplineTileArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  constexpr int T = kSplineT;
+  constexpr int RS = CONTIG ? T + 1 : T;  // row stride of the [point][line] tile
+  const int n = a.n;
+  double* tile = sm;                                // n * RS
+  double* wts = tile + (int64_t)n * RS;             // [T][4]
+  int* j0s = reinterpret_cast<int*>(wts + 4 * T);   // [T]
+  const int t = threadIdx.x;
+  const int64_t L0 = (int64_t)blockIdx.x * T;
+  const int lines = (int)min((int64_t)T, a.nlines - L0);
+
+  // ---- stage the tile ----
+  if (CONTIG) {
+    const double* base = a.src + L0 * n;
+    const int total = lines * n;
+    for (int e = t; e < total; e += T) {
+      int r = e / n, i = e - r * n;
+      tile[i * RS + r] = __ldcs(base + e);
+    }
+  } else if (t < lines) {
+    const int64_t L = L0 + t;
+    const int64_t outer = L / a.S, inner = L - outer * a.S;
+    const double* base = a.src + outer * a.S * n + inner;
+#pragma unroll 8
+    for (int i = 0; i < n; ++i) tile[i * RS + t] = __ldcs(base + (int64_t)i * a.S);
+  }
+  __syncthreads();
+
+  // ---- per-line solve + eval weights ----
+  if (t < lines) {
+    const double* mult = a.fac;
+    const double* denom = a.fac + n;
+    const double* rden = a.fac + 2 * n;
+    const double* z = a.fac + 3 * n;
+    const double sden = a.fac[4 * n], rsden = a.fac[4 * n + 1];
+    double* y = tile + t;
+    double prev = __dmul_rn(6.0, y[0]);
+    y[0] = prev;
+    for (int i = 1; i < n; ++i) {
+      double v = __dsub_rn(__dmul_rn(6.0, y[i * RS]), __dmul_rn(mult[i], prev));
+      y[i * RS] = v;
+      prev = v;
+    }
+    prev = div_exact(prev, denom[n - 1], rden[n - 1]);
+    y[(n - 1) * RS] = prev;
+    for (int i = n - 2; i >= 0; --i) {
+      double v = div_exact(__dsub_rn(y[i * RS], prev), denom[i], rden[i]);
+      y[i * RS] = v;
+      prev = v;
+    }
+    const double fac = div_exact(__dsub_rn(prev, __dmul_rn(0.25, y[(n - 1) * RS])), sden, rsden);
+    for (int i = 0; i < n; ++i) y[i * RS] = __dsub_rn(y[i * RS], __dmul_rn(fac, z[i]));
+
+    const int64_t L = L0 + t;
+    const int64_t row = a.idx ? a.idx[L] : (L / a.tdiv) % a.tmod;
+    const double shift = __dmul_rn(a.values[row], a.scale);
+    const double s = __ddiv_rn(shift, a.h);
+    double off = floor(-s);
+    double th = __dsub_rn(-s, off);
+    if (th >= 1.0) {
+      off = __dadd_rn(off, 1.0);
+      th = 0.0;
+    }
+    const double omt = __dsub_rn(1.0, th);
+    const double th2 = __dmul_rn(th, th), omt2 = __dmul_rn(omt, omt);
+    wts[4 * t + 0] = __ddiv_rn(__dmul_rn(omt2, omt), 6.0);
+    wts[4 * t + 1] = __ddiv_rn(
+        __dadd_rn(__dsub_rn(4.0, __dmul_rn(__dmul_rn(6.0, th), th)),
+                  __dmul_rn(__dmul_rn(__dmul_rn(3.0, th), th), th)),
+        6.0);
+    wts[4 * t + 2] = __ddiv_rn(
+        __dadd_rn(__dsub_rn(4.0, __dmul_rn(__dmul_rn(6.0, omt), omt)),
+                  __dmul_rn(__dmul_rn(__dmul_rn(3.0, omt), omt), omt)),
+        6.0);
+    wts[4 * t + 3] = __ddiv_rn(__dmul_rn(th2, th), 6.0);
+    (void)omt2;
+    j0s[t] = (int)wrap_mod((int64_t)off - 1, n);
+  }
+  __syncthreads();
+
+  // ---- evaluation, coalesced along memory ----
+  bool bad = false;
+  auto eval = [&](int r, int i) -> double {
+    const double* w = wts + 4 * r;
+    int j = j0s[r] + i;
+    if (j >= n) j -= n;
+    int j1 = j + 1 == n ? 0 : j + 1;
+    int j2 = j1 + 1 == n ? 0 : j1 + 1;
+    int j3 = j2 + 1 == n ? 0 : j2 + 1;
+    double o = __dmul_rn(w[0], tile[j * RS + r]);
+    o = __dadd_rn(o, __dmul_rn(w[1], tile[j1 * RS + r]));
+    o = __dadd_rn(o, __dmul_rn(w[2], tile[j2 * RS + r]));
+    o = __dadd_rn(o, __dmul_rn(w[3], tile[j3 * RS + r]));
+    return o;
+  };
+  if (CONTIG) {
+    double* base = a.dst + L0 * n;
+    const int total = lines * n;
+    for (int e = t; e < total; e += T) {
+      int r = e / n, i = e - r * n;
+      double o = eval(r, i);
+      bad |= not_finite(o);
+      __stcs(base + e, o);
+    }
+  } else if (t < lines) {
+    const int64_t L = L0 + t;
+    const int64_t outer = L / a.S, inner = L - outer * a.S;
+    double* base = a.dst + outer * a.S * n + inner;
+    for (int i = 0; i < n; ++i) {
+      double o = eval(t, i);
+      bad |= not_finite(o);
+      __stcs(base + (int64_t)i * a.S, o);
+    }
+  }
+  report_flag(bad, a.flag);
+}
+
+static size_t spline_smem(int n, bool contig) {
+  int rs = contig ? kSplineT + 1 : kSplineT;
+  return (size_t)n * rs * sizeof(double) + 4 * kSplineT * sizeof(double) + kSplineT * sizeof(int);
+}
+
+static int launch_spline(SplineTileArgs a, bool contig, cudaStream_t st) {
+  if (a.nlines == 0) return VPB_OK;
+  size_t smem = spline_smem(a.n, contig);
+  if (smem > 220 * 1024) {
+    set_error("spline line of %d points does not fit a shared-memory tile", a.n);
+    return VPB_ERR_UNSUPPORTED;
+  }
+  int rc = get_factors(a.n, &a.fac);
+  if (rc) return rc;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(spline_tile_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         220 * 1024);
+    cudaFuncSetAttribute(spline_tile_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         220 * 1024);
+    attr = true;
+  }
+  int64_t blocks = (a.nlines + kSplineT - 1) / kSplineT;
+  if (contig)
+    spline_tile_kernel<true><<<(unsigned)blocks, kSplineT, smem, st>>>(a);
+  else
+    spline_tile_kernel<false><<<(unsigned)blocks, kSplineT, smem, st>>>(a);
+  return check_launch("spline_tile_kernel");
+}
+
+__global__ void spline_gather4d_kernel(const double* __restrict__ view, double* __restrict__ lines,
+                                       int64_t s0, int64_t s1, int64_t s2, int64_t n, int64_t st0,
+                                       int64_t st1, int64_t st2, int64_t st3, int scatter,
+                                       double* __restrict__ view_out) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t total = s0 * s1 * s2 * n;
+  if (e >= total) return;
+  int64_t r = e / n, kk = e - r * n;
+  int64_t i2 = r % s2;
+  int64_t r2 = r / s2;
+  int64_t i1 = r2 % s1;
+  int64_t i0 = r2 / s1;
+  int64_t off = i0 * st0 + i1 * st1 + i2 * st2 + kk * st3;
+  if (scatter)
+    view_out[off] = lines[e];
+  else
+    lines[e] = view[off];
+}
+
+}  // namespace vpb
+
+using namespace vpb;
+
+extern "C" int vpb_spline_sweep_contig(const double* lines, double* out, int64_t nlines, int64_t n,
+                                       const int64_t* idx, const double* table, int64_t ntable,
+                                       double h, void* stream) {
+  VPB_REQUIRE(n >= 2, "need at least 2 samples per line, got %lld", (long long)n);
+  VPB_REQUIRE(h > 0.0, "spacing must be positive, got %g", h);
+  VPB_REQUIRE(lines != out, "out must not alias lines");
+  VPB_REQUIRE(idx != nullptr && table != nullptr && ntable > 0, "table index required");
+  SplineTileArgs a{lines, out, nlines, (int)n, 1, idx, 1, ntable, table, 1.0, h, nullptr, nullptr};
+  return launch_spline(a, true, (cudaStream_t)stream);
+}
+
+extern "C" int vpb_spline_sweep_strided(double* view, const int64_t shape[4],
+                                        const int64_t strides[4], const int64_t* idx,
+                                        const double* table, int64_t ntable, double h,
+                                        void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t nlines = shape[0] * shape[1] * shape[2];
+  int64_t total = nlines * shape[3];
+  if (total == 0) return VPB_OK;
+  double* tmp = nullptr;
+  if (cudaMallocAsync(&tmp, 2 * total * sizeof(double), st) != cudaSuccess)
+    return check_launch("cudaMallocAsync");
+  int64_t blocks = (total + 255) / 256;
+  spline_gather4d_kernel<<<(unsigned)blocks, 256, 0, st>>>(view, tmp, shape[0], shape[1],
+                                                           shape[2], shape[3], strides[0],
+                                                           strides[1], strides[2], strides[3], 0,
+                                                           nullptr);
+  int rc = vpb_spline_sweep_contig(tmp, tmp + total, nlines, shape[3], idx, table, ntable, h,
+                                   stream);
+  if (rc == VPB_OK) {
+    spline_gather4d_kernel<<<(unsigned)blocks, 256, 0, st>>>(
+        nullptr, tmp + total, shape[0], shape[1], shape[2], shape[3], strides[0], strides[1],
+        strides[2], strides[3], 1, view);
+    rc = check_launch("spline scatter4d");
+  }
+  cudaFreeAsync(tmp, st);
+  return rc;
+}
+
+extern "C" int vpb_spline_sweep_axis(int32_t axis, const double* src, double* dst,
+                                     const int64_t dims[4], const double* values, double scale,
+                                     double h, int32_t* flag, void* stream) {
+  VPB_REQUIRE(axis >= 0 && axis < 4, "axis %d out of range", axis);
+  VPB_REQUIRE(src != dst, "src and dst must be distinct buffers");
+  VPB_REQUIRE(h > 0.0, "spacing must be positive, got %g", h);
+  const int64_t n1 = dims[0], n2 = dims[1], nv1 = dims[2], nv2 = dims[3];
+  const int64_t total = n1 * n2 * nv1 * nv2;
+  const int64_t n = dims[axis];
+  VPB_REQUIRE(n >= 2, "need at least 2 samples per line");
+  SplineTileArgs a{src, dst, total / n, (int)n, 1, nullptr, 1, 1, values, scale, h, nullptr, flag};
+  if (axis == 0) {
+    a.tdiv = n2;  // lines = (iv2, iv1, ix2), row = iv1
+    a.tmod = nv1;
+    return launch_spline(a, true, (cudaStream_t)stream);
+  }
+  if (axis == 1) {
+    a.S = n1;
+    a.tdiv = n1 * nv1;  // row = iv2
+    a.tmod = nv2;
+  } else if (axis == 2) {
+    a.S = n1 * n2;
+    a.tdiv = 1;  // row = x index
+    a.tmod = n1 * n2;
+  } else {
+    a.S = n1 * n2 * nv1;
+    a.tdiv = 1;
+    a.tmod = n1 * n2;
+  }
+  return launch_spline(a, false, (cudaStream_t)stream);
+}

@@ -1,0 +1,500 @@
+"""Time integration on the device: problems, initial data, Strang step, run loop.
+
+Mirrors ``slvp.driver`` (/root/reference/pkg/src/slvp/driver.py).  One
+``strang_step`` (driver.py:245-265) is, for a 2x2v grid,
+
+    x1(tau/2) x2(tau/2) | rho -> E | v1(tau) v2(tau) | x1(tau/2) x2(tau/2)
+
+entirely in HBM: six sweep kernels ping-ponging between the field's buffer
+and one scratch buffer, the density reduction, four small transform GEMMs,
+and on-device table generation for the E-dependent velocity shifts.  The
+reference's per-sub-step ``isfinite(sum(f))`` checks (driver.py:209-211)
+become flag words set by each kernel's epilogue; they are read back once
+per step and the first flagged sub-step is raised as :class:`SubstepError`
+with the reference's exact message.  (Unlike the reference, the remaining
+sub-steps of a failing step still execute before the error is raised.)
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from functools import lru_cache
+
+import numpy as np
+import torch
+
+from . import _device, _lib
+from .dg import DeviceTables, sweep_dg
+from .field import DEFAULT_STRATEGY, DistributionField, LayoutDescriptor, write_snapshot
+from .grid import DG, SPACE, SPLINE, VELOCITY, Axis, GridSpec
+from .poisson import (
+    ElectricField,
+    _device_x,
+    _warn_if_not_neutral,
+    density_into,
+    geometry,
+    scratch,
+    solve_into,
+)
+from .spline import sweep_spline
+
+
+class SubstepError(RuntimeError):
+    """Non-finite values after a sub-step (driver.py:31-38)."""
+
+    def __init__(self, substep: str, time: float | None = None):
+        self.substep = substep
+        self.time = time
+        at = "" if time is None else f" at t={time:g}"
+        super().__init__(f"non-finite values after sub-step '{substep}'{at}")
+
+
+@dataclass(frozen=True)
+class ProblemSpec:
+    """Benchmark problem: extents and initial-data parameters (driver.py:41-58)."""
+
+    name: str
+    x_extents: tuple
+    v_extents: tuple
+    epsilon: float
+    wavenumber: float
+    drift: float = 0.0
+
+    @property
+    def ndim_x(self) -> int:
+        return len(self.x_extents)
+
+    @property
+    def ndim(self) -> int:
+        return 2 * self.ndim_x
+
+
+_FOUR_PI = 4.0 * math.pi
+_TEN_PI = 10.0 * math.pi
+
+_PROBLEMS = {
+    # driver.py:61-84
+    "landau2d": ProblemSpec("landau2d", ((0.0, _FOUR_PI),), ((-6.0, 6.0),), 0.5, 0.5),
+    "landau4d": ProblemSpec("landau4d", ((0.0, _FOUR_PI),) * 2, ((-6.0, 6.0),) * 2, 0.5, 0.5),
+    "twostream4d": ProblemSpec(
+        "twostream4d", ((0.0, _TEN_PI),) * 2, ((-6.0, 6.0),) * 2, 1e-3, 0.2, drift=2.4
+    ),
+    # BASELINE.json config 3: beams along v1 only, additive perturbation
+    # (1/2pi) * 0.5[e^{-(v1-d)^2/2} + e^{-(v1+d)^2/2}] e^{-v2^2/2} (1 + eps cos k x1 + eps cos k x2)
+    "twostream4d_baseline": ProblemSpec(
+        "twostream4d_baseline", ((0.0, _TEN_PI),) * 2, ((-6.0, 6.0),) * 2, 1e-3, 0.2, drift=2.4
+    ),
+}
+
+
+def problem_spec(name: str) -> ProblemSpec:
+    try:
+        return _PROBLEMS[name]
+    except KeyError:
+        known = ", ".join(sorted(_PROBLEMS))
+        raise ValueError(f"unknown problem {name!r} (known: {known})") from None
+
+
+def parse_method(name: str) -> tuple[str, int]:
+    """"spline" -> (spline, 0); "dg<order>" -> (dg, order-1) (driver.py:95-107)."""
+    if name == "spline":
+        return SPLINE, 0
+    if name.startswith("dg") and name[2:].isdigit():
+        order = int(name[2:])
+        if 1 <= order <= 9:
+            return DG, order - 1
+    raise ValueError(f"unknown method {name!r} (expected 'spline' or 'dg<order>')")
+
+
+def method_label(grid: GridSpec) -> str:
+    return "spline" if grid.method == SPLINE else f"dg{grid.dg_degree + 1}"
+
+
+def make_grid(problem: ProblemSpec, method: str, dofs, dg_order: int = 0) -> GridSpec:
+    """Grid targeting ``dofs`` points per axis (driver.py:114-144)."""
+    if isinstance(dofs, int):
+        dofs = (dofs,) * problem.ndim
+    if len(dofs) != problem.ndim:
+        raise ValueError(f"expected {problem.ndim} dof values, got {len(dofs)}")
+    if method == DG:
+        if not 1 <= dg_order <= 9:
+            raise ValueError("dg_order must be in 1..9")
+        counts = [max(4, round(d / dg_order)) for d in dofs]
+    elif method == SPLINE:
+        counts = list(dofs)
+    else:
+        raise ValueError(f"unknown method {method!r}")
+    axes = [Axis(lo, hi, counts[i], SPACE) for i, (lo, hi) in enumerate(problem.x_extents)]
+    axes += [
+        Axis(lo, hi, counts[problem.ndim_x + i], VELOCITY)
+        for i, (lo, hi) in enumerate(problem.v_extents)
+    ]
+    return GridSpec(tuple(axes), method, dg_order - 1 if method == DG else 0)
+
+
+def initial_value(problem: ProblemSpec, point) -> float:
+    """Pointwise initial distribution (driver.py:147-164)."""
+    eps, k = problem.epsilon, problem.wavenumber
+    if problem.name == "landau2d":
+        x, v = point
+        return (1.0 + eps * math.cos(k * x)) * math.exp(-0.5 * v * v) / math.sqrt(2.0 * math.pi)
+    if problem.name == "landau4d":
+        x1, x2, v1, v2 = point
+        return (1.0 + eps * (math.cos(k * x1) + math.cos(k * x2))) * math.exp(
+            -0.5 * (v1 * v1 + v2 * v2)) / (2.0 * math.pi)
+    d = problem.drift
+    x1, x2, v1, v2 = point
+    if problem.name == "twostream4d":
+        g1 = math.exp(-0.5 * (v1 - d) ** 2) + math.exp(-0.5 * (v1 + d) ** 2)
+        g2 = math.exp(-0.5 * (v2 - d) ** 2) + math.exp(-0.5 * (v2 + d) ** 2)
+        return (1.0 + eps * math.cos(k * x1) * math.cos(k * x2)) * g1 * g2 / (8.0 * math.pi)
+    if problem.name == "twostream4d_baseline":
+        g1 = 0.5 * (math.exp(-0.5 * (v1 - d) ** 2) + math.exp(-0.5 * (v1 + d) ** 2))
+        g2 = math.exp(-0.5 * v2 * v2)
+        return (1.0 + eps * (math.cos(k * x1) + math.cos(k * x2))) * g1 * g2 / (2.0 * math.pi)
+    raise ValueError(f"unknown problem {problem.name!r}")
+
+
+def separable_factors(problem: ProblemSpec, grid: GridSpec):
+    """(g1, g2, space) with f[iv2][iv1][ix2][ix1] = (g2*g1)*space, computed by
+    the same NumPy expressions as the reference broadcast (driver.py:182-198),
+    so the device product is bitwise the reference's initial state."""
+    eps, k = problem.epsilon, problem.wavenumber
+    pts = [grid.axis_points(a) for a in range(grid.ndim)]
+    root = math.sqrt(2.0 * math.pi)
+    if problem.name == "landau2d":
+        space = 1.0 + eps * np.cos(k * pts[0])
+        g1 = np.exp(-0.5 * pts[1] ** 2) / root
+        return g1, np.ones(1), space
+    if problem.name == "landau4d":
+        space = 1.0 + eps * (np.cos(k * pts[1])[:, None] + np.cos(k * pts[0])[None, :])
+        g1 = np.exp(-0.5 * pts[2] ** 2) / root
+        g2 = np.exp(-0.5 * pts[3] ** 2) / root
+        return g1, g2, space
+    d = problem.drift
+    if problem.name == "twostream4d":
+        space = np.cos(k * pts[1])[:, None] * np.cos(k * pts[0])[None, :]
+        space = (1.0 + eps * space) / (8.0 * math.pi)
+        g1 = np.exp(-0.5 * (pts[2] - d) ** 2) + np.exp(-0.5 * (pts[2] + d) ** 2)
+        g2 = np.exp(-0.5 * (pts[3] - d) ** 2) + np.exp(-0.5 * (pts[3] + d) ** 2)
+        return g1, g2, space
+    if problem.name == "twostream4d_baseline":
+        space = 1.0 + eps * (np.cos(k * pts[1])[:, None] + np.cos(k * pts[0])[None, :])
+        g1 = 0.5 * (np.exp(-0.5 * (pts[2] - d) ** 2) + np.exp(-0.5 * (pts[2] + d) ** 2)) / root
+        g2 = np.exp(-0.5 * pts[3] ** 2) / root
+        return g1, g2, space
+    raise ValueError(f"unknown problem {problem.name!r}")
+
+
+def initialize(problem: ProblemSpec, grid: GridSpec, strategy: str | None = None,
+               cache_block: int = 8) -> DistributionField:
+    """Sample the initial distribution on the device (driver.py:167-206)."""
+    if grid.ndim != problem.ndim:
+        raise ValueError(f"grid is {grid.ndim}-dimensional, problem needs {problem.ndim}")
+    g1, g2, space = separable_factors(problem, grid)
+    field = DistributionField.empty(grid, strategy, cache_block)
+    lib = _lib.load()
+    dg1, dg2 = _device.to_device(g1), _device.to_device(g2)
+    dsp = _device.to_device(np.ascontiguousarray(space).ravel())
+    _lib.check(
+        lib.vpb_fill_separable(field.data.data_ptr(), _lib.dims(grid.dims4), dg1.data_ptr(),
+                               dg2.data_ptr(), dsp.data_ptr(), _device.stream()),
+        "vpb_fill_separable",
+    )
+    return field
+
+
+# ---------------------------------------------------------------------------
+# Per-grid step state
+# ---------------------------------------------------------------------------
+class StepState:
+    """Scratch buffers, cached x tables and flag words for one grid."""
+
+    def __init__(self, grid: GridSpec):
+        self.grid = grid
+        dev = _device.device()
+        n = grid.total_dof
+        self.buf = torch.empty(n, dtype=torch.float64, device=dev)
+        self.geom = geometry(grid)
+        nx = self.geom.n1 * self.geom.n2
+        self.nx = nx
+        self.rho = torch.empty(nx, dtype=torch.float64, device=dev)
+        self.e = torch.empty(self.geom.ncomp * nx, dtype=torch.float64, device=dev)
+        self.flags = torch.zeros(8, dtype=torch.int32, device=dev)
+        self.stats = torch.zeros(4, dtype=torch.float64, device=dev)
+        self.flags_host = torch.zeros(8, dtype=torch.int32).pin_memory()
+        self.stats_host = torch.zeros(4, dtype=torch.float64).pin_memory()
+        self.vpoints = [_device.to_device(grid.axis_points(a)) for a in grid.velocity_axes]
+        self._xtab: dict = {}
+        self._vtab: list = [None] * grid.ndim_x
+        d = grid.ndim_x
+        names = ["x"] if d == 1 else ["x1", "x2"]
+        vnames = ["v"] if d == 1 else ["v1", "v2"]
+        self.names = (
+            [f"{x} half (open)" for x in names] + ["field solve"] + [f"{v} full" for v in vnames]
+            + [f"{x} half (close)" for x in names]
+        )
+        lib = _lib.load()
+        self.diag_work = torch.empty(int(lib.vpb_diag_work_len(_lib.dims(grid.dims4))),
+                                     dtype=torch.float64, device=dev)
+        self.diag_out = torch.zeros(8, dtype=torch.float64, device=dev)
+        self.diag_host = torch.zeros(8, dtype=torch.float64).pin_memory()
+        wv = [grid.axis_weights(a) for a in grid.velocity_axes]
+        vsq = [grid.axis_points(a) ** 2 for a in grid.velocity_axes]
+        if d == 1:
+            wv.append(np.ones(1))
+            vsq.append(np.zeros(1))
+        self.wv1, self.wv2 = (_device.to_device(w) for w in wv)
+        self.v1sq, self.v2sq = (_device.to_device(v) for v in vsq)
+
+    def x_tables(self, d: int, tau: float):
+        """Tables for the half x-sweep along space axis d: shift = v_d * (tau/2)."""
+        key = (d, float(tau))
+        tab = self._xtab.get(key)
+        if tab is None:
+            grid = self.grid
+            h = grid.axes[d].h
+            if grid.method == DG:
+                tab = DeviceTables(self.vpoints[d], 0.5 * tau, h, grid.dg_degree)
+            else:
+                tab = self.vpoints[d]
+            if len(self._xtab) > 16:
+                self._xtab.clear()
+            self._xtab[key] = tab
+        return tab
+
+    def v_tables(self, d: int, tau: float):
+        """Tables for the v-sweep along velocity axis d: shift = E_d * tau."""
+        grid = self.grid
+        e_d = self.e[d * self.nx:(d + 1) * self.nx]
+        h = grid.axes[grid.ndim_x + d].h
+        if grid.method != DG:
+            return e_d
+        tab = self._vtab[d]
+        if tab is None:
+            tab = DeviceTables(e_d, tau, h, grid.dg_degree)
+            self._vtab[d] = tab
+        else:
+            tab.refresh(e_d, tau, h)
+        return tab
+
+
+@lru_cache(maxsize=16)
+def _state_cached(grid: GridSpec, device_index: int) -> StepState:
+    return StepState(grid)
+
+
+def step_state(grid: GridSpec) -> StepState:
+    return _state_cached(grid, torch.cuda.current_device())
+
+
+def _sweep_into(state: StepState, axis: int, src, dst, tab, scale: float, flag) -> None:
+    grid = state.grid
+    if grid.method == DG:
+        sweep_dg(grid, axis, src, dst, tab, flag)
+    else:
+        h = grid.axes[axis].h
+        sweep_spline(grid, axis, src, dst, tab, scale, h, flag)
+
+
+def enqueue_step(field: DistributionField, tau: float, state: StepState | None = None,
+                 timer=None) -> None:
+    """Queue one Strang step on the current stream (no host synchronisation).
+
+    Flags and the density mean land in ``state.flags`` / ``state.stats``.
+    ``timer(label)`` (optional) is called before each sub-step kernel group
+    and once with ``None`` at the end; bench.py uses it to bracket kernels
+    with CUDA events.
+    """
+    grid = field.grid
+    st = state or step_state(grid)
+    mark = timer or (lambda label: None)
+    st.flags.zero_()
+    half = 0.5 * tau
+    k = 0
+
+    def sweep(axis: int, tab, scale: float, label: str) -> None:
+        nonlocal k
+        out = st.buf
+        mark(label)
+        _sweep_into(st, axis, field._phys.view(-1), out, tab, scale, st.flags[k:k + 1])
+        st.buf = field._swap(out.view(field._phys.shape)).view(-1)
+        k += 1
+
+    xn = ["x"] if grid.ndim_x == 1 else ["x1", "x2"]
+    vn = ["v"] if grid.ndim_x == 1 else ["v1", "v2"]
+    for d in range(grid.ndim_x):  # _advect_space(tau/2, "open")  driver.py:220-228
+        sweep(d, st.x_tables(d, tau), half, f"sweep_{xn[d]}")
+    mark("density")
+    density_into(field.data, grid, st.rho)  # compute_density  poisson.py:85-95
+    mark("field_solve")
+    solve_into(st.rho, grid, st.e, st.stats, st.flags[k:k + 1])  # solve_poisson
+    k += 1
+    for d in range(grid.ndim_x):  # _advect_velocity(tau)  driver.py:231-242
+        mark(f"tables_{vn[d]}")
+        tab = st.v_tables(d, tau)
+        sweep(grid.ndim_x + d, tab, tau, f"sweep_{vn[d]}")
+    for d in range(grid.ndim_x):  # _advect_space(tau/2, "close")
+        sweep(d, st.x_tables(d, tau), half, f"sweep_{xn[d]}")
+    mark(None)
+
+
+def check_step(state: StepState, time_label: float | None) -> None:
+    """Read the step's flags (one D2H + sync) and raise / warn like the reference."""
+    state.flags_host.copy_(state.flags, non_blocking=True)
+    state.stats_host.copy_(state.stats, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    flags = state.flags_host.numpy()
+    _warn_if_not_neutral(float(state.stats_host[0]))
+    for k, name in enumerate(state.names):
+        if flags[k]:
+            raise SubstepError(name, time_label)
+
+
+def strang_step(field: DistributionField, tau: float, workers: int = 1, consume: bool = False,
+                time_label: float | None = None) -> DistributionField:
+    """Advance by one Strang step of size tau (driver.py:245-265).
+
+    ``workers`` is the reference's CPU thread count; it has no effect here.
+    """
+    work = field if consume else field.copy()
+    st = step_state(work.grid)
+    enqueue_step(work, tau, st)
+    check_step(st, time_label)
+    return work
+
+
+@dataclass(frozen=True)
+class DiagnosticsRecord:
+    time: float
+    electric_energy: float
+    mass: float
+    l1_norm: float
+    l2_norm: float
+    kinetic_energy: float
+    total_energy: float
+
+
+def enqueue_diagnostics(field: DistributionField, st: StepState, e: torch.Tensor | None,
+                        stats: torch.Tensor | None) -> None:
+    grid = field.grid
+    if e is None:
+        density_into(field.data, grid, st.rho)
+        solve_into(st.rho, grid, st.e, stats, None)
+        e = st.e
+    lib = _lib.load()
+    _lib.check(
+        lib.vpb_diagnostics(field.data.data_ptr(), _lib.dims(grid.dims4),
+                            st.geom.tensors["wx"].data_ptr(), st.wv1.data_ptr(),
+                            st.wv2.data_ptr(), st.v1sq.data_ptr(), st.v2sq.data_ptr(),
+                            e.data_ptr(), st.geom.ncomp, st.diag_out.data_ptr(),
+                            st.diag_work.data_ptr(), _device.stream()),
+        "vpb_diagnostics",
+    )
+
+
+def diagnostics(field: DistributionField, time: float = 0.0,
+                efield: ElectricField | None = None) -> DiagnosticsRecord:
+    """Conserved quantities (driver.py:279-316), computed on the device."""
+    grid = field.grid
+    st = step_state(grid)
+    e = None
+    if efield is not None:
+        e = torch.cat([_device_x(grid, c) for c in efield.components])
+    stats = st.diag_out[5:6]
+    enqueue_diagnostics(field, st, e, stats if e is None else None)
+    st.diag_host.copy_(st.diag_out, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    v = st.diag_host.numpy().copy()
+    if e is None:
+        _warn_if_not_neutral(float(v[5]))
+    mass, l1, l2sq, kin, ee = (float(x) for x in v[:5])
+    return DiagnosticsRecord(
+        time=float(time),
+        electric_energy=ee,
+        mass=mass,
+        l1_norm=l1,
+        l2_norm=float(math.sqrt(max(l2sq, 0.0))),
+        kinetic_energy=kin,
+        total_energy=kin + ee,
+    )
+
+
+@dataclass(frozen=True)
+class RunConfig:
+    problem: ProblemSpec
+    grid: GridSpec
+    tau: float
+    t_end: float
+    layout: str | None = None
+    cache_block: int = 8
+    workers: int = 1
+    diag_every: int = 1
+    snapshot_times: tuple = ()
+    snapshot_stem: str | None = None
+
+
+def _steps_for(t: float, tau: float) -> int:
+    m = round(t / tau)
+    if abs(m * tau - t) > 1e-9 * max(1.0, abs(t)):
+        raise ValueError(f"time {t} is not an integer multiple of tau={tau}")
+    return m
+
+
+def run(config: RunConfig):
+    """Run to t_end with diagnostics and snapshots (driver.py:341-378)."""
+    if config.tau <= 0.0:
+        raise ValueError("tau must be positive")
+    if config.t_end < 0.0:
+        raise ValueError("t_end must be non-negative")
+    if config.diag_every < 1 or config.workers < 1:
+        raise ValueError("diag_every and workers must be >= 1")
+    nsteps = _steps_for(config.t_end, config.tau)
+    snap_at: dict[int, float] = {}
+    for t in config.snapshot_times:
+        m = _steps_for(float(t), config.tau)
+        if not 0 <= m <= nsteps:
+            raise ValueError(f"snapshot time {t} outside [0, t_end]")
+        snap_at[m] = float(t)
+
+    field = initialize(config.problem, config.grid, strategy=config.layout,
+                       cache_block=config.cache_block)
+    records = [diagnostics(field, time=0.0)]
+    snapshots: list = []
+
+    def capture(t: float) -> None:
+        copy = field.copy()
+        snapshots.append((t, copy))
+        if config.snapshot_stem is not None:
+            write_snapshot(copy, f"{config.snapshot_stem}_t{t:g}.vlf")
+
+    if 0 in snap_at:
+        capture(0.0)
+    for m in range(1, nsteps + 1):
+        t = m * config.tau
+        field = strang_step(field, config.tau, workers=config.workers, consume=True, time_label=t)
+        if m % config.diag_every == 0:
+            records.append(diagnostics(field, time=t))
+        if m in snap_at:
+            capture(snap_at[m])
+    return records, snapshots
+
+
+__all__ = [
+    "DEFAULT_STRATEGY",
+    "LayoutDescriptor",
+    "SubstepError",
+    "ProblemSpec",
+    "problem_spec",
+    "parse_method",
+    "method_label",
+    "make_grid",
+    "initial_value",
+    "initialize",
+    "strang_step",
+    "DiagnosticsRecord",
+    "diagnostics",
+    "RunConfig",
+    "run",
+]

@@ -1,0 +1,263 @@
+"""Step-level parity of the device Strang step against the reference.
+
+North-star bars (BASELINE.json): per-step max relative error in f <= 1e-12,
+electric-energy series within 1e-10 relative, mass conserved to 1e-13.
+Runs on the B200 box: ``pytest -m gpu``.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1803_02143_b200 as vpb
+from oracle import core
+from paper_1803_02143_b200 import driver
+from tests.conftest import max_rel
+
+pytestmark = pytest.mark.gpu
+
+F_TOL = 1e-12
+EE_TOL = 1e-10
+MASS_TOL = 1e-13
+
+STEP_CASES = [
+    ("landau4d_dg3", "landau4d", "dg", 12, 3, 0.1),
+    ("landau4d_dg4", "landau4d", "dg", 16, 4, 0.1),
+    ("landau4d_spline", "landau4d", "spline", 12, 0, 0.1),
+    ("twostream_dg2", "twostream4d_baseline", "dg", 12, 2, 0.1),
+    ("twostream_ref_dg3", "twostream4d", "dg", 12, 3, 0.1),
+    ("landau2d_dg4", "landau2d", "dg", 32, 4, 0.1),
+    ("landau2d_spline", "landau2d", "spline", 32, 0, 0.1),
+]
+KEYS = ("time", "electric_energy", "mass", "l1_norm", "l2_norm", "kinetic_energy", "total_energy")
+
+
+@pytest.mark.parametrize("tag,prob,method,dofs,order,tau", STEP_CASES)
+def test_steps_match_reference_golden(golden, tag, prob, method, dofs, order, tau):
+    z = golden("steps")
+    states, recs = z[tag + "_f"], z[tag + "_rec"]
+    problem = vpb.problem_spec(prob)
+    grid = vpb.make_grid(problem, method, dofs, dg_order=order)
+    field = vpb.initialize(problem, grid)
+    assert np.array_equal(field.numpy(), states[0])
+    for m in range(1, states.shape[0]):
+        field = vpb.strang_step(field, tau, consume=True)
+        assert max_rel(field.numpy(), states[m]) <= F_TOL, (tag, m)
+        rec = vpb.diagnostics(field, m * tau)
+        ee_ref = recs[m][1]
+        assert abs(rec.electric_energy - ee_ref) <= EE_TOL * abs(ee_ref), (tag, m)
+        for k, ref in zip(KEYS, recs[m]):
+            assert getattr(rec, k) == pytest.approx(ref, rel=1e-11), (tag, m, k)
+
+
+def _oracle_run(prob, method, dofs, order, tau, nsteps):
+    og = core.make_grid(prob, method, dofs, order)
+    f = core.initialize(prob, og)
+    for _ in range(nsteps):
+        f = core.strang_step(f, og, tau)
+        yield f, og
+
+
+def test_config1_parity_20_steps(golden):
+    """BASELINE config 1: Landau 4D, 16^4 cells, degree 2, dt=0.1, 20 steps.
+    f per step vs the live oracle (bitwise-pinned to the reference), EE and
+    mass series vs the reference's own series."""
+    z = golden("series")
+    recs, sums = z["cfg1_rec"], z["cfg1_sums"]
+    problem = vpb.problem_spec("landau4d")
+    grid = vpb.make_grid(problem, "dg", 48, dg_order=3)
+    field = vpb.initialize(problem, grid)
+    rec0 = vpb.diagnostics(field, 0.0)
+    m0 = rec0.mass
+    worst = 0.0
+    for m, (ref, _) in enumerate(_oracle_run("landau4d", "dg", 48, 3, 0.1, 20), start=1):
+        field = vpb.strang_step(field, 0.1, consume=True, time_label=m * 0.1)
+        got = field.numpy()
+        err = max_rel(got, ref)
+        worst = max(worst, err)
+        assert err <= F_TOL, (m, err)
+        np.testing.assert_allclose([got.sum(), (got * got).sum(), np.abs(got).max()],
+                                   sums[m - 1], rtol=1e-12)
+        rec = vpb.diagnostics(field, m * 0.1)
+        assert abs(rec.electric_energy - recs[m][1]) <= EE_TOL * abs(recs[m][1]), m
+        assert abs(rec.mass - m0) <= MASS_TOL * m0, m
+    print(f"config1 worst per-step max-rel error in f: {worst:.3e}")
+
+
+@pytest.mark.parametrize("tag,prob,method,dofs,order,nsteps", [
+    ("cfg3_small", "twostream4d_baseline", "dg", 32, 2, 20),
+    ("cfg4_small", "landau4d", "spline", 32, 0, 10),
+])
+def test_reduced_configs_energy_series(golden, tag, prob, method, dofs, order, nsteps):
+    z = golden("series")
+    recs = z[tag + "_rec"]
+    problem = vpb.problem_spec(prob)
+    grid = vpb.make_grid(problem, method, dofs, dg_order=order)
+    field = vpb.initialize(problem, grid)
+    m0 = vpb.diagnostics(field).mass
+    for m in range(1, nsteps + 1):
+        field = vpb.strang_step(field, 0.1, consume=True)
+        rec = vpb.diagnostics(field, m * 0.1)
+        assert abs(rec.electric_energy - recs[m][1]) <= EE_TOL * abs(recs[m][1]), (tag, m)
+        assert abs(rec.mass - m0) <= MASS_TOL * abs(m0) * 10, (tag, m)
+
+
+def test_run_loop_records_and_snapshots(tmp_path):
+    prob = vpb.problem_spec("landau4d")
+    grid = vpb.make_grid(prob, "dg", 12, dg_order=3)
+    cfg = vpb.RunConfig(problem=prob, grid=grid, tau=0.1, t_end=0.5, snapshot_times=(0.0, 0.3),
+                        snapshot_stem=str(tmp_path / "snap"), diag_every=2)
+    records, snaps = vpb.run(cfg)
+    np.testing.assert_allclose([r.time for r in records], [0.0, 0.2, 0.4], atol=1e-12)
+    assert [t for t, _ in snaps] == [0.0, 0.3]
+    assert (tmp_path / "snap_t0.vlf").exists() and (tmp_path / "snap_t0.3.vlf").exists()
+    back = vpb.read_snapshot(tmp_path / "snap_t0.3.vlf")
+    assert np.array_equal(back.numpy(), snaps[1][1].numpy())
+    with pytest.raises(ValueError):
+        vpb.run(vpb.RunConfig(problem=prob, grid=grid, tau=0.1, t_end=0.25))
+
+
+def test_run_is_deterministic_and_strategy_independent():
+    prob = vpb.problem_spec("landau4d")
+    grid = vpb.make_grid(prob, "dg", 24, dg_order=3)
+    outs = []
+    for strategy in ("strided", "transpose", "strided"):
+        f = vpb.initialize(prob, grid, strategy=strategy)
+        for _ in range(3):
+            f = vpb.strang_step(f, 0.1, consume=True)
+        outs.append(f.numpy())
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+
+
+def test_step_without_consume_leaves_input():
+    prob = vpb.problem_spec("landau4d")
+    grid = vpb.make_grid(prob, "spline", 12)
+    f = vpb.initialize(prob, grid)
+    before = f.numpy()
+    g = vpb.strang_step(f, 0.1)
+    assert np.array_equal(f.numpy(), before)
+    assert not np.array_equal(g.numpy(), before)
+
+
+def test_step_reports_first_nonfinite_substep():
+    prob = vpb.problem_spec("landau4d")
+    grid = vpb.make_grid(prob, "spline", 8)
+    f = vpb.initialize(prob, grid)
+    f.array[0, 0, 0, 0] = math.inf
+    with pytest.raises(vpb.SubstepError, match="x1 half"):
+        vpb.strang_step(f, 0.1)
+    two = vpb.problem_spec("landau2d")
+    g2 = vpb.make_grid(two, "dg", 16, dg_order=2)
+    f2 = vpb.initialize(two, g2)
+    f2.array[3, 3] = math.nan
+    with pytest.raises(vpb.SubstepError, match=r"sub-step 'x half \(open\)' at t=0\.1"):
+        vpb.strang_step(f2, 0.1, time_label=0.1)
+
+
+def test_step_reports_broken_field_solve(monkeypatch):
+    prob = vpb.problem_spec("landau4d")
+    grid = vpb.make_grid(prob, "dg", 12, dg_order=3)
+    f = vpb.initialize(prob, grid)
+    real = driver.solve_into
+
+    def poisoned(rho, grid_, e, stats, flag):
+        real(rho, grid_, e, stats, flag)
+        e.fill_(math.nan)
+        if flag is not None:
+            flag.fill_(1)
+
+    monkeypatch.setattr(driver, "solve_into", poisoned)
+    with pytest.raises(vpb.SubstepError, match="field solve"):
+        vpb.strang_step(f, 0.1)
+
+
+def test_identity_without_field():
+    flat = vpb.ProblemSpec("landau4d", ((0.0, 4 * math.pi),) * 2, ((-6.0, 6.0),) * 2, 0.0, 0.5)
+    grid = vpb.make_grid(flat, "dg", 16, dg_order=4)
+    before = vpb.initialize(flat, grid)
+    after = vpb.strang_step(before, 0.1)
+    scale = np.abs(before.numpy()).max()
+    assert np.abs(after.numpy() - before.numpy()).max() <= 1e-13 * scale
+
+
+def test_dg_l2_norm_never_grows():
+    prob = vpb.problem_spec("landau4d")
+    grid = vpb.make_grid(prob, "dg", 24, dg_order=3)
+    f = vpb.initialize(prob, grid)
+    vals = [vpb.diagnostics(f).l2_norm]
+    for _ in range(5):
+        f = vpb.strang_step(f, 0.1, consume=True)
+        vals.append(vpb.diagnostics(f).l2_norm)
+    assert all(c <= p * (1 + 1e-12) for p, c in zip(vals, vals[1:]))
+
+
+# ---- reference kernel-test mirrors (per-line API) -------------------------
+@pytest.mark.parametrize("m", [2, -3, 8, -11])
+def test_advect_whole_cell_shift_rolls_bitwise(m):
+    rng = np.random.default_rng(50 + abs(m))
+    line = rng.standard_normal(8 * 4)
+    out = vpb.advect_line_dg(line, m * 0.5, 0.5, 3)
+    assert np.array_equal(out, np.roll(line.reshape(8, 4), m, axis=0).ravel())
+
+
+def test_advect_near_integer_and_constants_and_mass():
+    rng = np.random.default_rng(53)
+    line = rng.standard_normal(32)
+    out = vpb.advect_line_dg(line, -3 * 0.7, 0.7, 3)
+    assert np.abs(out - np.roll(line.reshape(8, 4), -3, axis=0).ravel()).max() <= 1e-12
+    for degree in range(4):
+        out = vpb.advect_line_dg(np.full(6 * (degree + 1), 2.5), 0.213, 0.5, degree)
+        np.testing.assert_allclose(out, 2.5, rtol=1e-13)
+    for seed in range(5):
+        r = np.random.default_rng(700 + seed)
+        degree = int(r.integers(0, 4))
+        line = r.standard_normal(8 * (degree + 1))
+        shift = float(r.uniform(-5, 5))
+        _, w = vpb.gauss_nodes(degree + 1)
+        mass = lambda v: float(w @ v.reshape(8, -1).T @ np.ones(8))  # noqa: E731
+        out = vpb.advect_line_dg(line, shift, 1.0, degree)
+        assert abs(mass(out) - mass(line)) <= 1e-12 * max(1.0, abs(mass(line)))
+    with pytest.raises(ValueError):
+        vpb.advect_line_dg(np.ones(7), 0.1, 1.0, 1)
+
+
+@pytest.mark.parametrize("m", [1, 3, -2, 13, -45])
+def test_spline_integer_shift_is_circular(m):
+    rng = np.random.default_rng(400 + abs(m))
+    u = rng.standard_normal(16)
+    out = vpb.advect_line_spline(u, m * 0.3, 0.3)
+    assert np.abs(out - np.roll(u, m)).max() <= 1e-13 * np.abs(u).max()
+
+
+def test_spline_line_sum_and_wrap_and_symbol():
+    for seed in range(5):
+        r = np.random.default_rng(900 + seed)
+        u = r.standard_normal(48)
+        out = vpb.advect_line_spline(u, float(r.uniform(-20, 20)), 0.2)
+        assert abs(out.sum() - u.sum()) <= 1e-12 * max(1.0, abs(u.sum()))
+    u = np.random.default_rng(17).standard_normal(16)
+    base = vpb.advect_line_spline(u, 1.3, 0.5)
+    assert np.abs(base - vpb.advect_line_spline(u, 1.3 + 7 * 8.0, 0.5)).max() <= 1e-11
+    n = 32
+    x = np.arange(n)
+    for mode in range(n):
+        re = vpb.advect_line_spline(np.cos(2 * np.pi * mode * x / n), 0.37, 1.0)
+        im = vpb.advect_line_spline(np.sin(2 * np.pi * mode * x / n), 0.37, 1.0)
+        assert np.sqrt(re ** 2 + im ** 2).max() <= 1.0 + 1e-12
+
+
+def test_plugin_entry_points_with_torch_current_stream():
+    """The step runs on torch's current stream (side stream honoured)."""
+    prob = vpb.problem_spec("landau4d")
+    grid = vpb.make_grid(prob, "dg", 12, dg_order=3)
+    ref = vpb.strang_step(vpb.initialize(prob, grid), 0.1).numpy()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        f = vpb.initialize(prob, grid)
+        g = vpb.strang_step(f, 0.1)
+        got = g.numpy()
+    assert np.array_equal(got, ref)
