@@ -19,7 +19,7 @@ import paper_1803_02143_b200 as vpb
 from oracle import core
 from paper_1803_02143_b200 import _device, _lib, kernels
 from paper_1803_02143_b200 import dg as vdg
-from tests.conftest import max_rel
+from vpb_testutil import max_rel
 
 pytestmark = pytest.mark.gpu
 

@@ -16,7 +16,7 @@ import torch
 import paper_1803_02143_b200 as vpb
 from oracle import core
 from paper_1803_02143_b200 import driver
-from tests.conftest import max_rel
+from vpb_testutil import max_rel
 
 pytestmark = pytest.mark.gpu
 
