@@ -159,10 +159,13 @@ def test_dg_axis_sweep_bitwise(order, axis):
     dst = torch.empty_like(src.data)
     flag = torch.zeros(1, dtype=torch.int32, device="cuda")
     lib = _lib.load()
+    # keep the tables referenced: only raw pointers cross the ABI
+    da, db = dev(a[perm]), dev(b[perm])
+    dq, dal = dev(q[perm], torch.int64), dev(al[perm])
     _lib.check(lib.vpb_dg_sweep_axis(axis, src.data.data_ptr(), dst.data_ptr(),
-                                     _lib.dims(grid.dims4), order, dev(a[perm]).data_ptr(),
-                                     dev(b[perm]).data_ptr(), dev(q[perm], torch.int64).data_ptr(),
-                                     dev(al[perm]).data_ptr(), flag.data_ptr(), _device.stream()),
+                                     _lib.dims(grid.dims4), order, da.data_ptr(), db.data_ptr(),
+                                     dq.data_ptr(), dal.data_ptr(), flag.data_ptr(),
+                                     _device.stream()),
                "sweep")
     got = dst.view(src._phys.shape).permute(3, 2, 1, 0).cpu().numpy()
     assert np.array_equal(got, ref)
