@@ -252,12 +252,19 @@ __device__ __forceinline__ void sts_cell(double* p, const double (&u)[P]) {
 }
 
 // ---------------------------------------------------------------------------
-// K1: contiguous-axis sweep.  Block = `rows_per_block` consecutive rows,
-// processed in chunks of R rows; chunk k+2 is in flight while chunk k is
-// computed.  Thread layout inside a chunk: cpp cells x rpp rows.
+// K1: contiguous-axis sweep.  A persistent CTA owns `rows_per_block`
+// consecutive rows (whole (iv2, iv1) planes in the product layout, so the
+// projection coefficients stay in registers) and streams them through
+// shared memory in chunks of R rows: kStages bulk-async loads (TMA 1-D
+// bulk copies completing on mbarriers) are in flight while one chunk is
+// computed, and results leave through double-buffered bulk stores.  One
+// __syncthreads per chunk.  Thread layout inside a chunk: cpp cells x rpp
+// rows.
 // ---------------------------------------------------------------------------
+constexpr int kStages = 4;
+
 template <int P>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 2)
     dg_rows_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t nrows, int C,
                    int64_t rows_per_block, int R, int cpp, int rpp,
                    const int64_t* __restrict__ idx, int64_t tdiv, int64_t tmod,
@@ -268,32 +275,32 @@ __global__ void __launch_bounds__(256)
   const int n = C * P;
   const int chunk = R * n;
   double* inb = reinterpret_cast<double*>(smem_raw);
-  double* outb = inb + 2 * chunk;
+  double* outb = inb + kStages * chunk;
   uint64_t* bars = reinterpret_cast<uint64_t*>(outb + 2 * chunk);
 
   const int tid = threadIdx.x;
   const int64_t r_begin = blockIdx.x * rows_per_block;
   const int64_t r_end = min(nrows, r_begin + rows_per_block);
+  if (r_begin >= r_end) return;
   const int nchunks = (int)((r_end - r_begin + R - 1) / R);
 
   auto issue_load = [&](int kc) {
     int64_t r0 = r_begin + (int64_t)kc * R;
     int rows = (int)min((int64_t)R, r_end - r0);
     uint32_t bytes = (uint32_t)rows * n * 8u;
-    uint64_t* bar = bars + (kc & 1);
+    uint64_t* bar = bars + (kc % kStages);
     mbar_arrive_expect_tx(bar, bytes);
-    bulk_g2s(inb + (kc & 1) * chunk, src + r0 * n, bytes, bar);
+    bulk_g2s(inb + (kc % kStages) * chunk, src + r0 * n, bytes, bar);
   };
 
   if (tid == 0) {
-    mbar_init(bars + 0, 1);
-    mbar_init(bars + 1, 1);
+#pragma unroll
+    for (int s = 0; s < kStages; ++s) mbar_init(bars + s, 1);
     fence_mbar_init();
   }
   __syncthreads();
   if (tid == 0) {
-    issue_load(0);
-    if (nchunks > 1) issue_load(1);
+    for (int s = 0; s < kStages && s < nchunks; ++s) issue_load(s);
   }
 
   const bool active = tid < cpp * rpp;
@@ -307,14 +314,12 @@ __global__ void __launch_bounds__(256)
   bool bad = false;
 
   for (int kc = 0; kc < nchunks; ++kc) {
-    const int s = kc & 1;
+    const int s = kc % kStages;
     const int64_t r0 = r_begin + (int64_t)kc * R;
     const int rows = (int)min((int64_t)R, r_end - r0);
-    if (tid == 0) bulk_wait_read<1>();  // the store issued two chunks ago released outb[s]
-    __syncthreads();
-    mbar_wait(bars + s, (kc >> 1) & 1);
+    mbar_wait(bars + s, (kc / kStages) & 1);
     const double* in = inb + s * chunk;
-    double* out = outb + s * chunk;
+    double* out = outb + (kc & 1) * chunk;
     if (active) {
       for (int r = rr0; r < rows; r += rpp) {
         const int64_t grow = r0 + r;
@@ -348,11 +353,14 @@ __global__ void __launch_bounds__(256)
       }
     }
     fence_proxy_async_smem();
+    // the store of chunk kc-1 must have finished reading outb[(kc+1)&1]
+    // before anyone computes chunk kc+1 into it
+    if (tid == 0) bulk_wait_read<0>();
     __syncthreads();
     if (tid == 0) {
       bulk_s2g(dst + r0 * n, out, (uint32_t)rows * n * 8u);
       bulk_commit();
-      if (kc + 2 < nchunks) issue_load(kc + 2);
+      if (kc + kStages < nchunks) issue_load(kc + kStages);
     }
   }
   if (tid == 0) bulk_wait<0>();
@@ -461,10 +469,11 @@ __global__ void __launch_bounds__(256)
   if (lo < 0) lo += C;
   vec_t prev[P];
   ld(lo, prev);
-#pragma unroll 2
-  for (int c = 0; c < C; ++c) {
-    vec_t cur[P], res[P];
-    ld(up, cur);
+  // G source cells are loaded back to back before any of them is used, so
+  // each thread keeps G*P independent loads in flight.
+  constexpr int G = (VEC == 2 || P > 4) ? 2 : 4;
+  auto step = [&](int c, const vec_t (&cur)[P]) {
+    vec_t res[P];
     if constexpr (VEC == 2) {
       double l0[P], u0[P], r0[P], l1[P], u1[P], r1[P];
 #pragma unroll
@@ -489,7 +498,23 @@ __global__ void __launch_bounds__(256)
     st(c, res);
 #pragma unroll
     for (int m = 0; m < P; ++m) prev[m] = cur[m];
+  };
+  int c = 0;
+  for (; c + G <= C; c += G) {
+    vec_t cur[G][P];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      ld(up, cur[g]);
+      if (++up == C) up = 0;
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) step(c + g, cur[g]);
+  }
+  for (; c < C; ++c) {
+    vec_t cur[P];
+    ld(up, cur);
     if (++up == C) up = 0;
+    step(c, cur);
   }
   report_flag(bad, flag);
 }
@@ -519,6 +544,19 @@ __global__ void gather4d_kernel(const double* __restrict__ view, double* __restr
 // ---------------------------------------------------------------------------
 // Host-side launchers
 // ---------------------------------------------------------------------------
+static int sm_count() {
+  static int cached[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (cached[dev] == 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = v > 0 ? v : 148;
+  }
+  return cached[dev];
+}
+
 struct RowsArgs {
   const double* src;
   double* dst;
@@ -546,27 +584,29 @@ static int launch_rows(const RowsArgs& g, cudaStream_t st) {
         g.src, g.dst, g.nrows, g.C, g.idx, g.tdiv, g.tmod, g.a, g.b, g.q, g.alpha, g.flag);
     return check_launch("dg_rows_simple_kernel");
   }
-  const int target_bytes = 8192;
+  const int target_bytes = 12288;
   int R = (int)std::max<int64_t>(1, target_bytes / (n * 8));
-  int64_t rpb = g.rows_per_block;
-  if (rpb <= 0) rpb = (int64_t)R * 8;
-  if (R > rpb) R = (int)rpb;
+  int64_t unit = g.rows_per_block > 0 ? g.rows_per_block : R;  // rows that share coefficients
   int cpp = std::min(g.C, 256);
   int rpp = std::max(1, 256 / g.C);
   if (rpp > R) rpp = R;
   int threads = cpp * rpp;
   threads = ((threads + 31) / 32) * 32;
-  size_t smem = (size_t)4 * R * n * sizeof(double) + 2 * sizeof(uint64_t);
-  if (smem > 200 * 1024) {
+  size_t smem = (size_t)(kStages + 2) * R * n * sizeof(double) + kStages * sizeof(uint64_t);
+  if (smem > 110 * 1024) {
     set_error("dg row of %d dofs does not fit the shared-memory pipeline", n);
     return VPB_ERR_UNSUPPORTED;
   }
   static bool attr_set[kMaxOrder + 1] = {};
   if (!attr_set[P]) {
     cudaFuncSetAttribute(dg_rows_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
+                         110 * 1024);
     attr_set[P] = true;
   }
+  // persistent grid: 2 CTAs per SM, each owning a contiguous run of units
+  int64_t units = (g.nrows + unit - 1) / unit;
+  int64_t grid = std::min<int64_t>(units, 2 * (int64_t)sm_count());
+  int64_t rpb = ((units + grid - 1) / grid) * unit;
   int64_t blocks = (g.nrows + rpb - 1) / rpb;
   dg_rows_kernel<P><<<(unsigned)blocks, threads, smem, st>>>(
       g.src, g.dst, g.nrows, g.C, rpb, R, cpp, rpp, g.idx, g.tdiv, g.tmod, g.a, g.b, g.q,
@@ -706,9 +746,7 @@ extern "C" int vpb_dg_sweep_axis(int32_t axis, const double* src, double* dst,
     // rows = (iv2, iv1, ix2); table row = iv1.  A block spans whole
     // (iv2, iv1) planes so its coefficients stay in registers.
     int64_t nrows = n2 * nv1 * nv2;
-    int64_t rpb = n2;
-    int64_t plane_bytes = n2 * n1 * 8;
-    if (plane_bytes < 65536) rpb = n2 * std::max<int64_t>(1, 65536 / std::max<int64_t>(plane_bytes, 1));
+    int64_t rpb = n2;  // one (iv2, iv1) plane shares its coefficients
     RowsArgs g{src, dst, nrows, C, rpb, nullptr, n2, nv1, a, b, q, alpha, flag};
     VPB_DISPATCH_ORDER(order, launch_rows, g, st);
   }
