@@ -96,6 +96,18 @@ int vpb_dg_sweep_axis(int32_t axis, const double* src, double* dst, const int64_
                       int32_t order, const double* a, const double* b, const int64_t* q,
                       const double* alpha, int32_t* flag, void* stream);
 
+/* Both space sweeps of a Strang half step, x1 then x2, in ONE pass over f
+ * (driver.py:220-228 _advect_space): per (iv2, iv1) plane the x1 tables use
+ * row iv1 and the x2 tables row iv2.  Bitwise equal to vpb_dg_sweep_axis(0)
+ * followed by vpb_dg_sweep_axis(1); half the HBM traffic.  flag1/flag2 get
+ * the non-finite reports of the x1 and x2 results.  Needs a 2x2v field with
+ * dims[0]*order even. */
+int vpb_dg_sweep_xplane(const double* src, double* dst, const int64_t dims[4], int32_t order,
+                        const double* a1, const double* b1, const int64_t* q1,
+                        const double* alpha1, const double* a2, const double* b2,
+                        const int64_t* q2, const double* alpha2, int32_t* flag1,
+                        int32_t* flag2, void* stream);
+
 /* One spline sweep along `axis`; shift of line = values[table row]*scale. */
 int vpb_spline_sweep_axis(int32_t axis, const double* src, double* dst, const int64_t dims[4],
                           const double* values, double scale, double h, int32_t* flag,

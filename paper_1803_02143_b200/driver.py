@@ -25,7 +25,7 @@ import numpy as np
 import torch
 
 from . import _device, _lib
-from .dg import DeviceTables, sweep_dg
+from .dg import DeviceTables, sweep_dg, xplane_dg
 from .field import DEFAULT_STRATEGY, DistributionField, LayoutDescriptor, write_snapshot
 from .grid import DG, SPACE, SPLINE, VELOCITY, Axis, GridSpec
 from .poisson import (
@@ -38,6 +38,11 @@ from .poisson import (
     solve_into,
 )
 from .spline import sweep_spline
+
+
+# Fused x1+x2 plane sweeps (set False to run the two sweeps separately; the
+# results are bitwise identical either way).
+FUSE_X = True
 
 
 class SubstepError(RuntimeError):
@@ -235,6 +240,9 @@ class StepState:
             [f"{x} half (open)" for x in names] + ["field solve"] + [f"{v} full" for v in vnames]
             + [f"{x} half (close)" for x in names]
         )
+        # both x sweeps of a half step in one pass (bitwise-identical result)
+        self.fused_x = (grid.method == DG and grid.ndim == 4
+                        and (grid.dof(0) * grid.order) % 2 == 0 and FUSE_X)
         lib = _lib.load()
         self.diag_work = torch.empty(int(lib.vpb_diag_work_len(_lib.dims(grid.dims4))),
                                      dtype=torch.float64, device=dev)
@@ -322,10 +330,22 @@ def enqueue_step(field: DistributionField, tau: float, state: StepState | None =
         st.buf = field._swap(out.view(field._phys.shape)).view(-1)
         k += 1
 
+    def advect_space() -> None:  # _advect_space(tau/2)  driver.py:220-228
+        nonlocal k
+        if st.fused_x:
+            out = st.buf
+            mark("sweep_x12")
+            xplane_dg(grid, field._phys.view(-1), out, st.x_tables(0, tau), st.x_tables(1, tau),
+                      st.flags[k:k + 1], st.flags[k + 1:k + 2])
+            st.buf = field._swap(out.view(field._phys.shape)).view(-1)
+            k += 2
+            return
+        for d in range(grid.ndim_x):
+            sweep(d, st.x_tables(d, tau), half, f"sweep_{xn[d]}")
+
     xn = ["x"] if grid.ndim_x == 1 else ["x1", "x2"]
     vn = ["v"] if grid.ndim_x == 1 else ["v1", "v2"]
-    for d in range(grid.ndim_x):  # _advect_space(tau/2, "open")  driver.py:220-228
-        sweep(d, st.x_tables(d, tau), half, f"sweep_{xn[d]}")
+    advect_space()  # "open"
     mark("density")
     density_into(field.data, grid, st.rho)  # compute_density  poisson.py:85-95
     mark("field_solve")
@@ -335,8 +355,7 @@ def enqueue_step(field: DistributionField, tau: float, state: StepState | None =
         mark(f"tables_{vn[d]}")
         tab = st.v_tables(d, tau)
         sweep(grid.ndim_x + d, tab, tau, f"sweep_{vn[d]}")
-    for d in range(grid.ndim_x):  # _advect_space(tau/2, "close")
-        sweep(d, st.x_tables(d, tau), half, f"sweep_{xn[d]}")
+    advect_space()  # "close"
     mark(None)
 
 

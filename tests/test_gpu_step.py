@@ -261,3 +261,31 @@ def test_plugin_entry_points_with_torch_current_stream():
         g = vpb.strang_step(f, 0.1)
         got = g.numpy()
     assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("order,dofs", [(3, (24, 18, 12, 15)), (2, (16, 12, 8, 10)),
+                                        (4, (16, 20, 12, 8)), (1, (12, 10, 8, 6))])
+def test_fused_x_planes_bitwise_equal_to_separate_sweeps(monkeypatch, order, dofs):
+    """vpb_dg_sweep_xplane == x1 sweep then x2 sweep, bit for bit, over steps."""
+    prob = vpb.problem_spec("landau4d")
+    grid = vpb.make_grid(prob, "dg", dofs, dg_order=order)
+    outs = []
+    for fused in (False, True):
+        monkeypatch.setattr(driver, "FUSE_X", fused)
+        driver._state_cached.cache_clear()
+        f = vpb.initialize(prob, grid)
+        for _ in range(3):
+            f = vpb.strang_step(f, 0.37, consume=True)
+        assert driver.step_state(grid).fused_x == fused
+        outs.append(f.numpy())
+    driver._state_cached.cache_clear()
+    assert np.array_equal(outs[0], outs[1])
+
+
+def test_fused_x_reports_nonfinite_in_x1_and_x2():
+    prob = vpb.problem_spec("landau4d")
+    grid = vpb.make_grid(prob, "dg", 12, dg_order=3)
+    f = vpb.initialize(prob, grid)
+    f.array[5, 6, 7, 8] = math.nan
+    with pytest.raises(vpb.SubstepError, match=r"x1 half \(open\)"):
+        vpb.strang_step(f, 0.1)
