@@ -3,21 +3,25 @@
 // In the reference, _advect_space (driver.py:220-228) sweeps x1 and then x2,
 // each a full read+write of f.  Inside one (iv2, iv1) plane both shifts are
 // constant (x1 shift from v1, x2 shift from v2), so the plane can be swept
-// along x1 and then x2 while it streams through shared memory:
+// along x1 and then x2 while it streams through shared memory.  Output x2
+// cell c reads the x1-swept values g of source x2 cells c-q2-1 and c-q2, so
+// the plane is consumed in source order starting at s0 = (-q2-1) mod C2:
 //
-//   for every source x2-cell s of the plane (in the order the x2 stencil
-//   consumes them, starting at (-q2-1) mod C2, one extra to close the wrap):
-//     TMA-bulk-load the p rows of cell s into shared memory
-//     g(s)   = x1 sweep of those rows                 (registers)
-//     out    = A2 g(s-1) + B2 g(s)  -> x2-cell s+q2   (shared -> bulk store)
+//   chunk 0 of a plane:  source cells s0 .. s0+n   -> output cells 0 .. n-1
+//   chunk i > 0:         source cells s0+1+iG ...  -> output cells iG ...
+//   per source cell s:   g(s) = x1 sweep of its P rows   (registers)
+//                        out  = A2 g(s-1) + B2 g(s)      (shared -> bulk store)
 //
-// Every element goes through exactly the operations of the two separate
-// sweeps (same order, no contraction), so the result is bitwise the
-// unfused x1-then-x2 sequence, with 16 B/dof of traffic instead of 32.
+// Chunks hold G x2 cells and travel by TMA 1-D bulk copies (one or two
+// pieces when the source range wraps) into a kXStages-deep ring; results
+// leave by bulk stores from a double buffer.  Every element goes through the
+// exact operations of the separate x1 and x2 sweeps (same order, no
+// contraction), so the result is bitwise the unfused sequence, for 16 B/dof
+// of HBM traffic instead of 32.
 //
-// Thread t of a CTA owns x1 dof t (cell t/p, node t%p) of every row.  CTAs
-// are persistent: each walks a contiguous run of planes while the bulk-copy
-// pipeline (kXStages chunks in flight) runs ahead across plane boundaries.
+// Thread t of a CTA owns x1 dof t (cell t/P, node t%P) of every row; CTAs are
+// persistent over a contiguous run of planes and the load ring runs ahead
+// across plane boundaries.
 #include <algorithm>
 
 #include "async_copy.cuh"
@@ -25,43 +29,67 @@
 
 namespace vpb {
 
-constexpr int kXStages = 6;
+constexpr int kXStages = 3;
+
+struct XChunk {
+  int64_t plane;
+  int first;   // first output cell
+  int nout;    // output cells
+  int nsrc;    // source cells loaded (nout, +1 for the plane's first chunk)
+  int s_begin; // first source cell (mod C2)
+};
+
+__device__ __forceinline__ XChunk xchunk(int64_t j, int64_t pl_begin, int per_plane, int G,
+                                         int C2, const int64_t* __restrict__ q2, int64_t nv1) {
+  XChunk c;
+  c.plane = pl_begin + j / per_plane;
+  const int i = (int)(j % per_plane);
+  const int qm = (int)wrap_mod(q2[c.plane / nv1], C2);
+  const int s0 = C2 - qm - 1;  // (-q2-1) mod C2, in [0, C2)
+  c.first = i * G;
+  c.nout = min(G, C2 - c.first);
+  c.nsrc = c.nout + (i == 0 ? 1 : 0);
+  int sb = s0 + (i == 0 ? 0 : 1 + c.first);
+  while (sb >= C2) sb -= C2;
+  c.s_begin = sb;
+  return c;
+}
 
 template <int P>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(512, 1)
     dg_xplane_kernel(const double* __restrict__ src, double* __restrict__ dst, int n1, int C2,
-                     int64_t nv1, int64_t nplanes, int64_t planes_per_block,
+                     int G, int64_t nv1, int64_t nplanes, int64_t planes_per_block,
                      const double* __restrict__ a1, const double* __restrict__ b1,
                      const int64_t* __restrict__ q1, const double* __restrict__ al1,
                      const double* __restrict__ a2, const double* __restrict__ b2,
                      const int64_t* __restrict__ q2, const double* __restrict__ al2,
                      int32_t* __restrict__ flag1, int32_t* __restrict__ flag2) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int chunk = P * n1;  // one x2 cell: P rows of n1 dofs
+  const int cell = P * n1;                 // one x2 cell: P rows of n1 dofs
+  const int in_chunk = (G + 1) * cell;     // ring slot
+  const int out_chunk = G * cell;
   double* inb = reinterpret_cast<double*>(smem_raw);
-  double* outb = inb + kXStages * chunk;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(outb + 2 * chunk);
+  double* outb = inb + kXStages * in_chunk;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(outb + 2 * out_chunk);
 
   const int tid = threadIdx.x;
   const int64_t pl_begin = blockIdx.x * planes_per_block;
   const int64_t pl_end = min(nplanes, pl_begin + planes_per_block);
   if (pl_begin >= pl_end) return;
-  const int per_plane = C2 + 1;
+  const int per_plane = (C2 + G - 1) / G;
   const int64_t nchunks = (pl_end - pl_begin) * per_plane;
-  const int64_t plane_elems = (int64_t)C2 * chunk;
+  const int64_t plane_elems = (int64_t)C2 * cell;
 
-  // Producer (thread 0): chunk j = (plane pl_begin + j / per_plane, step j % per_plane)
   auto issue_load = [&](int64_t j) {
-    const int64_t pl = pl_begin + j / per_plane;
-    const int k = (int)(j % per_plane);
-    const int64_t iv2 = pl / nv1;
-    const int qm = (int)wrap_mod(q2[iv2], C2);
-    int s = C2 - qm - 1 + k;  // source cell (-q2-1+k) mod C2
-    while (s >= C2) s -= C2;
+    const XChunk c = xchunk(j, pl_begin, per_plane, G, C2, q2, nv1);
     const int st = (int)(j % kXStages);
-    mbar_arrive_expect_tx(bars + st, (uint32_t)chunk * 8u);
-    bulk_g2s(inb + st * chunk, src + pl * plane_elems + (int64_t)s * chunk, (uint32_t)chunk * 8u,
-             bars + st);
+    const double* base = src + c.plane * plane_elems;
+    double* dstp = inb + st * in_chunk;
+    mbar_arrive_expect_tx(bars + st, (uint32_t)c.nsrc * cell * 8u);
+    const int run1 = min(c.nsrc, C2 - c.s_begin);
+    bulk_g2s(dstp, base + (int64_t)c.s_begin * cell, (uint32_t)run1 * cell * 8u, bars + st);
+    if (run1 < c.nsrc)  // wrapped: the rest starts at source cell 0
+      bulk_g2s(dstp + run1 * cell, base, (uint32_t)(c.nsrc - run1) * cell * 8u, bars + st);
   };
 
   if (tid == 0) {
@@ -79,17 +107,19 @@ __global__ void __launch_bounds__(256, 2)
   double A1[P], B1[P], A2[P][P], B2[P][P];
   bool ex1 = true, ex2 = true;
   int lo1 = 0, up1 = 0;
-  double gprev[P], gcur[P];
+  double gprev[P];
   bool bad1 = false, bad2 = false;
 #pragma unroll
-  for (int m = 0; m < P; ++m) gprev[m] = gcur[m] = 0.0;
+  for (int m = 0; m < P; ++m) gprev[m] = 0.0;
+  int64_t cur_plane = -1;
 
-  int64_t j = 0;
-  for (int64_t pl = pl_begin; pl < pl_end; ++pl) {
-    const int64_t iv2 = pl / nv1, iv1 = pl - iv2 * nv1;
-    const int qm2 = (int)wrap_mod(q2[iv2], C2);
-    if (active) {
-      // per-plane coefficients: row j1 of the x1 pair, full x2 pair
+  for (int64_t j = 0; j < nchunks; ++j) {
+    const XChunk c = xchunk(j, pl_begin, per_plane, G, C2, q2, nv1);
+    const int st = (int)(j % kXStages);
+    if (active && c.plane != cur_plane) {
+      // per-plane coefficients: row j1 of the x1 pair, the full x2 pair
+      cur_plane = c.plane;
+      const int64_t iv2 = c.plane / nv1, iv1 = c.plane - iv2 * nv1;
       ex1 = (al1[iv1] == 0.0);
       ex2 = (al2[iv2] == 0.0);
 #pragma unroll
@@ -109,16 +139,17 @@ __global__ void __launch_bounds__(256, 2)
       if (lo1 < 0) lo1 += C1;
       up1 = lo1 + 1 == C1 ? 0 : lo1 + 1;
     }
-    for (int k = 0; k < per_plane; ++k, ++j) {
-      const int st = (int)(j % kXStages);
-      mbar_wait(bars + st, (uint32_t)((j / kXStages) & 1));
-      const double* in = inb + st * chunk;
-      double* out = outb + (j & 1) * chunk;
-      if (active) {
-        // x1 sweep of the P rows of this x2 cell, dof `tid` (_kernels.pyx:113-123)
+    mbar_wait(bars + st, (uint32_t)((j / kXStages) & 1));
+    const double* in = inb + st * in_chunk;
+    double* out = outb + (j & 1) * out_chunk;
+    if (active) {
+      const int lead = c.nsrc - c.nout;  // 1 on a plane's first chunk (the prologue cell)
+      for (int sc = 0; sc < c.nsrc; ++sc) {
+        // x1 sweep of the P rows of source cell sc (_kernels.pyx:113-123)
+        double g[P];
 #pragma unroll
         for (int m2 = 0; m2 < P; ++m2) {
-          const double* row = in + m2 * n1;
+          const double* row = in + (sc * P + m2) * n1;
           double v;
           if (ex1) {
             v = row[up1 * P + j1];
@@ -131,45 +162,43 @@ __global__ void __launch_bounds__(256, 2)
             for (int m = 1; m < P; ++m) acc_b = dadd(acc_b, dmul(B1[m], row[up1 * P + m]));
             v = dadd(acc_a, acc_b);
           }
-          gcur[m2] = v;
+          g[m2] = v;
           bad1 |= not_finite(v);
         }
-        if (k > 0) {
-          // x2 sweep: output cell k-1 from g(s-1), g(s)
+        if (sc >= lead) {
+          // x2 sweep: output cell c.first + sc - lead from g(s-1), g(s)
+          double* orow = out + (sc - lead) * cell;
 #pragma unroll
           for (int jj = 0; jj < P; ++jj) {
             double o;
             if (ex2) {
-              o = gcur[jj];
+              o = g[jj];
             } else {
               double acc_a = dmul(A2[jj][0], gprev[0]);
 #pragma unroll
               for (int m = 1; m < P; ++m) acc_a = dadd(acc_a, dmul(A2[jj][m], gprev[m]));
-              double acc_b = dmul(B2[jj][0], gcur[0]);
+              double acc_b = dmul(B2[jj][0], g[0]);
 #pragma unroll
-              for (int m = 1; m < P; ++m) acc_b = dadd(acc_b, dmul(B2[jj][m], gcur[m]));
+              for (int m = 1; m < P; ++m) acc_b = dadd(acc_b, dmul(B2[jj][m], g[m]));
               o = dadd(acc_a, acc_b);
             }
             bad2 |= not_finite(o);
-            out[jj * n1 + tid] = o;
+            orow[jj * n1 + tid] = o;
           }
         }
 #pragma unroll
-        for (int m = 0; m < P; ++m) gprev[m] = gcur[m];
-      }
-      fence_proxy_async_smem();
-      if (tid == 0) bulk_wait_read<0>();  // store of chunk j-1 released outb[(j+1)&1]
-      __syncthreads();
-      if (tid == 0) {
-        if (k > 0) {
-          // output x2 cell c2 = k-1 (exact: (c2 - q2) mod C2 source pairing)
-          bulk_s2g(dst + pl * plane_elems + (int64_t)(k - 1) * chunk, out, (uint32_t)chunk * 8u);
-          bulk_commit();
-        }
-        if (j + kXStages < nchunks) issue_load(j + kXStages);
+        for (int m = 0; m < P; ++m) gprev[m] = g[m];
       }
     }
-    (void)qm2;
+    fence_proxy_async_smem();
+    if (tid == 0) bulk_wait_read<0>();  // store of chunk j-1 released outb[(j+1)&1]
+    __syncthreads();
+    if (tid == 0) {
+      bulk_s2g(dst + c.plane * plane_elems + (int64_t)c.first * cell, out,
+               (uint32_t)c.nout * cell * 8u);
+      bulk_commit();
+      if (j + kXStages < nchunks) issue_load(j + kXStages);
+    }
   }
   if (tid == 0) bulk_wait<0>();
   report_flag(bad1, flag1);
@@ -198,19 +227,28 @@ static int launch_xplane(const double* src, double* dst, const int64_t dims[4], 
   const int64_t nplanes = dims[2] * dims[3];
   if (nplanes == 0) return VPB_OK;
   const int threads = ((n1 + 31) / 32) * 32;
-  if (threads > 1024) {
+  if (threads > 512) {
     set_error("x rows of %d dofs exceed one CTA", n1);
     return VPB_ERR_UNSUPPORTED;
   }
-  const size_t smem = (size_t)(kXStages + 2) * P * n1 * sizeof(double) + kXStages * 8;
-  if (smem > 200 * 1024) {
+  const int cell_bytes = P * n1 * 8;
+  // ~16 KB of new source cells per chunk; two CTAs per SM
+  int G = std::max(1, 16384 / cell_bytes);
+  G = std::min(G, C2);
+  size_t smem = (size_t)kXStages * (G + 1) * cell_bytes + 2 * (size_t)G * cell_bytes +
+                kXStages * 8;
+  while (G > 1 && smem > 110 * 1024) {
+    --G;
+    smem = (size_t)kXStages * (G + 1) * cell_bytes + 2 * (size_t)G * cell_bytes + kXStages * 8;
+  }
+  if (smem > 220 * 1024) {
     set_error("x plane chunk of %d dofs does not fit shared memory", P * n1);
     return VPB_ERR_UNSUPPORTED;
   }
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(dg_xplane_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
+                         220 * 1024);
     attr = true;
   }
   int occ = 0;
@@ -220,7 +258,7 @@ static int launch_xplane(const double* src, double* dst, const int64_t dims[4], 
   const int64_t ppb = (nplanes + grid - 1) / grid;
   const int64_t blocks = (nplanes + ppb - 1) / ppb;
   dg_xplane_kernel<P><<<(unsigned)blocks, threads, smem, st>>>(
-      src, dst, n1, C2, nv1, nplanes, ppb, a1, b1, q1, al1, a2, b2, q2, al2, f1, f2);
+      src, dst, n1, C2, G, nv1, nplanes, ppb, a1, b1, q1, al1, a2, b2, q2, al2, f1, f2);
   return check_launch("dg_xplane_kernel");
 }
 
@@ -237,7 +275,7 @@ extern "C" int vpb_dg_sweep_xplane(const double* src, double* dst, const int64_t
   VPB_REQUIRE(order >= 1 && order <= kMaxOrder, "order %d outside 1..9", order);
   VPB_REQUIRE(dims[0] % order == 0 && dims[1] % order == 0, "x axes not whole cells");
   VPB_REQUIRE(dims[1] > 1, "fused x sweep needs a 2x2v field");
-  VPB_REQUIRE((dims[0] * order) % 2 == 0, "x1 rows must be a multiple of 16 bytes per cell row");
+  VPB_REQUIRE((dims[0] * order) % 2 == 0, "a cell row block must be a multiple of 16 bytes");
   VPB_REQUIRE((reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
                   (reinterpret_cast<uintptr_t>(dst) & 15) == 0,
               "field buffers must be 16-byte aligned");
