@@ -9,19 +9,21 @@
 //
 //   chunk 0 of a plane:  source cells s0 .. s0+n   -> output cells 0 .. n-1
 //   chunk i > 0:         source cells s0+1+iG ...  -> output cells iG ...
-//   per source cell s:   g(s) = x1 sweep of its P rows   (registers)
-//                        out  = A2 g(s-1) + B2 g(s)      (shared -> bulk store)
 //
-// Chunks hold G x2 cells and travel by TMA 1-D bulk copies (one or two
-// pieces when the source range wraps) into a kXStages-deep ring; results
-// leave by bulk stores from a double buffer.  Every element goes through the
-// exact operations of the separate x1 and x2 sweeps (same order, no
-// contraction), so the result is bitwise the unfused sequence, for 16 B/dof
-// of HBM traffic instead of 32.
+// Per chunk (G x2 cells = G*P rows of n1 dofs):
+//   1. TMA 1-D bulk copies (one or two pieces when the source range wraps)
+//      land the rows in a kXStages-deep shared-memory ring (mbarriers);
+//   2. x1 phase: every row is swept along x1 into a shared g buffer;
+//   3. x2 phase: out = A2 g(s-1) + B2 g(s) is written straight to HBM with
+//      coalesced streaming stores (g of the previous chunk's last cell is
+//      carried in a small double buffer).
+// Every element goes through the exact operations of the separate x1 and
+// x2 sweeps (same order, no contraction), so the result is bitwise the
+// unfused sequence, for 16 B/dof of HBM traffic instead of 32.
 //
-// Thread t of a CTA owns x1 dof t (cell t/P, node t%P) of every row; CTAs are
-// persistent over a contiguous run of planes and the load ring runs ahead
-// across plane boundaries.
+// Thread (r, x) of a CTA owns x1 dof x (cell x/P, node x%P) of rows r, r+R,
+// ...; CTAs are persistent over a contiguous run of planes and the load ring
+// runs ahead across plane boundaries.
 #include <algorithm>
 
 #include "async_copy.cuh"
@@ -33,10 +35,10 @@ constexpr int kXStages = 3;
 
 struct XChunk {
   int64_t plane;
-  int first;   // first output cell
-  int nout;    // output cells
-  int nsrc;    // source cells loaded (nout, +1 for the plane's first chunk)
-  int s_begin; // first source cell (mod C2)
+  int first;    // first output cell
+  int nout;     // output cells
+  int nsrc;     // source cells loaded (nout, +1 for the plane's first chunk)
+  int s_begin;  // first source cell (mod C2)
 };
 
 __device__ __forceinline__ XChunk xchunk(int64_t j, int64_t pl_begin, int per_plane, int G,
@@ -56,21 +58,21 @@ __device__ __forceinline__ XChunk xchunk(int64_t j, int64_t pl_begin, int per_pl
 }
 
 template <int P>
-__global__ void __launch_bounds__(512, 1)
+__global__ void __launch_bounds__(768, 1)
     dg_xplane_kernel(const double* __restrict__ src, double* __restrict__ dst, int n1, int C2,
-                     int G, int64_t nv1, int64_t nplanes, int64_t planes_per_block,
+                     int G, int R, int64_t nv1, int64_t nplanes, int64_t planes_per_block,
                      const double* __restrict__ a1, const double* __restrict__ b1,
                      const int64_t* __restrict__ q1, const double* __restrict__ al1,
                      const double* __restrict__ a2, const double* __restrict__ b2,
                      const int64_t* __restrict__ q2, const double* __restrict__ al2,
                      int32_t* __restrict__ flag1, int32_t* __restrict__ flag2) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int cell = P * n1;                 // one x2 cell: P rows of n1 dofs
-  const int in_chunk = (G + 1) * cell;     // ring slot
-  const int out_chunk = G * cell;
+  const int cell = P * n1;              // one x2 cell: P rows of n1 dofs
+  const int slot = (G + 1) * cell;      // ring slot (G cells + the plane prologue cell)
   double* inb = reinterpret_cast<double*>(smem_raw);
-  double* outb = inb + kXStages * in_chunk;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(outb + 2 * out_chunk);
+  double* gbuf = inb + kXStages * slot;  // x1-swept rows of the current chunk
+  double* carry = gbuf + slot;           // [2][cell]: g of the previous chunk's last cell
+  uint64_t* bars = reinterpret_cast<uint64_t*>(carry + 2 * cell);
 
   const int tid = threadIdx.x;
   const int64_t pl_begin = blockIdx.x * planes_per_block;
@@ -84,7 +86,7 @@ __global__ void __launch_bounds__(512, 1)
     const XChunk c = xchunk(j, pl_begin, per_plane, G, C2, q2, nv1);
     const int st = (int)(j % kXStages);
     const double* base = src + c.plane * plane_elems;
-    double* dstp = inb + st * in_chunk;
+    double* dstp = inb + st * slot;
     mbar_arrive_expect_tx(bars + st, (uint32_t)c.nsrc * cell * 8u);
     const int run1 = min(c.nsrc, C2 - c.s_begin);
     bulk_g2s(dstp, base + (int64_t)c.s_begin * cell, (uint32_t)run1 * cell * 8u, bars + st);
@@ -101,16 +103,15 @@ __global__ void __launch_bounds__(512, 1)
   if (tid == 0)
     for (int64_t j = 0; j < kXStages && j < nchunks; ++j) issue_load(j);
 
-  const bool active = tid < n1;
-  const int c1 = tid / P, j1 = tid % P;
+  const int x = tid % n1;
+  const int rg = tid / n1;  // row group
+  const bool active = rg < R;
+  const int c1 = x / P, j1 = x % P;
   const int C1 = n1 / P;
   double A1[P], B1[P], A2[P][P], B2[P][P];
   bool ex1 = true, ex2 = true;
   int lo1 = 0, up1 = 0;
-  double gprev[P];
   bool bad1 = false, bad2 = false;
-#pragma unroll
-  for (int m = 0; m < P; ++m) gprev[m] = 0.0;
   int64_t cur_plane = -1;
 
   for (int64_t j = 0; j < nchunks; ++j) {
@@ -140,67 +141,74 @@ __global__ void __launch_bounds__(512, 1)
       up1 = lo1 + 1 == C1 ? 0 : lo1 + 1;
     }
     mbar_wait(bars + st, (uint32_t)((j / kXStages) & 1));
-    const double* in = inb + st * in_chunk;
-    double* out = outb + (j & 1) * out_chunk;
+    const double* in = inb + st * slot;
+    // ---- x1 phase: g[row][x] for every row of the chunk (_kernels.pyx:113-123)
     if (active) {
-      const int lead = c.nsrc - c.nout;  // 1 on a plane's first chunk (the prologue cell)
-      for (int sc = 0; sc < c.nsrc; ++sc) {
-        // x1 sweep of the P rows of source cell sc (_kernels.pyx:113-123)
-        double g[P];
+      const int rows = c.nsrc * P;
+      for (int r = rg; r < rows; r += R) {
+        const double* row = in + r * n1;
+        double v;
+        if (ex1) {
+          v = row[up1 * P + j1];
+        } else {
+          double acc_a = dmul(A1[0], row[lo1 * P]);
 #pragma unroll
-        for (int m2 = 0; m2 < P; ++m2) {
-          const double* row = in + (sc * P + m2) * n1;
-          double v;
-          if (ex1) {
-            v = row[up1 * P + j1];
-          } else {
-            double acc_a = dmul(A1[0], row[lo1 * P]);
+          for (int m = 1; m < P; ++m) acc_a = dadd(acc_a, dmul(A1[m], row[lo1 * P + m]));
+          double acc_b = dmul(B1[0], row[up1 * P]);
 #pragma unroll
-            for (int m = 1; m < P; ++m) acc_a = dadd(acc_a, dmul(A1[m], row[lo1 * P + m]));
-            double acc_b = dmul(B1[0], row[up1 * P]);
-#pragma unroll
-            for (int m = 1; m < P; ++m) acc_b = dadd(acc_b, dmul(B1[m], row[up1 * P + m]));
-            v = dadd(acc_a, acc_b);
-          }
-          g[m2] = v;
-          bad1 |= not_finite(v);
+          for (int m = 1; m < P; ++m) acc_b = dadd(acc_b, dmul(B1[m], row[up1 * P + m]));
+          v = dadd(acc_a, acc_b);
         }
-        if (sc >= lead) {
-          // x2 sweep: output cell c.first + sc - lead from g(s-1), g(s)
-          double* orow = out + (sc - lead) * cell;
-#pragma unroll
-          for (int jj = 0; jj < P; ++jj) {
-            double o;
-            if (ex2) {
-              o = g[jj];
-            } else {
-              double acc_a = dmul(A2[jj][0], gprev[0]);
-#pragma unroll
-              for (int m = 1; m < P; ++m) acc_a = dadd(acc_a, dmul(A2[jj][m], gprev[m]));
-              double acc_b = dmul(B2[jj][0], g[0]);
-#pragma unroll
-              for (int m = 1; m < P; ++m) acc_b = dadd(acc_b, dmul(B2[jj][m], g[m]));
-              o = dadd(acc_a, acc_b);
-            }
-            bad2 |= not_finite(o);
-            orow[jj * n1 + tid] = o;
-          }
-        }
-#pragma unroll
-        for (int m = 0; m < P; ++m) gprev[m] = g[m];
+        gbuf[r * n1 + x] = v;
+        bad1 |= not_finite(v);
       }
     }
-    fence_proxy_async_smem();
-    if (tid == 0) bulk_wait_read<0>();  // store of chunk j-1 released outb[(j+1)&1]
     __syncthreads();
-    if (tid == 0) {
-      bulk_s2g(dst + c.plane * plane_elems + (int64_t)c.first * cell, out,
-               (uint32_t)c.nout * cell * 8u);
-      bulk_commit();
-      if (j + kXStages < nchunks) issue_load(j + kXStages);
+    // the ring slot has been consumed: refill it
+    if (tid == 0 && j + kXStages < nchunks) issue_load(j + kXStages);
+    // ---- x2 phase: output cells of the chunk, straight to HBM
+    if (active) {
+      const int lead = c.nsrc - c.nout;  // 1 on a plane's first chunk
+      const double* cprev = carry + ((j + 1) & 1) * cell;  // written by chunk j-1
+      double* out = dst + c.plane * plane_elems + (int64_t)c.first * cell;
+      for (int oc = rg; oc < c.nout; oc += R) {
+        const int sc = oc + lead;  // source cell of the "up" side
+        const double* gu = gbuf + sc * cell;
+        const double* gl = sc > 0 ? gbuf + (sc - 1) * cell : cprev;
+        double gp[P], gc[P];
+#pragma unroll
+        for (int m = 0; m < P; ++m) {
+          gp[m] = gl[m * n1 + x];
+          gc[m] = gu[m * n1 + x];
+        }
+#pragma unroll
+        for (int jj = 0; jj < P; ++jj) {
+          double o;
+          if (ex2) {
+            o = gc[jj];
+          } else {
+            double acc_a = dmul(A2[jj][0], gp[0]);
+#pragma unroll
+            for (int m = 1; m < P; ++m) acc_a = dadd(acc_a, dmul(A2[jj][m], gp[m]));
+            double acc_b = dmul(B2[jj][0], gc[0]);
+#pragma unroll
+            for (int m = 1; m < P; ++m) acc_b = dadd(acc_b, dmul(B2[jj][m], gc[m]));
+            o = dadd(acc_a, acc_b);
+          }
+          bad2 |= not_finite(o);
+          __stcs(out + (int64_t)oc * cell + jj * n1 + x, o);
+        }
+      }
+      // carry g of this chunk's last source cell into the other buffer
+      if (rg == 0) {
+        const double* glast = gbuf + (c.nsrc - 1) * cell;
+        double* cnext = carry + (j & 1) * cell;
+#pragma unroll
+        for (int m = 0; m < P; ++m) cnext[m * n1 + x] = glast[m * n1 + x];
+      }
     }
+    __syncthreads();  // gbuf and carry[(j+1)&1] are free for chunk j+1
   }
-  if (tid == 0) bulk_wait<0>();
   report_flag(bad1, flag1);
   report_flag(bad2, flag2);
 }
@@ -226,21 +234,20 @@ static int launch_xplane(const double* src, double* dst, const int64_t dims[4], 
   const int64_t nv1 = dims[2];
   const int64_t nplanes = dims[2] * dims[3];
   if (nplanes == 0) return VPB_OK;
-  const int threads = ((n1 + 31) / 32) * 32;
-  if (threads > 512) {
+  if (n1 > 768) {
     set_error("x rows of %d dofs exceed one CTA", n1);
     return VPB_ERR_UNSUPPORTED;
   }
-  const int cell_bytes = P * n1 * 8;
-  // ~16 KB of new source cells per chunk; two CTAs per SM
-  int G = std::max(1, 16384 / cell_bytes);
+  const int R = std::max(1, 384 / n1);  // row groups
+  const int threads = ((n1 * R + 31) / 32) * 32;
+  const size_t cell_bytes = (size_t)P * n1 * 8;
+  auto smem_for = [&](int g) {
+    return (size_t)(kXStages + 1) * (g + 1) * cell_bytes + 2 * cell_bytes + kXStages * 8;
+  };
+  int G = std::max<int>(1, (int)(16384 / cell_bytes));
   G = std::min(G, C2);
-  size_t smem = (size_t)kXStages * (G + 1) * cell_bytes + 2 * (size_t)G * cell_bytes +
-                kXStages * 8;
-  while (G > 1 && smem > 110 * 1024) {
-    --G;
-    smem = (size_t)kXStages * (G + 1) * cell_bytes + 2 * (size_t)G * cell_bytes + kXStages * 8;
-  }
+  while (G > 1 && smem_for(G) > 110 * 1024) --G;
+  const size_t smem = smem_for(G);
   if (smem > 220 * 1024) {
     set_error("x plane chunk of %d dofs does not fit shared memory", P * n1);
     return VPB_ERR_UNSUPPORTED;
@@ -258,7 +265,7 @@ static int launch_xplane(const double* src, double* dst, const int64_t dims[4], 
   const int64_t ppb = (nplanes + grid - 1) / grid;
   const int64_t blocks = (nplanes + ppb - 1) / ppb;
   dg_xplane_kernel<P><<<(unsigned)blocks, threads, smem, st>>>(
-      src, dst, n1, C2, G, nv1, nplanes, ppb, a1, b1, q1, al1, a2, b2, q2, al2, f1, f2);
+      src, dst, n1, C2, G, R, nv1, nplanes, ppb, a1, b1, q1, al1, a2, b2, q2, al2, f1, f2);
   return check_launch("dg_xplane_kernel");
 }
 
