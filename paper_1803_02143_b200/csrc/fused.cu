@@ -25,6 +25,7 @@
 // ...; CTAs are persistent over a contiguous run of planes and the load ring
 // runs ahead across plane boundaries.
 #include <algorithm>
+#include <cstdlib>
 
 #include "async_copy.cuh"
 #include "common.cuh"
@@ -34,28 +35,38 @@ namespace vpb {
 constexpr int kXStages = 3;
 
 struct XChunk {
-  int64_t plane;
   int first;    // first output cell
   int nout;     // output cells
   int nsrc;     // source cells loaded (nout, +1 for the plane's first chunk)
   int s_begin;  // first source cell (mod C2)
 };
 
-__device__ __forceinline__ XChunk xchunk(int64_t j, int64_t pl_begin, int per_plane, int G,
-                                         int C2, const int64_t* __restrict__ q2, int64_t nv1) {
-  XChunk c;
-  c.plane = pl_begin + j / per_plane;
-  const int i = (int)(j % per_plane);
-  const int qm = (int)wrap_mod(q2[c.plane / nv1], C2);
-  const int s0 = C2 - qm - 1;  // (-q2-1) mod C2, in [0, C2)
-  c.first = i * G;
-  c.nout = min(G, C2 - c.first);
-  c.nsrc = c.nout + (i == 0 ? 1 : 0);
-  int sb = s0 + (i == 0 ? 0 : 1 + c.first);
-  while (sb >= C2) sb -= C2;
-  c.s_begin = sb;
-  return c;
-}
+// Walks the chunks of a run of planes with 32-bit bookkeeping only.
+struct XCursor {
+  int64_t plane;
+  int i;    // chunk index inside the plane
+  int s0;   // (-q2-1) mod C2 of the current plane
+  __device__ __forceinline__ void start(int64_t pl, int C2, const int64_t* __restrict__ q2,
+                                        int64_t nv1) {
+    plane = pl;
+    i = 0;
+    s0 = C2 - 1 - (int)wrap_mod(q2[pl / nv1], C2);
+  }
+  __device__ __forceinline__ XChunk chunk(int G, int C2) const {
+    XChunk c;
+    c.first = i * G;
+    c.nout = min(G, C2 - c.first);
+    c.nsrc = c.nout + (i == 0 ? 1 : 0);
+    int sb = s0 + (i == 0 ? 0 : 1 + c.first);
+    if (sb >= C2) sb -= C2;
+    c.s_begin = sb;
+    return c;
+  }
+  __device__ __forceinline__ void advance(int per_plane, int C2, const int64_t* __restrict__ q2,
+                                          int64_t nv1) {
+    if (++i == per_plane) start(plane + 1, C2, q2, nv1);
+  }
+};
 
 template <int P>
 __global__ void __launch_bounds__(768, 1)
@@ -82,16 +93,22 @@ __global__ void __launch_bounds__(768, 1)
   const int64_t nchunks = (pl_end - pl_begin) * per_plane;
   const int64_t plane_elems = (int64_t)C2 * cell;
 
-  auto issue_load = [&](int64_t j) {
-    const XChunk c = xchunk(j, pl_begin, per_plane, G, C2, q2, nv1);
-    const int st = (int)(j % kXStages);
-    const double* base = src + c.plane * plane_elems;
+  // producer cursor (thread 0 only): chunk j + kXStages is the next to load
+  XCursor prod;
+  prod.start(pl_begin, C2, q2, nv1);
+  int64_t prod_j = 0;
+  auto issue_next = [&]() {
+    const XChunk c = prod.chunk(G, C2);
+    const int st = (int)(prod_j % kXStages);
+    const double* base = src + prod.plane * plane_elems;
     double* dstp = inb + st * slot;
     mbar_arrive_expect_tx(bars + st, (uint32_t)c.nsrc * cell * 8u);
     const int run1 = min(c.nsrc, C2 - c.s_begin);
     bulk_g2s(dstp, base + (int64_t)c.s_begin * cell, (uint32_t)run1 * cell * 8u, bars + st);
     if (run1 < c.nsrc)  // wrapped: the rest starts at source cell 0
       bulk_g2s(dstp + run1 * cell, base, (uint32_t)(c.nsrc - run1) * cell * 8u, bars + st);
+    ++prod_j;
+    prod.advance(per_plane, C2, q2, nv1);
   };
 
   if (tid == 0) {
@@ -101,7 +118,7 @@ __global__ void __launch_bounds__(768, 1)
   }
   __syncthreads();
   if (tid == 0)
-    for (int64_t j = 0; j < kXStages && j < nchunks; ++j) issue_load(j);
+    while (prod_j < kXStages && prod_j < nchunks) issue_next();
 
   const int x = tid % n1;
   const int rg = tid / n1;  // row group
@@ -112,15 +129,17 @@ __global__ void __launch_bounds__(768, 1)
   bool ex1 = true, ex2 = true;
   int lo1 = 0, up1 = 0;
   bool bad1 = false, bad2 = false;
-  int64_t cur_plane = -1;
+  XCursor cur;
+  cur.start(pl_begin, C2, q2, nv1);
+  int st = 0;
+  uint32_t phase = 0;
 
   for (int64_t j = 0; j < nchunks; ++j) {
-    const XChunk c = xchunk(j, pl_begin, per_plane, G, C2, q2, nv1);
-    const int st = (int)(j % kXStages);
-    if (active && c.plane != cur_plane) {
+    const XChunk c = cur.chunk(G, C2);
+    const int64_t plane = cur.plane;
+    if (active && cur.i == 0) {
       // per-plane coefficients: row j1 of the x1 pair, the full x2 pair
-      cur_plane = c.plane;
-      const int64_t iv2 = c.plane / nv1, iv1 = c.plane - iv2 * nv1;
+      const int64_t iv2 = plane / nv1, iv1 = plane - iv2 * nv1;
       ex1 = (al1[iv1] == 0.0);
       ex2 = (al2[iv2] == 0.0);
 #pragma unroll
@@ -140,7 +159,7 @@ __global__ void __launch_bounds__(768, 1)
       if (lo1 < 0) lo1 += C1;
       up1 = lo1 + 1 == C1 ? 0 : lo1 + 1;
     }
-    mbar_wait(bars + st, (uint32_t)((j / kXStages) & 1));
+    mbar_wait(bars + st, phase);
     const double* in = inb + st * slot;
     // ---- x1 phase: g[row][x] for every row of the chunk (_kernels.pyx:113-123)
     if (active) {
@@ -165,12 +184,12 @@ __global__ void __launch_bounds__(768, 1)
     }
     __syncthreads();
     // the ring slot has been consumed: refill it
-    if (tid == 0 && j + kXStages < nchunks) issue_load(j + kXStages);
+    if (tid == 0 && prod_j < nchunks) issue_next();
     // ---- x2 phase: output cells of the chunk, straight to HBM
     if (active) {
       const int lead = c.nsrc - c.nout;  // 1 on a plane's first chunk
       const double* cprev = carry + ((j + 1) & 1) * cell;  // written by chunk j-1
-      double* out = dst + c.plane * plane_elems + (int64_t)c.first * cell;
+      double* out = dst + plane * plane_elems + (int64_t)c.first * cell;
       for (int oc = rg; oc < c.nout; oc += R) {
         const int sc = oc + lead;  // source cell of the "up" side
         const double* gu = gbuf + sc * cell;
@@ -208,6 +227,11 @@ __global__ void __launch_bounds__(768, 1)
       }
     }
     __syncthreads();  // gbuf and carry[(j+1)&1] are free for chunk j+1
+    cur.advance(per_plane, C2, q2, nv1);
+    if (++st == kXStages) {
+      st = 0;
+      phase ^= 1u;
+    }
   }
   report_flag(bad1, flag1);
   report_flag(bad2, flag2);
@@ -238,15 +262,18 @@ static int launch_xplane(const double* src, double* dst, const int64_t dims[4], 
     set_error("x rows of %d dofs exceed one CTA", n1);
     return VPB_ERR_UNSUPPORTED;
   }
-  const int R = std::max(1, 384 / n1);  // row groups
+  static const int env_threads = getenv("VPB_XPLANE_THREADS") ? atoi(getenv("VPB_XPLANE_THREADS")) : 384;
+  static const int env_chunk = getenv("VPB_XPLANE_CHUNK") ? atoi(getenv("VPB_XPLANE_CHUNK")) : 16384;
+  static const int env_smem = getenv("VPB_XPLANE_SMEM") ? atoi(getenv("VPB_XPLANE_SMEM")) : 110 * 1024;
+  const int R = std::max(1, env_threads / n1);  // row groups
   const int threads = ((n1 * R + 31) / 32) * 32;
   const size_t cell_bytes = (size_t)P * n1 * 8;
   auto smem_for = [&](int g) {
     return (size_t)(kXStages + 1) * (g + 1) * cell_bytes + 2 * cell_bytes + kXStages * 8;
   };
-  int G = std::max<int>(1, (int)(16384 / cell_bytes));
+  int G = std::max<int>(1, (int)(env_chunk / cell_bytes));
   G = std::min(G, C2);
-  while (G > 1 && smem_for(G) > 110 * 1024) --G;
+  while (G > 1 && (int)smem_for(G) > env_smem) --G;
   const size_t smem = smem_for(G);
   if (smem > 220 * 1024) {
     set_error("x plane chunk of %d dofs does not fit shared memory", P * n1);
