@@ -11,19 +11,19 @@
 //   chunk i > 0:         source cells s0+1+iG ...  -> output cells iG ...
 //
 // Per chunk (G x2 cells = G*P rows of n1 dofs):
-//   1. TMA 1-D bulk copies (one or two pieces when the source range wraps)
-//      land the rows in a kXStages-deep shared-memory ring (mbarriers);
-//   2. x1 phase: every row is swept along x1 into a shared g buffer;
-//   3. x2 phase: out = A2 g(s-1) + B2 g(s) is written straight to HBM with
-//      coalesced streaming stores (g of the previous chunk's last cell is
-//      carried in a small double buffer).
+//   * TMA 1-D bulk copies (one or two pieces when the source range wraps)
+//     land the rows in a kXStages-deep shared-memory ring (mbarriers);
+//   * thread c owns x1 cell c: for each source x2 cell it sweeps the cell's
+//     P rows along x1 (2P smem loads per row, P outputs), keeping the P x P
+//     block g in registers, then applies the x2 pair to g(s-1), g(s) and
+//     writes the P x P output block to a staging tile;
+//   * the tile leaves by a bulk store (double buffered).
 // Every element goes through the exact operations of the separate x1 and
 // x2 sweeps (same order, no contraction), so the result is bitwise the
 // unfused sequence, for 16 B/dof of HBM traffic instead of 32.
 //
-// Thread (r, x) of a CTA owns x1 dof x (cell x/P, node x%P) of rows r, r+R,
-// ...; CTAs are persistent over a contiguous run of planes and the load ring
-// runs ahead across plane boundaries.
+// CTAs are small (one warp per 32 x1 cells) and persistent over a
+// contiguous run of planes; the load ring runs ahead across planes.
 #include <algorithm>
 #include <cstdlib>
 
@@ -32,7 +32,7 @@
 
 namespace vpb {
 
-constexpr int kXStages = 3;
+constexpr int kXStages = 4;
 
 struct XChunk {
   int first;    // first output cell
@@ -44,8 +44,8 @@ struct XChunk {
 // Walks the chunks of a run of planes with 32-bit bookkeeping only.
 struct XCursor {
   int64_t plane;
-  int i;    // chunk index inside the plane
-  int s0;   // (-q2-1) mod C2 of the current plane
+  int i;   // chunk index inside the plane
+  int s0;  // (-q2-1) mod C2 of the current plane
   __device__ __forceinline__ void start(int64_t pl, int C2, const int64_t* __restrict__ q2,
                                         int64_t nv1) {
     plane = pl;
@@ -69,21 +69,35 @@ struct XCursor {
 };
 
 template <int P>
-__global__ void __launch_bounds__(768, 1)
+__device__ __forceinline__ void lds_row_cell(const double* p, double (&u)[P]) {
+  if constexpr (P % 2 == 0) {
+#pragma unroll
+    for (int m = 0; m < P; m += 2) {
+      const double2 v = *reinterpret_cast<const double2*>(p + m);
+      u[m] = v.x;
+      u[m + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int m = 0; m < P; ++m) u[m] = p[m];
+  }
+}
+
+template <int P>
+__global__ void __launch_bounds__(128)
     dg_xplane_kernel(const double* __restrict__ src, double* __restrict__ dst, int n1, int C2,
-                     int G, int R, int64_t nv1, int64_t nplanes, int64_t planes_per_block,
+                     int G, int64_t nv1, int64_t nplanes, int64_t planes_per_block,
                      const double* __restrict__ a1, const double* __restrict__ b1,
                      const int64_t* __restrict__ q1, const double* __restrict__ al1,
                      const double* __restrict__ a2, const double* __restrict__ b2,
                      const int64_t* __restrict__ q2, const double* __restrict__ al2,
                      int32_t* __restrict__ flag1, int32_t* __restrict__ flag2) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int cell = P * n1;              // one x2 cell: P rows of n1 dofs
-  const int slot = (G + 1) * cell;      // ring slot (G cells + the plane prologue cell)
+  const int cell = P * n1;          // one x2 cell: P rows of n1 dofs
+  const int slot = (G + 1) * cell;  // ring slot (G cells + the plane prologue cell)
   double* inb = reinterpret_cast<double*>(smem_raw);
-  double* gbuf = inb + kXStages * slot;  // x1-swept rows of the current chunk
-  double* carry = gbuf + slot;           // [2][cell]: g of the previous chunk's last cell
-  uint64_t* bars = reinterpret_cast<uint64_t*>(carry + 2 * cell);
+  double* outb = inb + kXStages * slot;  // [2][G*cell] staging tiles
+  uint64_t* bars = reinterpret_cast<uint64_t*>(outb + 2 * G * cell);
 
   const int tid = threadIdx.x;
   const int64_t pl_begin = blockIdx.x * planes_per_block;
@@ -93,21 +107,24 @@ __global__ void __launch_bounds__(768, 1)
   const int64_t nchunks = (pl_end - pl_begin) * per_plane;
   const int64_t plane_elems = (int64_t)C2 * cell;
 
-  // producer cursor (thread 0 only): chunk j + kXStages is the next to load
+  // producer cursor (thread 0 only)
   XCursor prod;
   prod.start(pl_begin, C2, q2, nv1);
   int64_t prod_j = 0;
+  int prod_st = 0;
   auto issue_next = [&]() {
     const XChunk c = prod.chunk(G, C2);
-    const int st = (int)(prod_j % kXStages);
     const double* base = src + prod.plane * plane_elems;
-    double* dstp = inb + st * slot;
-    mbar_arrive_expect_tx(bars + st, (uint32_t)c.nsrc * cell * 8u);
+    double* dstp = inb + prod_st * slot;
+    mbar_arrive_expect_tx(bars + prod_st, (uint32_t)c.nsrc * cell * 8u);
     const int run1 = min(c.nsrc, C2 - c.s_begin);
-    bulk_g2s(dstp, base + (int64_t)c.s_begin * cell, (uint32_t)run1 * cell * 8u, bars + st);
+    bulk_g2s(dstp, base + (int64_t)c.s_begin * cell, (uint32_t)run1 * cell * 8u,
+             bars + prod_st);
     if (run1 < c.nsrc)  // wrapped: the rest starts at source cell 0
-      bulk_g2s(dstp + run1 * cell, base, (uint32_t)(c.nsrc - run1) * cell * 8u, bars + st);
+      bulk_g2s(dstp + run1 * cell, base, (uint32_t)(c.nsrc - run1) * cell * 8u,
+               bars + prod_st);
     ++prod_j;
+    if (++prod_st == kXStages) prod_st = 0;
     prod.advance(per_plane, C2, q2, nv1);
   };
 
@@ -120,14 +137,12 @@ __global__ void __launch_bounds__(768, 1)
   if (tid == 0)
     while (prod_j < kXStages && prod_j < nchunks) issue_next();
 
-  const int x = tid % n1;
-  const int rg = tid / n1;  // row group
-  const bool active = rg < R;
-  const int c1 = x / P, j1 = x % P;
   const int C1 = n1 / P;
-  double A1[P], B1[P], A2[P][P], B2[P][P];
+  const bool active = tid < C1;
+  double A1[P][P], B1[P][P], A2[P][P], B2[P][P];
   bool ex1 = true, ex2 = true;
-  int lo1 = 0, up1 = 0;
+  int lo_off = 0, up_off = 0;  // element offsets of the two x1 source cells in a row
+  double gp[P][P];             // g of the previous source x2 cell: [row m2][dof j]
   bool bad1 = false, bad2 = false;
   XCursor cur;
   cur.start(pl_begin, C2, q2, nv1);
@@ -138,101 +153,111 @@ __global__ void __launch_bounds__(768, 1)
     const XChunk c = cur.chunk(G, C2);
     const int64_t plane = cur.plane;
     if (active && cur.i == 0) {
-      // per-plane coefficients: row j1 of the x1 pair, the full x2 pair
       const int64_t iv2 = plane / nv1, iv1 = plane - iv2 * nv1;
       ex1 = (al1[iv1] == 0.0);
       ex2 = (al2[iv2] == 0.0);
 #pragma unroll
-      for (int m = 0; m < P; ++m) {
-        A1[m] = __ldg(a1 + iv1 * P * P + j1 * P + m);
-        B1[m] = __ldg(b1 + iv1 * P * P + j1 * P + m);
-      }
-#pragma unroll
       for (int jj = 0; jj < P; ++jj)
 #pragma unroll
         for (int m = 0; m < P; ++m) {
+          A1[jj][m] = __ldg(a1 + iv1 * P * P + jj * P + m);
+          B1[jj][m] = __ldg(b1 + iv1 * P * P + jj * P + m);
           A2[jj][m] = __ldg(a2 + iv2 * P * P + jj * P + m);
           B2[jj][m] = __ldg(b2 + iv2 * P * P + jj * P + m);
         }
       const int qm1 = (int)wrap_mod(q1[iv1], C1);
-      lo1 = c1 - qm1 - 1;
-      if (lo1 < 0) lo1 += C1;
-      up1 = lo1 + 1 == C1 ? 0 : lo1 + 1;
+      int lo = tid - qm1 - 1;
+      if (lo < 0) lo += C1;
+      const int up = lo + 1 == C1 ? 0 : lo + 1;
+      lo_off = lo * P;
+      up_off = up * P;
     }
     mbar_wait(bars + st, phase);
     const double* in = inb + st * slot;
-    // ---- x1 phase: g[row][x] for every row of the chunk (_kernels.pyx:113-123)
-    if (active) {
-      const int rows = c.nsrc * P;
-      for (int r = rg; r < rows; r += R) {
-        const double* row = in + r * n1;
-        double v;
-        if (ex1) {
-          v = row[up1 * P + j1];
-        } else {
-          double acc_a = dmul(A1[0], row[lo1 * P]);
-#pragma unroll
-          for (int m = 1; m < P; ++m) acc_a = dadd(acc_a, dmul(A1[m], row[lo1 * P + m]));
-          double acc_b = dmul(B1[0], row[up1 * P]);
-#pragma unroll
-          for (int m = 1; m < P; ++m) acc_b = dadd(acc_b, dmul(B1[m], row[up1 * P + m]));
-          v = dadd(acc_a, acc_b);
-        }
-        gbuf[r * n1 + x] = v;
-        bad1 |= not_finite(v);
-      }
-    }
-    __syncthreads();
-    // the ring slot has been consumed: refill it
-    if (tid == 0 && prod_j < nchunks) issue_next();
-    // ---- x2 phase: output cells of the chunk, straight to HBM
+    double* out = outb + (j & 1) * (G * cell);
     if (active) {
       const int lead = c.nsrc - c.nout;  // 1 on a plane's first chunk
-      const double* cprev = carry + ((j + 1) & 1) * cell;  // written by chunk j-1
-      double* out = dst + plane * plane_elems + (int64_t)c.first * cell;
-      for (int oc = rg; oc < c.nout; oc += R) {
-        const int sc = oc + lead;  // source cell of the "up" side
-        const double* gu = gbuf + sc * cell;
-        const double* gl = sc > 0 ? gbuf + (sc - 1) * cell : cprev;
-        double gp[P], gc[P];
+      for (int sc = 0; sc < c.nsrc; ++sc) {
+        double g[P][P];
 #pragma unroll
-        for (int m = 0; m < P; ++m) {
-          gp[m] = gl[m * n1 + x];
-          gc[m] = gu[m * n1 + x];
-        }
+        for (int m2 = 0; m2 < P; ++m2) {
+          // x1 sweep of row m2 of source cell sc, this thread's cell (_kernels.pyx:113-123)
+          const double* row = in + (sc * P + m2) * n1;
+          double uu[P];
+          lds_row_cell<P>(row + up_off, uu);
+          if (ex1) {
 #pragma unroll
-        for (int jj = 0; jj < P; ++jj) {
-          double o;
-          if (ex2) {
-            o = gc[jj];
+            for (int jj = 0; jj < P; ++jj) g[m2][jj] = uu[jj];
           } else {
-            double acc_a = dmul(A2[jj][0], gp[0]);
+            double ul[P];
+            lds_row_cell<P>(row + lo_off, ul);
 #pragma unroll
-            for (int m = 1; m < P; ++m) acc_a = dadd(acc_a, dmul(A2[jj][m], gp[m]));
-            double acc_b = dmul(B2[jj][0], gc[0]);
+            for (int jj = 0; jj < P; ++jj) {
+              double acc_a = dmul(A1[jj][0], ul[0]);
 #pragma unroll
-            for (int m = 1; m < P; ++m) acc_b = dadd(acc_b, dmul(B2[jj][m], gc[m]));
-            o = dadd(acc_a, acc_b);
+              for (int m = 1; m < P; ++m) acc_a = dadd(acc_a, dmul(A1[jj][m], ul[m]));
+              double acc_b = dmul(B1[jj][0], uu[0]);
+#pragma unroll
+              for (int m = 1; m < P; ++m) acc_b = dadd(acc_b, dmul(B1[jj][m], uu[m]));
+              g[m2][jj] = dadd(acc_a, acc_b);
+            }
           }
-          bad2 |= not_finite(o);
-          __stcs(out + (int64_t)oc * cell + jj * n1 + x, o);
-        }
-      }
-      // carry g of this chunk's last source cell into the other buffer
-      if (rg == 0) {
-        const double* glast = gbuf + (c.nsrc - 1) * cell;
-        double* cnext = carry + (j & 1) * cell;
 #pragma unroll
-        for (int m = 0; m < P; ++m) cnext[m * n1 + x] = glast[m * n1 + x];
+          for (int jj = 0; jj < P; ++jj) bad1 |= not_finite(g[m2][jj]);
+        }
+        if (sc >= lead) {
+          // x2 sweep for output x2 cell c.first + sc - lead: rows j2, dofs jj of this cell
+          double* otile = out + (sc - lead) * cell + tid * P;
+#pragma unroll
+          for (int j2 = 0; j2 < P; ++j2) {
+            double o[P];
+#pragma unroll
+            for (int jj = 0; jj < P; ++jj) {
+              if (ex2) {
+                o[jj] = g[j2][jj];
+              } else {
+                double acc_a = dmul(A2[j2][0], gp[0][jj]);
+#pragma unroll
+                for (int m = 1; m < P; ++m) acc_a = dadd(acc_a, dmul(A2[j2][m], gp[m][jj]));
+                double acc_b = dmul(B2[j2][0], g[0][jj]);
+#pragma unroll
+                for (int m = 1; m < P; ++m) acc_b = dadd(acc_b, dmul(B2[j2][m], g[m][jj]));
+                o[jj] = dadd(acc_a, acc_b);
+              }
+              bad2 |= not_finite(o[jj]);
+            }
+            if constexpr (P % 2 == 0) {
+#pragma unroll
+              for (int jj = 0; jj < P; jj += 2)
+                *reinterpret_cast<double2*>(otile + j2 * n1 + jj) = make_double2(o[jj], o[jj + 1]);
+            } else {
+#pragma unroll
+              for (int jj = 0; jj < P; ++jj) otile[j2 * n1 + jj] = o[jj];
+            }
+          }
+        }
+#pragma unroll
+        for (int m2 = 0; m2 < P; ++m2)
+#pragma unroll
+          for (int jj = 0; jj < P; ++jj) gp[m2][jj] = g[m2][jj];
       }
     }
-    __syncthreads();  // gbuf and carry[(j+1)&1] are free for chunk j+1
+    fence_proxy_async_smem();
+    if (tid == 0) bulk_wait_read<0>();  // store of chunk j-1 released the other tile
+    __syncthreads();
+    if (tid == 0) {
+      bulk_s2g(dst + plane * plane_elems + (int64_t)c.first * cell, out,
+               (uint32_t)c.nout * cell * 8u);
+      bulk_commit();
+      if (prod_j < nchunks) issue_next();
+    }
     cur.advance(per_plane, C2, q2, nv1);
     if (++st == kXStages) {
       st = 0;
       phase ^= 1u;
     }
   }
+  if (tid == 0) bulk_wait<0>();
   report_flag(bad1, flag1);
   report_flag(bad2, flag2);
 }
@@ -254,22 +279,23 @@ static int launch_xplane(const double* src, double* dst, const int64_t dims[4], 
                          const double* a2, const double* b2, const int64_t* q2,
                          const double* al2, int32_t* f1, int32_t* f2, cudaStream_t st) {
   const int n1 = (int)dims[0];
+  const int C1 = n1 / P;
   const int C2 = (int)(dims[1] / P);
   const int64_t nv1 = dims[2];
   const int64_t nplanes = dims[2] * dims[3];
   if (nplanes == 0) return VPB_OK;
-  if (n1 > 768) {
-    set_error("x rows of %d dofs exceed one CTA", n1);
+  if (C1 > 128) {
+    set_error("x1 lines of %d cells exceed one CTA", C1);
     return VPB_ERR_UNSUPPORTED;
   }
-  static const int env_threads = getenv("VPB_XPLANE_THREADS") ? atoi(getenv("VPB_XPLANE_THREADS")) : 384;
-  static const int env_chunk = getenv("VPB_XPLANE_CHUNK") ? atoi(getenv("VPB_XPLANE_CHUNK")) : 16384;
-  static const int env_smem = getenv("VPB_XPLANE_SMEM") ? atoi(getenv("VPB_XPLANE_SMEM")) : 110 * 1024;
-  const int R = std::max(1, env_threads / n1);  // row groups
-  const int threads = ((n1 * R + 31) / 32) * 32;
+  static const int env_chunk =
+      getenv("VPB_XPLANE_CHUNK") ? atoi(getenv("VPB_XPLANE_CHUNK")) : 8192;
+  static const int env_smem =
+      getenv("VPB_XPLANE_SMEM") ? atoi(getenv("VPB_XPLANE_SMEM")) : 56 * 1024;
+  const int threads = ((C1 + 31) / 32) * 32;
   const size_t cell_bytes = (size_t)P * n1 * 8;
   auto smem_for = [&](int g) {
-    return (size_t)(kXStages + 1) * (g + 1) * cell_bytes + 2 * cell_bytes + kXStages * 8;
+    return (size_t)kXStages * (g + 1) * cell_bytes + 2 * (size_t)g * cell_bytes + kXStages * 8;
   };
   int G = std::max<int>(1, (int)(env_chunk / cell_bytes));
   G = std::min(G, C2);
@@ -292,7 +318,7 @@ static int launch_xplane(const double* src, double* dst, const int64_t dims[4], 
   const int64_t ppb = (nplanes + grid - 1) / grid;
   const int64_t blocks = (nplanes + ppb - 1) / ppb;
   dg_xplane_kernel<P><<<(unsigned)blocks, threads, smem, st>>>(
-      src, dst, n1, C2, G, R, nv1, nplanes, ppb, a1, b1, q1, al1, a2, b2, q2, al2, f1, f2);
+      src, dst, n1, C2, G, nv1, nplanes, ppb, a1, b1, q1, al1, a2, b2, q2, al2, f1, f2);
   return check_launch("dg_xplane_kernel");
 }
 
