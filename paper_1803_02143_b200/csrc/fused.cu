@@ -7,8 +7,8 @@
 // cell c reads the x1-swept values g of source x2 cells c-q2-1 and c-q2, so
 // the plane is consumed in source order starting at s0 = (-q2-1) mod C2:
 //
-//   chunk 0 of a plane:  source cells s0 .. s0+n   -> output cells 0 .. n-1
-//   chunk i > 0:         source cells s0+1+iG ...  -> output cells iG ...
+//   chunk 0 of a plane:  source cell s0 only (prologue, no output)
+//   chunk i > 0:         source cells s0+1+(i-1)G ...  -> output cells (i-1)G ...
 //
 // Per chunk (G x2 cells = G*P rows of n1 dofs):
 //   * TMA 1-D bulk copies (one or two pieces when the source range wraps)
@@ -32,12 +32,12 @@
 
 namespace vpb {
 
-constexpr int kXStages = 4;
+constexpr int kXStages = 6;
 
 struct XChunk {
   int first;    // first output cell
   int nout;     // output cells
-  int nsrc;     // source cells loaded (nout, +1 for the plane's first chunk)
+  int nsrc;     // source cells loaded (1 for the prologue chunk, else nout)
   int s_begin;  // first source cell (mod C2)
 };
 
@@ -54,10 +54,17 @@ struct XCursor {
   }
   __device__ __forceinline__ XChunk chunk(int G, int C2) const {
     XChunk c;
-    c.first = i * G;
+    if (i == 0) {
+      c.first = 0;
+      c.nout = 0;
+      c.nsrc = 1;
+      c.s_begin = s0;
+      return c;
+    }
+    c.first = (i - 1) * G;
     c.nout = min(G, C2 - c.first);
-    c.nsrc = c.nout + (i == 0 ? 1 : 0);
-    int sb = s0 + (i == 0 ? 0 : 1 + c.first);
+    c.nsrc = c.nout;
+    int sb = s0 + 1 + c.first;
     if (sb >= C2) sb -= C2;
     c.s_begin = sb;
     return c;
@@ -94,7 +101,7 @@ __global__ void __launch_bounds__(128)
                      int32_t* __restrict__ flag1, int32_t* __restrict__ flag2) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int cell = P * n1;          // one x2 cell: P rows of n1 dofs
-  const int slot = (G + 1) * cell;  // ring slot (G cells + the plane prologue cell)
+  const int slot = G * cell;        // ring slot
   double* inb = reinterpret_cast<double*>(smem_raw);
   double* outb = inb + kXStages * slot;  // [2][G*cell] staging tiles
   uint64_t* bars = reinterpret_cast<uint64_t*>(outb + 2 * G * cell);
@@ -103,7 +110,7 @@ __global__ void __launch_bounds__(128)
   const int64_t pl_begin = blockIdx.x * planes_per_block;
   const int64_t pl_end = min(nplanes, pl_begin + planes_per_block);
   if (pl_begin >= pl_end) return;
-  const int per_plane = (C2 + G - 1) / G;
+  const int per_plane = 1 + (C2 + G - 1) / G;
   const int64_t nchunks = (pl_end - pl_begin) * per_plane;
   const int64_t plane_elems = (int64_t)C2 * cell;
 
@@ -176,7 +183,6 @@ __global__ void __launch_bounds__(128)
     const double* in = inb + st * slot;
     double* out = outb + (j & 1) * (G * cell);
     if (active) {
-      const int lead = c.nsrc - c.nout;  // 1 on a plane's first chunk
       for (int sc = 0; sc < c.nsrc; ++sc) {
         double g[P][P];
 #pragma unroll
@@ -205,9 +211,9 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
           for (int jj = 0; jj < P; ++jj) bad1 |= not_finite(g[m2][jj]);
         }
-        if (sc >= lead) {
-          // x2 sweep for output x2 cell c.first + sc - lead: rows j2, dofs jj of this cell
-          double* otile = out + (sc - lead) * cell + tid * P;
+        if (c.nout > 0) {
+          // x2 sweep for output x2 cell c.first + sc: rows j2, dofs jj of this cell
+          double* otile = out + sc * cell + tid * P;
 #pragma unroll
           for (int j2 = 0; j2 < P; ++j2) {
             double o[P];
@@ -246,9 +252,11 @@ __global__ void __launch_bounds__(128)
     if (tid == 0) bulk_wait_read<0>();  // store of chunk j-1 released the other tile
     __syncthreads();
     if (tid == 0) {
-      bulk_s2g(dst + plane * plane_elems + (int64_t)c.first * cell, out,
-               (uint32_t)c.nout * cell * 8u);
-      bulk_commit();
+      if (c.nout > 0) {
+        bulk_s2g(dst + plane * plane_elems + (int64_t)c.first * cell, out,
+                 (uint32_t)c.nout * cell * 8u);
+        bulk_commit();
+      }
       if (prod_j < nchunks) issue_next();
     }
     cur.advance(per_plane, C2, q2, nv1);
@@ -295,7 +303,7 @@ static int launch_xplane(const double* src, double* dst, const int64_t dims[4], 
   const int threads = ((C1 + 31) / 32) * 32;
   const size_t cell_bytes = (size_t)P * n1 * 8;
   auto smem_for = [&](int g) {
-    return (size_t)kXStages * (g + 1) * cell_bytes + 2 * (size_t)g * cell_bytes + kXStages * 8;
+    return (size_t)kXStages * g * cell_bytes + 2 * (size_t)g * cell_bytes + kXStages * 8;
   };
   int G = std::max<int>(1, (int)(env_chunk / cell_bytes));
   G = std::min(G, C2);
