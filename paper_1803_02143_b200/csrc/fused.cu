@@ -297,7 +297,7 @@ static int launch_xplane(const double* src, double* dst, const int64_t dims[4], 
     return VPB_ERR_UNSUPPORTED;
   }
   static const int env_chunk =
-      getenv("VPB_XPLANE_CHUNK") ? atoi(getenv("VPB_XPLANE_CHUNK")) : 8192;
+      getenv("VPB_XPLANE_CHUNK") ? atoi(getenv("VPB_XPLANE_CHUNK")) : 4608;
   static const int env_smem =
       getenv("VPB_XPLANE_SMEM") ? atoi(getenv("VPB_XPLANE_SMEM")) : 56 * 1024;
   const int threads = ((C1 + 31) / 32) * 32;
