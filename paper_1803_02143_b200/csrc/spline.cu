@@ -22,6 +22,7 @@
 #include <map>
 #include <mutex>
 
+#include "async_copy.cuh"
 #include "common.cuh"
 
 namespace vpb {
@@ -114,61 +115,121 @@ struct SplineTileArgs {
   int32_t* flag;
 };
 
+constexpr int kSplineBars = 8;  // row groups with their own mbarrier (strided tiles)
+
+// Row stride of the contiguous-axis tile [line][point]: even (16-B aligned
+// bulk destinations) and not a multiple of 16 doubles (few bank conflicts).
+__host__ __device__ __forceinline__ int contig_rs(int n) { return n + 2 - (n & 1); }
+
+// One warp per tile of kSplineT lines; each lane runs the Thomas recurrence
+// of one line in shared memory.  Strided axes: the tile is [point][lane] and
+// every point row (kSplineT consecutive lines, 256 contiguous bytes) arrives
+// by its own bulk copy; the forward elimination consumes row groups as their
+// mbarriers complete, overlapping the solve with the load.  Contiguous axis:
+// [lane][point] rows land by one bulk copy per line.  The evaluation writes
+// HBM coalesced: lane-parallel along the line index (strided) or along the
+// points of each line (contiguous).
 template <bool CONTIG>
 __global__ void __launch_bounds__(kSplineT)
     spline_tile_kernel(SplineTileArgs a) {
-  extern __shared__ __align__(16) double sm[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int T = kSplineT;
-  constexpr int RS = CONTIG ? T + 1 : T;  // row stride of the [point][line] tile
   const int n = a.n;
-  double* tile = sm;                                // n * RS
-  double* wts = tile + (int64_t)n * RS;             // [T][4]
-  int* j0s = reinterpret_cast<int*>(wts + 4 * T);   // [T]
+  const int RS = CONTIG ? contig_rs(n) : T;  // row stride
+  const int YS = CONTIG ? 1 : T;             // stride between points of one line
+  double* tile = reinterpret_cast<double*>(smem_raw);
+  const int tile_elems = CONTIG ? T * RS : n * T;
+  double* wts = tile + tile_elems;                                   // [T][4]
+  int* j0s = reinterpret_cast<int*>(wts + 4 * T);                    // [T]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + ((tile_elems + 4 * T) * 8 + T * 4 + 7) / 8 * 8);
   const int t = threadIdx.x;
   const int64_t L0 = (int64_t)blockIdx.x * T;
   const int lines = (int)min((int64_t)T, a.nlines - L0);
+  const int64_t outer0 = CONTIG ? 0 : L0 / a.S;
+  const int64_t inner0 = CONTIG ? 0 : L0 - outer0 * a.S;
 
-  // ---- stage the tile ----
+  // ---- stage the tile -------------------------------------------------------
+  const bool aligned = ((reinterpret_cast<uintptr_t>(a.src) & 15) == 0);
+  bool bulk;
+  int nbars = 1, rows_per_bar = n;
   if (CONTIG) {
-    const double* base = a.src + L0 * n;
-    const int total = lines * n;
-    for (int e = t; e < total; e += T) {
-      int r = e / n, i = e - r * n;
-      tile[i * RS + r] = __ldcs(base + e);
-    }
-  } else if (t < lines) {
-    const int64_t L = L0 + t;
-    const int64_t outer = L / a.S, inner = L - outer * a.S;
-    const double* base = a.src + outer * a.S * n + inner;
-#pragma unroll 8
-    for (int i = 0; i < n; ++i) tile[i * RS + t] = __ldcs(base + (int64_t)i * a.S);
+    bulk = aligned && (n % 2 == 0);
+  } else {
+    bulk = aligned && lines == T && (a.S % T == 0);
+    nbars = min(kSplineBars, n);
+    rows_per_bar = (n + nbars - 1) / nbars;
+    nbars = (n + rows_per_bar - 1) / rows_per_bar;
   }
-  __syncthreads();
+  if (bulk) {
+    if (t == 0) {
+      for (int b = 0; b < nbars; ++b) mbar_init(bars + b, 1);
+      fence_mbar_init();
+      if (CONTIG) {
+        mbar_arrive_expect_tx(bars, (uint32_t)lines * n * 8u);
+      } else {
+        for (int b = 0; b < nbars; ++b) {
+          const int rows = min(rows_per_bar, n - b * rows_per_bar);
+          mbar_arrive_expect_tx(bars + b, (uint32_t)rows * T * 8u);
+        }
+      }
+    }
+    __syncwarp();
+    if (CONTIG) {
+      if (t < lines) bulk_g2s(tile + t * RS, a.src + (L0 + t) * n, (uint32_t)n * 8u, bars);
+    } else {
+      const double* base = a.src + outer0 * a.S * n + inner0;
+      for (int i = t; i < n; i += T)
+        bulk_g2s(tile + i * T, base + (int64_t)i * a.S, (uint32_t)T * 8u, bars + i / rows_per_bar);
+    }
+  } else {
+    if (CONTIG) {
+      const double* base = a.src + L0 * n;
+      for (int e = t; e < lines * n; e += T) {
+        const int r = e / n, i = e - r * n;
+        tile[r * RS + i] = __ldcs(base + e);
+      }
+    } else if (t < lines) {
+      const int64_t L = L0 + t;
+      const int64_t outer = L / a.S, inner = L - outer * a.S;
+      const double* base = a.src + outer * a.S * n + inner;
+#pragma unroll 8
+      for (int i = 0; i < n; ++i) tile[i * T + t] = __ldcs(base + (int64_t)i * a.S);
+    }
+    __syncwarp();
+  }
 
-  // ---- per-line solve + eval weights ----
+  // ---- per-line solve (Thomas + Sherman-Morrison) and eval weights ----------
   if (t < lines) {
     const double* mult = a.fac;
     const double* denom = a.fac + n;
     const double* rden = a.fac + 2 * n;
     const double* z = a.fac + 3 * n;
     const double sden = a.fac[4 * n], rsden = a.fac[4 * n + 1];
-    double* y = tile + t;
-    double prev = __dmul_rn(6.0, y[0]);
-    y[0] = prev;
-    for (int i = 1; i < n; ++i) {
-      double v = __dsub_rn(__dmul_rn(6.0, y[i * RS]), __dmul_rn(mult[i], prev));
-      y[i * RS] = v;
+    double* y = CONTIG ? tile + t * RS : tile + t;
+    double prev = 0.0;
+    int b = 0;
+    int next_group = 0;  // first row of the next barrier group
+    for (int i = 0; i < n; ++i) {
+      if (bulk && i == next_group) {
+        mbar_wait(bars + b, 0);
+        ++b;
+        next_group += rows_per_bar;
+        if (CONTIG) next_group = n;
+      }
+      const double u6 = __dmul_rn(6.0, y[i * YS]);
+      const double v = i == 0 ? u6 : __dsub_rn(u6, __dmul_rn(__ldg(mult + i), prev));
+      y[i * YS] = v;
       prev = v;
     }
-    prev = div_exact(prev, denom[n - 1], rden[n - 1]);
-    y[(n - 1) * RS] = prev;
+    prev = div_exact(prev, __ldg(denom + n - 1), __ldg(rden + n - 1));
+    y[(n - 1) * YS] = prev;
     for (int i = n - 2; i >= 0; --i) {
-      double v = div_exact(__dsub_rn(y[i * RS], prev), denom[i], rden[i]);
-      y[i * RS] = v;
+      const double v = div_exact(__dsub_rn(y[i * YS], prev), __ldg(denom + i), __ldg(rden + i));
+      y[i * YS] = v;
       prev = v;
     }
-    const double fac = div_exact(__dsub_rn(prev, __dmul_rn(0.25, y[(n - 1) * RS])), sden, rsden);
-    for (int i = 0; i < n; ++i) y[i * RS] = __dsub_rn(y[i * RS], __dmul_rn(fac, z[i]));
+    const double fac = div_exact(__dsub_rn(prev, __dmul_rn(0.25, y[(n - 1) * YS])), sden, rsden);
+    for (int i = 0; i < n; ++i) y[i * YS] = __dsub_rn(y[i * YS], __dmul_rn(fac, __ldg(z + i)));
 
     const int64_t L = L0 + t;
     const int64_t row = a.idx ? a.idx[L] : (L / a.tdiv) % a.tmod;
@@ -181,8 +242,7 @@ __global__ void __launch_bounds__(kSplineT)
       th = 0.0;
     }
     const double omt = __dsub_rn(1.0, th);
-    const double th2 = __dmul_rn(th, th), omt2 = __dmul_rn(omt, omt);
-    wts[4 * t + 0] = __ddiv_rn(__dmul_rn(omt2, omt), 6.0);
+    wts[4 * t + 0] = __ddiv_rn(__dmul_rn(__dmul_rn(omt, omt), omt), 6.0);
     wts[4 * t + 1] = __ddiv_rn(
         __dadd_rn(__dsub_rn(4.0, __dmul_rn(__dmul_rn(6.0, th), th)),
                   __dmul_rn(__dmul_rn(__dmul_rn(3.0, th), th), th)),
@@ -191,42 +251,42 @@ __global__ void __launch_bounds__(kSplineT)
         __dadd_rn(__dsub_rn(4.0, __dmul_rn(__dmul_rn(6.0, omt), omt)),
                   __dmul_rn(__dmul_rn(__dmul_rn(3.0, omt), omt), omt)),
         6.0);
-    wts[4 * t + 3] = __ddiv_rn(__dmul_rn(th2, th), 6.0);
-    (void)omt2;
+    wts[4 * t + 3] = __ddiv_rn(__dmul_rn(__dmul_rn(th, th), th), 6.0);
     j0s[t] = (int)wrap_mod((int64_t)off - 1, n);
   }
-  __syncthreads();
+  __syncwarp();
 
-  // ---- evaluation, coalesced along memory ----
+  // ---- evaluation, coalesced along memory ----------------------------------
   bool bad = false;
   auto eval = [&](int r, int i) -> double {
     const double* w = wts + 4 * r;
+    const double* om = CONTIG ? tile + r * RS : tile + r;
     int j = j0s[r] + i;
     if (j >= n) j -= n;
-    int j1 = j + 1 == n ? 0 : j + 1;
-    int j2 = j1 + 1 == n ? 0 : j1 + 1;
-    int j3 = j2 + 1 == n ? 0 : j2 + 1;
-    double o = __dmul_rn(w[0], tile[j * RS + r]);
-    o = __dadd_rn(o, __dmul_rn(w[1], tile[j1 * RS + r]));
-    o = __dadd_rn(o, __dmul_rn(w[2], tile[j2 * RS + r]));
-    o = __dadd_rn(o, __dmul_rn(w[3], tile[j3 * RS + r]));
+    const int j1 = j + 1 == n ? 0 : j + 1;
+    const int j2 = j1 + 1 == n ? 0 : j1 + 1;
+    const int j3 = j2 + 1 == n ? 0 : j2 + 1;
+    double o = __dmul_rn(w[0], om[j * YS]);
+    o = __dadd_rn(o, __dmul_rn(w[1], om[j1 * YS]));
+    o = __dadd_rn(o, __dmul_rn(w[2], om[j2 * YS]));
+    o = __dadd_rn(o, __dmul_rn(w[3], om[j3 * YS]));
     return o;
   };
   if (CONTIG) {
-    double* base = a.dst + L0 * n;
-    const int total = lines * n;
-    for (int e = t; e < total; e += T) {
-      int r = e / n, i = e - r * n;
-      double o = eval(r, i);
-      bad |= not_finite(o);
-      __stcs(base + e, o);
+    for (int r = 0; r < lines; ++r) {
+      double* out = a.dst + (L0 + r) * n;
+      for (int i = t; i < n; i += T) {
+        const double o = eval(r, i);
+        bad |= not_finite(o);
+        __stcs(out + i, o);
+      }
     }
   } else if (t < lines) {
     const int64_t L = L0 + t;
     const int64_t outer = L / a.S, inner = L - outer * a.S;
     double* base = a.dst + outer * a.S * n + inner;
     for (int i = 0; i < n; ++i) {
-      double o = eval(t, i);
+      const double o = eval(t, i);
       bad |= not_finite(o);
       __stcs(base + (int64_t)i * a.S, o);
     }
@@ -235,8 +295,8 @@ __global__ void __launch_bounds__(kSplineT)
 }
 
 static size_t spline_smem(int n, bool contig) {
-  int rs = contig ? kSplineT + 1 : kSplineT;
-  return (size_t)n * rs * sizeof(double) + 4 * kSplineT * sizeof(double) + kSplineT * sizeof(int);
+  const size_t tile = contig ? (size_t)kSplineT * contig_rs(n) : (size_t)n * kSplineT;
+  return ((tile + 4 * kSplineT) * 8 + kSplineT * 4 + 7) / 8 * 8 + kSplineBars * 8;
 }
 
 static int launch_spline(SplineTileArgs a, bool contig, cudaStream_t st) {
