@@ -206,30 +206,71 @@ __global__ void __launch_bounds__(kSplineT)
     const double* z = a.fac + 3 * n;
     const double sden = a.fac[4 * n], rsden = a.fac[4 * n + 1];
     double* y = CONTIG ? tile + t * RS : tile + t;
-    double prev = 0.0;
+    // Forward elimination y_i = 6u_i - mult_i*y_{i-1}, in blocks of U points:
+    // the U loads are issued before the dependent chain so only the two
+    // fp64 ops per point sit on the critical path.
+    constexpr int U = 8;
     int b = 0;
     int next_group = 0;  // first row of the next barrier group
-    for (int i = 0; i < n; ++i) {
-      if (bulk && i == next_group) {
+    auto wait_rows = [&](int upto) {  // rows [0, upto) landed
+      while (bulk && next_group < upto) {
         mbar_wait(bars + b, 0);
         ++b;
-        next_group += rows_per_bar;
-        if (CONTIG) next_group = n;
+        next_group = CONTIG ? n : next_group + rows_per_bar;
       }
-      const double u6 = __dmul_rn(6.0, y[i * YS]);
-      const double v = i == 0 ? u6 : __dsub_rn(u6, __dmul_rn(__ldg(mult + i), prev));
-      y[i * YS] = v;
-      prev = v;
+    };
+    wait_rows(1);
+    double prev = __dmul_rn(6.0, y[0]);
+    y[0] = prev;
+    int i = 1;
+    for (; i + U <= n; i += U) {
+      wait_rows(i + U);
+      double u[U], m[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        u[k] = y[(i + k) * YS];
+        m[k] = __ldg(mult + i + k);
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        prev = __dsub_rn(__dmul_rn(6.0, u[k]), __dmul_rn(m[k], prev));
+        u[k] = prev;
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) y[(i + k) * YS] = u[k];
     }
+    wait_rows(n);
+    for (; i < n; ++i) {
+      prev = __dsub_rn(__dmul_rn(6.0, y[i * YS]), __dmul_rn(__ldg(mult + i), prev));
+      y[i * YS] = prev;
+    }
+    // Back substitution y_i = (y_i - y_{i+1}) / denom_i
     prev = div_exact(prev, __ldg(denom + n - 1), __ldg(rden + n - 1));
     y[(n - 1) * YS] = prev;
-    for (int i = n - 2; i >= 0; --i) {
-      const double v = div_exact(__dsub_rn(y[i * YS], prev), __ldg(denom + i), __ldg(rden + i));
-      y[i * YS] = v;
-      prev = v;
+    i = n - 2;
+    for (; i - U + 1 >= 0; i -= U) {
+      double v[U], d[U], r[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        v[k] = y[(i - k) * YS];
+        d[k] = __ldg(denom + i - k);
+        r[k] = __ldg(rden + i - k);
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        prev = div_exact(__dsub_rn(v[k], prev), d[k], r[k]);
+        v[k] = prev;
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) y[(i - k) * YS] = v[k];
+    }
+    for (; i >= 0; --i) {
+      prev = div_exact(__dsub_rn(y[i * YS], prev), __ldg(denom + i), __ldg(rden + i));
+      y[i * YS] = prev;
     }
     const double fac = div_exact(__dsub_rn(prev, __dmul_rn(0.25, y[(n - 1) * YS])), sden, rsden);
-    for (int i = 0; i < n; ++i) y[i * YS] = __dsub_rn(y[i * YS], __dmul_rn(fac, __ldg(z + i)));
+#pragma unroll 8
+    for (int k = 0; k < n; ++k) y[k * YS] = __dsub_rn(y[k * YS], __dmul_rn(fac, __ldg(z + k)));
 
     const int64_t L = L0 + t;
     const int64_t row = a.idx ? a.idx[L] : (L / a.tdiv) % a.tmod;
