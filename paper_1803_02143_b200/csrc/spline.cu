@@ -73,15 +73,30 @@ static int get_factors(int64_t n, const double** out) {
     *out = it->second;
     return VPB_OK;
   }
-  double* h = new double[4 * n + 2];
+  const int64_t len = 4 * n + 7;
+  double* h = new double[len];
   double sden;
   host_factors(n, h, h + n, h + 3 * n, &sden);
   for (int64_t i = 0; i < n; ++i) h[2 * n + i] = 1.0 / h[n + i];
   h[4 * n] = sden;
   h[4 * n + 1] = 1.0 / sden;
+  // The elimination factors reach an exact floating-point fixed point after a
+  // few dozen rows.  kf: mult[i] == mc for all i in [kf, n-1]; kb: denom[i] ==
+  // dc (and rden == rc) for all i in [kb, n-2].  Past those rows the kernel
+  // keeps the factors in registers instead of loading them per point.
+  const double mc = h[n - 1], dc = n >= 2 ? h[n + n - 2] : h[n];
+  int64_t kf = n - 1;
+  while (kf > 1 && h[kf - 1] == mc) --kf;
+  int64_t kb = n - 2 >= 0 ? n - 2 : 0;
+  while (kb > 0 && h[n + kb - 1] == dc) --kb;
+  h[4 * n + 2] = (double)kf;
+  h[4 * n + 3] = (double)kb;
+  h[4 * n + 4] = mc;
+  h[4 * n + 5] = dc;
+  h[4 * n + 6] = 1.0 / dc;
   double* d = nullptr;
-  if (cudaMalloc(&d, (4 * n + 2) * sizeof(double)) != cudaSuccess ||
-      cudaMemcpy(d, h, (4 * n + 2) * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) {
+  if (cudaMalloc(&d, len * sizeof(double)) != cudaSuccess ||
+      cudaMemcpy(d, h, len * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) {
     delete[] h;
     return check_launch("spline factors upload");
   }
@@ -198,17 +213,21 @@ __global__ void __launch_bounds__(kSplineT)
     __syncwarp();
   }
 
-  // ---- per-line solve (Thomas + Sherman-Morrison) and eval weights ----------
+  // ---- per-line solve (Thomas + Sherman-Morrison) and evaluation -----------
+  bool bad = false;
   if (t < lines) {
     const double* mult = a.fac;
     const double* denom = a.fac + n;
     const double* rden = a.fac + 2 * n;
     const double* z = a.fac + 3 * n;
     const double sden = a.fac[4 * n], rsden = a.fac[4 * n + 1];
+    const int kf = (int)a.fac[4 * n + 2], kb = (int)a.fac[4 * n + 3];
+    const double mc = a.fac[4 * n + 4], dc = a.fac[4 * n + 5], rc = a.fac[4 * n + 6];
     double* y = CONTIG ? tile + t * RS : tile + t;
     // Forward elimination y_i = 6u_i - mult_i*y_{i-1}, in blocks of U points:
     // the U loads are issued before the dependent chain so only the two
-    // fp64 ops per point sit on the critical path.
+    // fp64 ops per point sit on the critical path; past row kf the factor is
+    // the exact fixed point mc.
     constexpr int U = 8;
     int b = 0;
     int next_group = 0;  // first row of the next barrier group
@@ -226,10 +245,11 @@ __global__ void __launch_bounds__(kSplineT)
     for (; i + U <= n; i += U) {
       wait_rows(i + U);
       double u[U], m[U];
+      const bool cst = i >= kf;
 #pragma unroll
       for (int k = 0; k < U; ++k) {
         u[k] = y[(i + k) * YS];
-        m[k] = __ldg(mult + i + k);
+        m[k] = cst ? mc : __ldg(mult + i + k);
       }
 #pragma unroll
       for (int k = 0; k < U; ++k) {
@@ -244,17 +264,18 @@ __global__ void __launch_bounds__(kSplineT)
       prev = __dsub_rn(__dmul_rn(6.0, y[i * YS]), __dmul_rn(__ldg(mult + i), prev));
       y[i * YS] = prev;
     }
-    // Back substitution y_i = (y_i - y_{i+1}) / denom_i
+    // Back substitution y_i = (y_i - y_{i+1}) / denom_i (constant past kb)
     prev = div_exact(prev, __ldg(denom + n - 1), __ldg(rden + n - 1));
     y[(n - 1) * YS] = prev;
     i = n - 2;
     for (; i - U + 1 >= 0; i -= U) {
       double v[U], d[U], r[U];
+      const bool cst = i - U + 1 >= kb;
 #pragma unroll
       for (int k = 0; k < U; ++k) {
         v[k] = y[(i - k) * YS];
-        d[k] = __ldg(denom + i - k);
-        r[k] = __ldg(rden + i - k);
+        d[k] = cst ? dc : __ldg(denom + i - k);
+        r[k] = cst ? rc : __ldg(rden + i - k);
       }
 #pragma unroll
       for (int k = 0; k < U; ++k) {
@@ -272,6 +293,7 @@ __global__ void __launch_bounds__(kSplineT)
 #pragma unroll 8
     for (int k = 0; k < n; ++k) y[k * YS] = __dsub_rn(y[k * YS], __dmul_rn(fac, __ldg(z + k)));
 
+    // evaluation weights (_kernels.pyx:62-87)
     const int64_t L = L0 + t;
     const int64_t row = a.idx ? a.idx[L] : (L / a.tdiv) % a.tmod;
     const double shift = __dmul_rn(a.values[row], a.scale);
@@ -283,53 +305,66 @@ __global__ void __launch_bounds__(kSplineT)
       th = 0.0;
     }
     const double omt = __dsub_rn(1.0, th);
-    wts[4 * t + 0] = __ddiv_rn(__dmul_rn(__dmul_rn(omt, omt), omt), 6.0);
-    wts[4 * t + 1] = __ddiv_rn(
-        __dadd_rn(__dsub_rn(4.0, __dmul_rn(__dmul_rn(6.0, th), th)),
-                  __dmul_rn(__dmul_rn(__dmul_rn(3.0, th), th), th)),
-        6.0);
-    wts[4 * t + 2] = __ddiv_rn(
-        __dadd_rn(__dsub_rn(4.0, __dmul_rn(__dmul_rn(6.0, omt), omt)),
-                  __dmul_rn(__dmul_rn(__dmul_rn(3.0, omt), omt), omt)),
-        6.0);
-    wts[4 * t + 3] = __ddiv_rn(__dmul_rn(__dmul_rn(th, th), th), 6.0);
-    j0s[t] = (int)wrap_mod((int64_t)off - 1, n);
+    const double w0 = __ddiv_rn(__dmul_rn(__dmul_rn(omt, omt), omt), 6.0);
+    const double w1 = __ddiv_rn(__dadd_rn(__dsub_rn(4.0, __dmul_rn(__dmul_rn(6.0, th), th)),
+                                          __dmul_rn(__dmul_rn(__dmul_rn(3.0, th), th), th)),
+                                6.0);
+    const double w2 = __ddiv_rn(__dadd_rn(__dsub_rn(4.0, __dmul_rn(__dmul_rn(6.0, omt), omt)),
+                                          __dmul_rn(__dmul_rn(__dmul_rn(3.0, omt), omt), omt)),
+                                6.0);
+    const double w3 = __ddiv_rn(__dmul_rn(__dmul_rn(th, th), th), 6.0);
+    const int j0 = (int)wrap_mod((int64_t)off - 1, n);
+    j0s[t] = j0;
+
+    // out_i = w0 om[j0+i] + w1 om[j0+i+1] + w2 om[j0+i+2] + w3 om[j0+i+3]
+    // with a 4-value sliding window (one smem load per output).  On the
+    // contiguous axis out_i overwrites om[j0+i] in place (rotated by j0); the
+    // three window values that wrap past the start are saved first.
+    int jn = j0;
+    auto nxt = [&]() {
+      const double v = y[jn * YS];
+      if (++jn == n) jn = 0;
+      return v;
+    };
+    const double s0 = nxt(), s1 = nxt(), s2 = nxt();
+    double c0 = s0, c1 = s1, c2 = s2;
+    int64_t obase = 0;
+    if (!CONTIG) {
+      const int64_t outer = L / a.S, inner = L - outer * a.S;
+      obase = outer * a.S * n + inner;
+    }
+    int p = j0;  // position of out_i in the rotated in-place row
+    for (int k = 0; k < n; ++k) {
+      const int back = k - (n - 3);
+      const double c3 = back < 0 ? nxt() : (back == 0 ? s0 : (back == 1 ? s1 : s2));
+      double o = __dmul_rn(w0, c0);
+      o = __dadd_rn(o, __dmul_rn(w1, c1));
+      o = __dadd_rn(o, __dmul_rn(w2, c2));
+      o = __dadd_rn(o, __dmul_rn(w3, c3));
+      bad |= not_finite(o);
+      if (CONTIG) {
+        y[p] = o;
+        if (++p == n) p = 0;
+      } else {
+        __stcs(a.dst + obase + (int64_t)k * a.S, o);
+      }
+      c0 = c1;
+      c1 = c2;
+      c2 = c3;
+    }
   }
   __syncwarp();
-
-  // ---- evaluation, coalesced along memory ----------------------------------
-  bool bad = false;
-  auto eval = [&](int r, int i) -> double {
-    const double* w = wts + 4 * r;
-    const double* om = CONTIG ? tile + r * RS : tile + r;
-    int j = j0s[r] + i;
-    if (j >= n) j -= n;
-    const int j1 = j + 1 == n ? 0 : j + 1;
-    const int j2 = j1 + 1 == n ? 0 : j1 + 1;
-    const int j3 = j2 + 1 == n ? 0 : j2 + 1;
-    double o = __dmul_rn(w[0], om[j * YS]);
-    o = __dadd_rn(o, __dmul_rn(w[1], om[j1 * YS]));
-    o = __dadd_rn(o, __dmul_rn(w[2], om[j2 * YS]));
-    o = __dadd_rn(o, __dmul_rn(w[3], om[j3 * YS]));
-    return o;
-  };
   if (CONTIG) {
+    // rows hold out rotated by j0: write them out coalesced
     for (int r = 0; r < lines; ++r) {
       double* out = a.dst + (L0 + r) * n;
-      for (int i = t; i < n; i += T) {
-        const double o = eval(r, i);
-        bad |= not_finite(o);
-        __stcs(out + i, o);
+      const double* row = tile + r * RS;
+      const int jr = j0s[r];
+      for (int k = t; k < n; k += T) {
+        int q = jr + k;
+        if (q >= n) q -= n;
+        __stcs(out + k, row[q]);
       }
-    }
-  } else if (t < lines) {
-    const int64_t L = L0 + t;
-    const int64_t outer = L / a.S, inner = L - outer * a.S;
-    double* base = a.dst + outer * a.S * n + inner;
-    for (int i = 0; i < n; ++i) {
-      const double o = eval(t, i);
-      bad |= not_finite(o);
-      __stcs(base + (int64_t)i * a.S, o);
     }
   }
   report_flag(bad, a.flag);
