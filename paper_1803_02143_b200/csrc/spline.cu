@@ -19,6 +19,7 @@
 // is sized to keep several CTAs per SM), then the evaluation is remapped so
 // that stores are coalesced along the memory-contiguous direction.
 #include <algorithm>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 
@@ -27,7 +28,8 @@
 
 namespace vpb {
 
-constexpr int kSplineT = 32;  // lines per CTA
+constexpr int kSplineT = 32;   // lines per CTA
+constexpr int kPcrLevels = 5;  // cyclic-reduction levels (strides 1..16)
 
 struct SplineFactors {
   int64_t n;
@@ -73,7 +75,7 @@ static int get_factors(int64_t n, const double** out) {
     *out = it->second;
     return VPB_OK;
   }
-  const int64_t len = 4 * n + 7;
+  const int64_t len = 4 * n + 8 + kPcrLevels;
   double* h = new double[len];
   double sden;
   host_factors(n, h, h + n, h + 3 * n, &sden);
@@ -94,6 +96,25 @@ static int get_factors(int64_t n, const double** out) {
   h[4 * n + 4] = mc;
   h[4 * n + 5] = dc;
   h[4 * n + 6] = 1.0 / dc;
+  // Parallel cyclic reduction of w_{i-1} + 4 w_i + w_{i+1} = u_i (constant
+  // coefficients, periodic): level l eliminates stride 2^l neighbours with
+  // k_l = a_l/b_l, a_{l+1} = -a_l k_l, b_{l+1} = b_l - 2 a_l k_l.  After
+  // kPcrLevels the coupling |a/b| is ~5e-19, and the solution is d/b (plus
+  // 2a when the final stride wraps onto the row itself).  The 6 of the
+  // right-hand side 6u is folded into the final scale.
+  {
+    double pa = 1.0, pb = 4.0;
+    for (int l = 0; l < kPcrLevels; ++l) {
+      const double k = pa / pb;
+      h[4 * n + 7 + l] = k;
+      const double na = -pa * k;
+      const double nb = pb - 2.0 * pa * k;
+      pa = na;
+      pb = nb;
+    }
+    const bool wraps = ((1LL << kPcrLevels) % n) == 0;
+    h[4 * n + 7 + kPcrLevels] = 6.0 / (wraps ? pb + 2.0 * pa : pb);
+  }
   double* d = nullptr;
   if (cudaMalloc(&d, len * sizeof(double)) != cudaSuccess ||
       cudaMemcpy(d, h, len * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) {
@@ -144,7 +165,46 @@ __host__ __device__ __forceinline__ int contig_rs(int n) { return n + 2 - (n & 1
 // [lane][point] rows land by one bulk copy per line.  The evaluation writes
 // HBM coalesced: lane-parallel along the line index (strided) or along the
 // points of each line (contiguous).
-template <bool CONTIG>
+// One level of cyclic reduction with stride S, in place on one line:
+//   y_i <- y_i - k (y_{i-S} + y_{i+S})   (indices mod n), all i from OLD values.
+// Old y_{i-S} comes from a register ring (the value loaded S points earlier),
+// old y_{i+S} from shared memory except in the last block, where it wrapped
+// onto the first block (already overwritten) and comes from `first`.
+// Requires n % S == 0 and n >= 2S.
+template <int S>
+__device__ __forceinline__ void pcr_level(double* y, const int YS, const int n, const double k) {
+  double first[S], ring[S];
+#pragma unroll
+  for (int r = 0; r < S; ++r) {
+    first[r] = y[r * YS];
+    ring[r] = y[(n - S + r) * YS];
+  }
+#pragma unroll
+  for (int r = 0; r < S; ++r) {  // block 0: old y_i is first[r]
+    const double c = first[r];
+    const double b = y[(r + S) * YS];
+    y[r * YS] = __fma_rn(-k, ring[r] + b, c);
+    ring[r] = c;
+  }
+  for (int i0 = S; i0 < n - S; i0 += S) {
+#pragma unroll
+    for (int r = 0; r < S; ++r) {
+      const int i = i0 + r;
+      const double c = y[i * YS];
+      const double b = y[(i + S) * YS];
+      y[i * YS] = __fma_rn(-k, ring[r] + b, c);
+      ring[r] = c;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < S; ++r) {  // last block: y_{i+S} wrapped to first[r]
+    const int i = n - S + r;
+    const double c = y[i * YS];
+    y[i * YS] = __fma_rn(-k, ring[r] + first[r], c);
+  }
+}
+
+template <bool CONTIG, bool PCR>
 __global__ void __launch_bounds__(kSplineT)
     spline_tile_kernel(SplineTileArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -224,6 +284,19 @@ __global__ void __launch_bounds__(kSplineT)
     const int kf = (int)a.fac[4 * n + 2], kb = (int)a.fac[4 * n + 3];
     const double mc = a.fac[4 * n + 4], dc = a.fac[4 * n + 5], rc = a.fac[4 * n + 6];
     double* y = CONTIG ? tile + t * RS : tile + t;
+    double wscale = 1.0;
+    if constexpr (PCR) {
+      // parallel cyclic reduction in shared memory: no serial chain per line
+      if (bulk)
+        for (int bb = 0; bb < nbars; ++bb) mbar_wait(bars + bb, 0);
+      const double* pk = a.fac + 4 * n + 7;
+      pcr_level<1>(y, YS, n, pk[0]);
+      pcr_level<2>(y, YS, n, pk[1]);
+      pcr_level<4>(y, YS, n, pk[2]);
+      pcr_level<8>(y, YS, n, pk[3]);
+      pcr_level<16>(y, YS, n, pk[4]);
+      wscale = pk[kPcrLevels];  // 6 / b_L: folded into the evaluation weights
+    } else {
     // Forward elimination y_i = 6u_i - mult_i*y_{i-1}, in blocks of U points:
     // the U loads are issued before the dependent chain so only the two
     // fp64 ops per point sit on the critical path; past row kf the factor is
@@ -292,6 +365,7 @@ __global__ void __launch_bounds__(kSplineT)
     const double fac = div_exact(__dsub_rn(prev, __dmul_rn(0.25, y[(n - 1) * YS])), sden, rsden);
 #pragma unroll 8
     for (int k = 0; k < n; ++k) y[k * YS] = __dsub_rn(y[k * YS], __dmul_rn(fac, __ldg(z + k)));
+    }  // Thomas
 
     // evaluation weights (_kernels.pyx:62-87)
     const int64_t L = L0 + t;
@@ -305,14 +379,20 @@ __global__ void __launch_bounds__(kSplineT)
       th = 0.0;
     }
     const double omt = __dsub_rn(1.0, th);
-    const double w0 = __ddiv_rn(__dmul_rn(__dmul_rn(omt, omt), omt), 6.0);
-    const double w1 = __ddiv_rn(__dadd_rn(__dsub_rn(4.0, __dmul_rn(__dmul_rn(6.0, th), th)),
+    double w0 = __ddiv_rn(__dmul_rn(__dmul_rn(omt, omt), omt), 6.0);
+    double w1 = __ddiv_rn(__dadd_rn(__dsub_rn(4.0, __dmul_rn(__dmul_rn(6.0, th), th)),
                                           __dmul_rn(__dmul_rn(__dmul_rn(3.0, th), th), th)),
                                 6.0);
-    const double w2 = __ddiv_rn(__dadd_rn(__dsub_rn(4.0, __dmul_rn(__dmul_rn(6.0, omt), omt)),
+    double w2 = __ddiv_rn(__dadd_rn(__dsub_rn(4.0, __dmul_rn(__dmul_rn(6.0, omt), omt)),
                                           __dmul_rn(__dmul_rn(__dmul_rn(3.0, omt), omt), omt)),
                                 6.0);
-    const double w3 = __ddiv_rn(__dmul_rn(__dmul_rn(th, th), th), 6.0);
+    double w3 = __ddiv_rn(__dmul_rn(__dmul_rn(th, th), th), 6.0);
+    if constexpr (PCR) {
+      w0 *= wscale;
+      w1 *= wscale;
+      w2 *= wscale;
+      w3 *= wscale;
+    }
     const int j0 = (int)wrap_mod((int64_t)off - 1, n);
     j0s[t] = j0;
 
@@ -375,7 +455,10 @@ static size_t spline_smem(int n, bool contig) {
   return ((tile + 4 * kSplineT) * 8 + kSplineT * 4 + 7) / 8 * 8 + kSplineBars * 8;
 }
 
-static int launch_spline(SplineTileArgs a, bool contig, cudaStream_t st) {
+// exact: Thomas + Sherman-Morrison, bitwise the reference (plugin API);
+// otherwise parallel cyclic reduction when the line length allows it
+// (n % 16 == 0, n >= 32), within ~4e-16 relative of the reference.
+static int launch_spline(SplineTileArgs a, bool contig, bool exact, cudaStream_t st) {
   if (a.nlines == 0) return VPB_OK;
   size_t smem = spline_smem(a.n, contig);
   if (smem > 220 * 1024) {
@@ -386,17 +469,30 @@ static int launch_spline(SplineTileArgs a, bool contig, cudaStream_t st) {
   if (rc) return rc;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(spline_tile_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         220 * 1024);
-    cudaFuncSetAttribute(spline_tile_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         220 * 1024);
+    cudaFuncSetAttribute(spline_tile_kernel<true, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(spline_tile_kernel<false, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(spline_tile_kernel<true, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(spline_tile_kernel<false, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr = true;
   }
+  static const bool force_exact = getenv("VPB_SPLINE_EXACT") != nullptr;
+  const bool pcr = !exact && !force_exact && a.n % 16 == 0 && a.n >= 32;
   int64_t blocks = (a.nlines + kSplineT - 1) / kSplineT;
-  if (contig)
-    spline_tile_kernel<true><<<(unsigned)blocks, kSplineT, smem, st>>>(a);
-  else
-    spline_tile_kernel<false><<<(unsigned)blocks, kSplineT, smem, st>>>(a);
+  if (contig) {
+    if (pcr)
+      spline_tile_kernel<true, true><<<(unsigned)blocks, kSplineT, smem, st>>>(a);
+    else
+      spline_tile_kernel<true, false><<<(unsigned)blocks, kSplineT, smem, st>>>(a);
+  } else {
+    if (pcr)
+      spline_tile_kernel<false, true><<<(unsigned)blocks, kSplineT, smem, st>>>(a);
+    else
+      spline_tile_kernel<false, false><<<(unsigned)blocks, kSplineT, smem, st>>>(a);
+  }
   return check_launch("spline_tile_kernel");
 }
 
@@ -431,7 +527,7 @@ extern "C" int vpb_spline_sweep_contig(const double* lines, double* out, int64_t
   VPB_REQUIRE(lines != out, "out must not alias lines");
   VPB_REQUIRE(idx != nullptr && table != nullptr && ntable > 0, "table index required");
   SplineTileArgs a{lines, out, nlines, (int)n, 1, idx, 1, ntable, table, 1.0, h, nullptr, nullptr};
-  return launch_spline(a, true, (cudaStream_t)stream);
+  return launch_spline(a, true, true, (cudaStream_t)stream);
 }
 
 extern "C" int vpb_spline_sweep_strided(double* view, const int64_t shape[4],
@@ -476,7 +572,7 @@ extern "C" int vpb_spline_sweep_axis(int32_t axis, const double* src, double* ds
   if (axis == 0) {
     a.tdiv = n2;  // lines = (iv2, iv1, ix2), row = iv1
     a.tmod = nv1;
-    return launch_spline(a, true, (cudaStream_t)stream);
+    return launch_spline(a, true, false, (cudaStream_t)stream);
   }
   if (axis == 1) {
     a.S = n1;
@@ -491,5 +587,5 @@ extern "C" int vpb_spline_sweep_axis(int32_t axis, const double* src, double* ds
     a.tdiv = 1;
     a.tmod = n1 * n2;
   }
-  return launch_spline(a, false, (cudaStream_t)stream);
+  return launch_spline(a, false, false, (cudaStream_t)stream);
 }
