@@ -167,40 +167,38 @@ __host__ __device__ __forceinline__ int contig_rs(int n) { return n + 2 - (n & 1
 // points of each line (contiguous).
 // One level of cyclic reduction with stride S, in place on one line:
 //   y_i <- y_i - k (y_{i-S} + y_{i+S})   (indices mod n), all i from OLD values.
-// Old y_{i-S} comes from a register ring (the value loaded S points earlier),
-// old y_{i+S} from shared memory except in the last block, where it wrapped
-// onto the first block (already overwritten) and comes from `first`.
-// Requires n % S == 0 and n >= 2S.
+// Points go in blocks of B = 16: the block's old values (and the S values
+// past it) are loaded before any of its results is stored, so the loads are
+// not serialised behind the stores.  Old y_{i-S} of the block's first S
+// points comes from a register ring (the previous block's tail); in the last
+// block y_{i+S} wrapped onto the first block and comes from `first`.
+// Requires n % 16 == 0 and n >= 2S.
 template <int S>
 __device__ __forceinline__ void pcr_level(double* y, const int YS, const int n, const double k) {
+  constexpr int B = 16;
   double first[S], ring[S];
 #pragma unroll
   for (int r = 0; r < S; ++r) {
     first[r] = y[r * YS];
     ring[r] = y[(n - S + r) * YS];
   }
+  for (int i0 = 0; i0 < n; i0 += B) {
+    const bool last = i0 + B == n;
+    double c[B], nb[S], o[B];
 #pragma unroll
-  for (int r = 0; r < S; ++r) {  // block 0: old y_i is first[r]
-    const double c = first[r];
-    const double b = y[(r + S) * YS];
-    y[r * YS] = __fma_rn(-k, ring[r] + b, c);
-    ring[r] = c;
-  }
-  for (int i0 = S; i0 < n - S; i0 += S) {
+    for (int r = 0; r < B; ++r) c[r] = y[(i0 + r) * YS];
 #pragma unroll
-    for (int r = 0; r < S; ++r) {
-      const int i = i0 + r;
-      const double c = y[i * YS];
-      const double b = y[(i + S) * YS];
-      y[i * YS] = __fma_rn(-k, ring[r] + b, c);
-      ring[r] = c;
+    for (int r = 0; r < S; ++r) nb[r] = last ? first[r] : y[(i0 + B + r) * YS];
+#pragma unroll
+    for (int r = 0; r < B; ++r) {
+      const double lo = r < S ? ring[r] : c[r - S];
+      const double hi = r + S < B ? c[r + S] : nb[r + S - B];
+      o[r] = __fma_rn(-k, lo + hi, c[r]);
     }
-  }
 #pragma unroll
-  for (int r = 0; r < S; ++r) {  // last block: y_{i+S} wrapped to first[r]
-    const int i = n - S + r;
-    const double c = y[i * YS];
-    y[i * YS] = __fma_rn(-k, ring[r] + first[r], c);
+    for (int r = 0; r < S; ++r) ring[r] = c[B - S + r];
+#pragma unroll
+    for (int r = 0; r < B; ++r) y[(i0 + r) * YS] = o[r];
   }
 }
 
@@ -400,6 +398,8 @@ __global__ void __launch_bounds__(kSplineT)
     // with a 4-value sliding window (one smem load per output).  On the
     // contiguous axis out_i overwrites om[j0+i] in place (rotated by j0); the
     // three window values that wrap past the start are saved first.
+    // (blocks of E outputs: the window values of a block are loaded before
+    //  its in-place stores so loads are not serialised behind them)
     int jn = j0;
     auto nxt = [&]() {
       const double v = y[jn * YS];
@@ -414,23 +414,45 @@ __global__ void __launch_bounds__(kSplineT)
       obase = outer * a.S * n + inner;
     }
     int p = j0;  // position of out_i in the rotated in-place row
-    for (int k = 0; k < n; ++k) {
-      const int back = k - (n - 3);
-      const double c3 = back < 0 ? nxt() : (back == 0 ? s0 : (back == 1 ? s1 : s2));
+    auto emit = [&](int k, double c3) {
       double o = __dmul_rn(w0, c0);
       o = __dadd_rn(o, __dmul_rn(w1, c1));
       o = __dadd_rn(o, __dmul_rn(w2, c2));
       o = __dadd_rn(o, __dmul_rn(w3, c3));
+      c0 = c1;
+      c1 = c2;
+      c2 = c3;
       bad |= not_finite(o);
+      return o;
+    };
+    constexpr int E = 16;
+    int k = 0;
+    for (; k + E <= n - 3; k += E) {
+      double v[E], o[E];
+#pragma unroll
+      for (int r = 0; r < E; ++r) v[r] = nxt();
+#pragma unroll
+      for (int r = 0; r < E; ++r) o[r] = emit(k + r, v[r]);
+#pragma unroll
+      for (int r = 0; r < E; ++r) {
+        if (CONTIG) {
+          y[p] = o[r];
+          if (++p == n) p = 0;
+        } else {
+          __stcs(a.dst + obase + (int64_t)(k + r) * a.S, o[r]);
+        }
+      }
+    }
+    for (; k < n; ++k) {
+      const int back = k - (n - 3);
+      const double c3 = back < 0 ? nxt() : (back == 0 ? s0 : (back == 1 ? s1 : s2));
+      const double o = emit(k, c3);
       if (CONTIG) {
         y[p] = o;
         if (++p == n) p = 0;
       } else {
         __stcs(a.dst + obase + (int64_t)k * a.S, o);
       }
-      c0 = c1;
-      c1 = c2;
-      c2 = c3;
     }
   }
   __syncwarp();
