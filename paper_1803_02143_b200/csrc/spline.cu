@@ -246,13 +246,18 @@ __global__ void __launch_bounds__(kSplineT)
         }
       }
     }
-    __syncwarp();
-    if (CONTIG) {
-      if (t < lines) bulk_g2s(tile + t * RS, a.src + (L0 + t) * n, (uint32_t)n * 8u, bars);
-    } else {
-      const double* base = a.src + outer0 * a.S * n + inner0;
-      for (int i = t; i < n; i += T)
-        bulk_g2s(tile + i * T, base + (int64_t)i * a.S, (uint32_t)T * 8u, bars + i / rows_per_bar);
+    // one lane issues every copy (a lane-divergent bulk copy compiles to an
+    // elect-and-broadcast loop over the lanes)
+    if (t == 0) {
+      if (CONTIG) {
+        for (int r = 0; r < lines; ++r)
+          bulk_g2s(tile + r * RS, a.src + (L0 + r) * n, (uint32_t)n * 8u, bars);
+      } else {
+        const double* base = a.src + outer0 * a.S * n + inner0;
+        for (int i = 0; i < n; ++i)
+          bulk_g2s(tile + i * T, base + (int64_t)i * a.S, (uint32_t)T * 8u,
+                   bars + i / rows_per_bar);
+      }
     }
   } else {
     if (CONTIG) {
