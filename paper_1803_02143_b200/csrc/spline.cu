@@ -20,11 +20,13 @@
 // that stores are coalesced along the memory-contiguous direction.
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <map>
 #include <mutex>
 
 #include "async_copy.cuh"
 #include "common.cuh"
+#include "tensormap.cuh"
 
 namespace vpb {
 
@@ -149,6 +151,7 @@ struct SplineTileArgs {
   double scale, h;
   const double* fac;
   int32_t* flag;
+  int use_tma;  // strided tiles: one TMA tensor copy per tile (tmap valid)
 };
 
 constexpr int kSplineBars = 8;  // row groups with their own mbarrier (strided tiles)
@@ -204,7 +207,7 @@ __device__ __forceinline__ void pcr_level(double* y, const int YS, const int n, 
 
 template <bool CONTIG, bool PCR>
 __global__ void __launch_bounds__(kSplineT)
-    spline_tile_kernel(SplineTileArgs a) {
+    spline_tile_kernel(SplineTileArgs a, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int T = kSplineT;
   const int n = a.n;
@@ -229,9 +232,14 @@ __global__ void __launch_bounds__(kSplineT)
     bulk = aligned && (n % 2 == 0);
   } else {
     bulk = aligned && lines == T && (a.S % T == 0);
-    nbars = min(kSplineBars, n);
-    rows_per_bar = (n + nbars - 1) / nbars;
-    nbars = (n + rows_per_bar - 1) / rows_per_bar;
+    if (a.use_tma) {
+      nbars = 1;
+      rows_per_bar = n;
+    } else {
+      nbars = min(kSplineBars, n);
+      rows_per_bar = (n + nbars - 1) / nbars;
+      nbars = (n + rows_per_bar - 1) / rows_per_bar;
+    }
   }
   if (bulk) {
     if (t == 0) {
@@ -246,18 +254,19 @@ __global__ void __launch_bounds__(kSplineT)
         }
       }
     }
-    // one lane issues every copy (a lane-divergent bulk copy compiles to an
-    // elect-and-broadcast loop over the lanes)
-    if (t == 0) {
-      if (CONTIG) {
+    if (CONTIG) {
+      if (t == 0)
         for (int r = 0; r < lines; ++r)
           bulk_g2s(tile + r * RS, a.src + (L0 + r) * n, (uint32_t)n * 8u, bars);
-      } else {
-        const double* base = a.src + outer0 * a.S * n + inner0;
-        for (int i = 0; i < n; ++i)
-          bulk_g2s(tile + i * T, base + (int64_t)i * a.S, (uint32_t)T * 8u,
-                   bars + i / rows_per_bar);
-      }
+    } else if (a.use_tma) {
+      // the whole [n][32] tile in one (or two, n > 256) TMA tensor copies
+      if (t == 0)
+        for (int r0 = 0; r0 < n; r0 += 256)
+          tma_load_3d(tile + r0 * T, &tmap, (int)inner0, r0, (int)outer0, bars);
+    } else {
+      const double* base = a.src + outer0 * a.S * n + inner0;
+      for (int i = t; i < n; i += T)
+        bulk_g2s(tile + i * T, base + (int64_t)i * a.S, (uint32_t)T * 8u, bars + i / rows_per_bar);
     }
   } else {
     if (CONTIG) {
@@ -509,16 +518,28 @@ static int launch_spline(SplineTileArgs a, bool contig, bool exact, cudaStream_t
   static const bool force_exact = getenv("VPB_SPLINE_EXACT") != nullptr;
   const bool pcr = !exact && !force_exact && a.n % 16 == 0 && a.n >= 32;
   int64_t blocks = (a.nlines + kSplineT - 1) / kSplineT;
+  CUtensorMap tmap;
+  memset(&tmap, 0, sizeof(tmap));
+  a.use_tma = 0;
+  if (!contig && a.S % kSplineT == 0 && a.S % 2 == 0 &&
+      (reinterpret_cast<uintptr_t>(a.src) & 15) == 0 && a.nlines % a.S == 0) {
+    const uint64_t O = (uint64_t)(a.nlines / a.S);
+    a.use_tma = encode_tmap_3d(&tmap, a.src, (uint64_t)a.S, (uint64_t)a.n, O,
+                               (uint64_t)a.S * 8, (uint64_t)a.S * a.n * 8, kSplineT,
+                               (uint32_t)std::min(a.n, 256), 1)
+                    ? 1
+                    : 0;
+  }
   if (contig) {
     if (pcr)
-      spline_tile_kernel<true, true><<<(unsigned)blocks, kSplineT, smem, st>>>(a);
+      spline_tile_kernel<true, true><<<(unsigned)blocks, kSplineT, smem, st>>>(a, tmap);
     else
-      spline_tile_kernel<true, false><<<(unsigned)blocks, kSplineT, smem, st>>>(a);
+      spline_tile_kernel<true, false><<<(unsigned)blocks, kSplineT, smem, st>>>(a, tmap);
   } else {
     if (pcr)
-      spline_tile_kernel<false, true><<<(unsigned)blocks, kSplineT, smem, st>>>(a);
+      spline_tile_kernel<false, true><<<(unsigned)blocks, kSplineT, smem, st>>>(a, tmap);
     else
-      spline_tile_kernel<false, false><<<(unsigned)blocks, kSplineT, smem, st>>>(a);
+      spline_tile_kernel<false, false><<<(unsigned)blocks, kSplineT, smem, st>>>(a, tmap);
   }
   return check_launch("spline_tile_kernel");
 }
