@@ -1,0 +1,500 @@
+"""Multi-GPU layer: x-sharded distribution function, halo exchange, ρ gather.
+
+SURVEY.md §8e / BASELINE north star.  The 4-D field is split along x1 (and x2
+on 8 GPUs, a 4 x 2 process grid) into whole cells; every rank owns the
+canonical-layout box f[v2][v1][x2 local][x1 local].  One Strang step:
+
+* x half sweeps: each sharded x axis needs the source cells c-q-1, c-q of
+  its neighbours: one-sided halo slabs whose widths come from the sweep's
+  q range (wl = max(q)+1 cells on the left, wr = -min(q) on the right) are
+  packed on device (``vpb_halo_pack``), exchanged with the two neighbours
+  (grouped NCCL send/recv over NVLink), and the sweep reads them in place
+  (``vpb_dg_sweep_axis_halo``).  An unsharded x axis is swept locally
+  (periodic).  When neither x axis is sharded the fused x-plane kernel runs.
+* density: the local ρ slab is all-gathered and every rank solves the
+  Poisson problem redundantly (a few hundred kB, microseconds).
+* v sweeps: fully local, tables from the local slice of E.
+* non-finite flags are max-reduced so every rank raises the same
+  ``SubstepError``; diagnostics are sum-reduced.
+
+Communication is pluggable: :class:`TorchComm` wraps ``torch.distributed``
+(NCCL on GPUs, gloo in the CPU tests); :class:`VirtualComm` runs several
+shards inside one process (halo "messages" are device copies), which lets a
+single GPU check the sharded kernels bitwise against the unsharded step.
+The local compute is pluggable too (:class:`CudaOps` is the product; the
+CPU tests substitute an oracle-backed implementation).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .grid import DG, GridSpec
+
+
+# ---------------------------------------------------------------------------
+# Decomposition
+# ---------------------------------------------------------------------------
+def process_grid(world: int) -> tuple[int, int]:
+    """(p1, p2) for x1 x x2 sharding: x1 only up to 4 ranks, 4 x 2 at 8
+    (the north-star layout); other counts split x1 as evenly as possible."""
+    if world == 8:
+        return 4, 2
+    if world <= 4:
+        return world, 1
+    for p2 in (2, 3, 4):
+        if world % p2 == 0 and world // p2 <= 8:
+            return world // p2, p2
+    return world, 1
+
+
+def split_cells(ncells: int, parts: int, r: int) -> tuple[int, int]:
+    """Cell range [c0, c1) of part r (near-equal contiguous split)."""
+    base, extra = divmod(ncells, parts)
+    c0 = r * base + min(r, extra)
+    return c0, c0 + base + (1 if r < extra else 0)
+
+
+@dataclass(frozen=True)
+class Decomposition:
+    grid: GridSpec
+    p1: int
+    p2: int
+
+    def __post_init__(self) -> None:
+        if self.grid.ndim != 4:
+            raise ValueError("sharding needs a 2x2v grid")
+        for p, ax in ((self.p1, 0), (self.p2, 1)):
+            if p < 1 or p > self.grid.axes[ax].count:
+                raise ValueError(f"cannot split {self.grid.axes[ax].count} cells into {p} shards")
+
+    @property
+    def world(self) -> int:
+        return self.p1 * self.p2
+
+    def coords(self, rank: int) -> tuple[int, int]:
+        return divmod(rank, self.p2)
+
+    def rank_of(self, r1: int, r2: int) -> int:
+        return (r1 % self.p1) * self.p2 + (r2 % self.p2)
+
+    def cells(self, rank: int, axis: int) -> tuple[int, int]:
+        r = self.coords(rank)[axis]
+        return split_cells(self.grid.axes[axis].count, (self.p1, self.p2)[axis], r)
+
+    def local_dims(self, rank: int) -> tuple[int, int, int, int]:
+        p = self.grid.order
+        a0, b0 = self.cells(rank, 0)
+        a1, b1 = self.cells(rank, 1)
+        return ((b0 - a0) * p, (b1 - a1) * p, self.grid.dof(2), self.grid.dof(3))
+
+    def neighbours(self, rank: int, axis: int) -> tuple[int, int]:
+        """(left, right) ranks along a sharded x axis (periodic)."""
+        r1, r2 = self.coords(rank)
+        if axis == 0:
+            return self.rank_of(r1 - 1, r2), self.rank_of(r1 + 1, r2)
+        return self.rank_of(r1, r2 - 1), self.rank_of(r1, r2 + 1)
+
+    def sharded(self, axis: int) -> bool:
+        return (self.p1, self.p2)[axis] > 1
+
+    # host-side views for tests and I/O
+    def local_slice(self, rank: int, logical: np.ndarray) -> np.ndarray:
+        p = self.grid.order
+        a0, b0 = self.cells(rank, 0)
+        a1, b1 = self.cells(rank, 1)
+        return logical[a0 * p:b0 * p, a1 * p:b1 * p]
+
+
+def halo_widths(q: np.ndarray) -> tuple[int, int]:
+    """Cells needed left / right of a shard for cell offsets q (dg.py:116-124)."""
+    q = np.asarray(q)
+    if q.size == 0:
+        return 0, 0
+    return max(0, int(q.max()) + 1), max(0, -int(q.min()))
+
+
+# ---------------------------------------------------------------------------
+# Communication
+# ---------------------------------------------------------------------------
+# message kinds of a halo exchange: "L" becomes the receiver's LEFT halo (the
+# sender's last cells, sent to its right neighbour); "R" its RIGHT halo.
+KIND_L, KIND_R = 0, 1
+
+
+class TorchComm:
+    """torch.distributed: one shard per process (NCCL or gloo)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def exchange(self, msgs: dict) -> None:
+        """msgs: {local_rank: [(kind, send_peer, send_buf, recv_peer, recv_buf), ...]}.
+        Every rank posts, per kind in order, its send and its receive."""
+        ops = []
+        for _, items in msgs.items():
+            for kind, sp, sbuf, rp, rbuf in items:
+                if sbuf is not None and sbuf.numel():
+                    ops.append(self.dist.P2POp(self.dist.isend, sbuf, sp, self.group, tag=kind))
+                if rbuf is not None and rbuf.numel():
+                    ops.append(self.dist.P2POp(self.dist.irecv, rbuf, rp, self.group, tag=kind))
+        if ops:
+            for req in self.dist.batch_isend_irecv(ops):
+                req.wait()
+
+    def allgather(self, local: dict) -> list:
+        (t,) = local.values()
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t.contiguous(), group=self.group)
+        return out
+
+    def allreduce(self, local: dict, op: str) -> torch.Tensor:
+        (t,) = local.values()
+        t = t.clone()
+        red = {"sum": self.dist.ReduceOp.SUM, "max": self.dist.ReduceOp.MAX}[op]
+        self.dist.all_reduce(t, op=red, group=self.group)
+        return t
+
+
+class VirtualComm:
+    """All shards live in this process; messages are tensor copies."""
+
+    def __init__(self, world: int):
+        self.world = world
+
+    def exchange(self, msgs: dict) -> None:
+        # index sends by (receiver, kind, sender)
+        sent = {}
+        for rank, items in msgs.items():
+            for kind, sp, sbuf, _, _ in items:
+                if sbuf is not None:
+                    sent[(sp, kind, rank)] = sbuf
+        for rank, items in msgs.items():
+            for kind, _, _, rp, rbuf in items:
+                if rbuf is not None and rbuf.numel():
+                    rbuf.copy_(sent[(rank, kind, rp)])
+
+    def allgather(self, local: dict) -> list:
+        return [local[r] for r in range(self.world)]
+
+    def allreduce(self, local: dict, op: str) -> torch.Tensor:
+        ts = [local[r] for r in sorted(local)]
+        out = ts[0].clone()
+        for t in ts[1:]:
+            out = out + t if op == "sum" else torch.maximum(out, t)
+        return out
+
+
+# ---------------------------------------------------------------------------
+# Local compute (product: the CUDA kernels)
+# ---------------------------------------------------------------------------
+class CudaOps:
+    """Local kernels of a shard, through the C ABI."""
+
+    def __init__(self):
+        from . import _device, _lib
+
+        self.lib = _lib.load()
+        self._lib = _lib
+        self._device = _device
+
+    def tables(self, values, scale, h, degree):
+        from .dg import DeviceTables
+
+        return DeviceTables(values, scale, h, degree)
+
+    def tables_q(self, tab) -> np.ndarray:
+        return tab.q.cpu().numpy()
+
+    def sweep(self, axis, src, dst, dims, order, tab, flag):
+        L = self._lib
+        L.check(self.lib.vpb_dg_sweep_axis(axis, src.data_ptr(), dst.data_ptr(), L.dims(dims), order,
+                                           tab.a.data_ptr(), tab.b.data_ptr(), tab.q.data_ptr(),
+                                           tab.alpha.data_ptr(), flag.data_ptr(),
+                                           self._device.stream()), "vpb_dg_sweep_axis")
+
+    def xplane(self, src, dst, dims, order, t1, t2, f1, f2):
+        L = self._lib
+        L.check(self.lib.vpb_dg_sweep_xplane(src.data_ptr(), dst.data_ptr(), L.dims(dims), order,
+                                             t1.a.data_ptr(), t1.b.data_ptr(), t1.q.data_ptr(),
+                                             t1.alpha.data_ptr(), t2.a.data_ptr(), t2.b.data_ptr(),
+                                             t2.q.data_ptr(), t2.alpha.data_ptr(), f1.data_ptr(),
+                                             f2.data_ptr(), self._device.stream()),
+                "vpb_dg_sweep_xplane")
+
+    def pack(self, axis, f, dims, order, cell0, width, buf):
+        L = self._lib
+        L.check(self.lib.vpb_halo_pack(axis, f.data_ptr(), L.dims(dims), order, cell0, width,
+                                       buf.data_ptr(), self._device.stream()), "vpb_halo_pack")
+
+    def halo_sweep(self, axis, src, dst, dims, order, left, wl, right, wr, tab, flag):
+        L = self._lib
+        L.check(self.lib.vpb_dg_sweep_axis_halo(
+            axis, src.data_ptr(), dst.data_ptr(), L.dims(dims), order,
+            left.data_ptr() if wl else None, wl, right.data_ptr() if wr else None, wr,
+            tab.a.data_ptr(), tab.b.data_ptr(), tab.q.data_ptr(), tab.alpha.data_ptr(),
+            flag.data_ptr(), self._device.stream()), "vpb_dg_sweep_axis_halo")
+
+    def density(self, f, dims, wv1, wv2, rho, work):
+        L = self._lib
+        L.check(self.lib.vpb_density(f.data_ptr(), L.dims(dims), wv1.data_ptr(), wv2.data_ptr(),
+                                     rho.data_ptr(), work.data_ptr(), self._device.stream()),
+                "vpb_density")
+
+    def density_work(self, dims) -> int:
+        return int(self.lib.vpb_density_work_len(self._lib.dims(dims)))
+
+    def field_solve(self, grid, rho, e, stats, flag):
+        from .poisson import solve_into
+
+        solve_into(rho, grid, e, stats, flag)
+
+    def diag_work(self, dims) -> int:
+        return int(self.lib.vpb_diag_work_len(self._lib.dims(dims)))
+
+    def diag_sums(self, f, dims, wx, wv1, wv2, v1sq, v2sq, out, work):
+        """out[0..3] = local mass, l1, l2^2, kinetic (EE excluded)."""
+        L = self._lib
+        L.check(self.lib.vpb_diagnostics(f.data_ptr(), L.dims(dims), wx.data_ptr(),
+                                         wv1.data_ptr(), wv2.data_ptr(), v1sq.data_ptr(),
+                                         v2sq.data_ptr(), None, 2, out.data_ptr(),
+                                         work.data_ptr(), self._device.stream()),
+                "vpb_diagnostics")
+
+    def electric_energy(self, e, nx, wx, out):
+        L = self._lib
+        L.check(self.lib.vpb_electric_energy(e.data_ptr(), 2, nx, wx.data_ptr(), out.data_ptr(),
+                                             self._device.stream()), "vpb_electric_energy")
+
+
+# ---------------------------------------------------------------------------
+# Sharded solver
+# ---------------------------------------------------------------------------
+class Shard:
+    """One rank's box of f plus its scratch buffers."""
+
+    def __init__(self, dec: Decomposition, rank: int, device, dtype=torch.float64):
+        self.rank = rank
+        self.dims = dec.local_dims(rank)
+        n = int(np.prod(self.dims))
+        self.f = torch.empty(n, dtype=dtype, device=device)
+        self.buf = torch.empty(n, dtype=dtype, device=device)
+        self.flags = torch.zeros(8, dtype=torch.int32, device=device)
+        self.cells = (dec.cells(rank, 0), dec.cells(rank, 1))
+
+    def swap(self) -> None:
+        self.f, self.buf = self.buf, self.f
+
+
+class ShardedSolver:
+    """Strang steps of a sharded 2x2v dG field (driver.py:245-265)."""
+
+    def __init__(self, grid: GridSpec, dec: Decomposition, comm, ranks, ops=None, device=None):
+        if grid.method != DG:
+            raise NotImplementedError("the sharded step covers the SLDG path")
+        self.grid = grid
+        self.dec = dec
+        self.comm = comm
+        self.ops = ops or CudaOps()
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.shards = {r: Shard(dec, r, self.device) for r in ranks}
+        self.order = grid.order
+        self._xtab = {}
+        self._geom = None
+        n1, n2 = grid.dof(0), grid.dof(1)
+        self.n1, self.n2 = n1, n2
+        dev = self.device
+        w = [torch.as_tensor(grid.axis_weights(a), dtype=torch.float64).to(dev) for a in range(4)]
+        self.wv1, self.wv2 = w[2], w[3]
+        self.v1sq = torch.as_tensor(grid.axis_points(2) ** 2, dtype=torch.float64).to(dev)
+        self.v2sq = torch.as_tensor(grid.axis_points(3) ** 2, dtype=torch.float64).to(dev)
+        self.wx_full = (w[1][:, None] * w[0][None, :]).reshape(-1).contiguous()
+        self.vpoints = [torch.as_tensor(grid.axis_points(a), dtype=torch.float64).to(dev)
+                        for a in (2, 3)]
+        self.rho = torch.empty(n1 * n2, dtype=torch.float64, device=dev)
+        self.e = torch.empty(2 * n1 * n2, dtype=torch.float64, device=dev)
+        self.stats = torch.zeros(4, dtype=torch.float64, device=dev)
+        self.solve_flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.names = ["x1 half (open)", "x2 half (open)", "field solve", "v1 full", "v2 full",
+                      "x1 half (close)", "x2 half (close)"]
+        self.fused = (not dec.sharded(0) and not dec.sharded(1)
+                      and (n1 * self.order) % 2 == 0 and hasattr(self.ops, "xplane"))
+
+    # -- data movement helpers (tests / I/O) ----------------------------------
+    def scatter(self, logical: np.ndarray) -> None:
+        for r, sh in self.shards.items():
+            box = np.ascontiguousarray(self.dec.local_slice(r, logical).transpose(3, 2, 1, 0))
+            sh.f.copy_(torch.from_numpy(box.reshape(-1)).to(sh.f.device))
+
+    def local_logical(self, rank: int) -> np.ndarray:
+        sh = self.shards[rank]
+        d = sh.dims
+        return sh.f.view(d[3], d[2], d[1], d[0]).permute(3, 2, 1, 0).cpu().numpy()
+
+    def gather(self) -> np.ndarray:
+        """Full logical f (only valid when this process holds every shard)."""
+        g = self.grid
+        out = np.empty(g.dofs)
+        for r in self.shards:
+            p = self.order
+            a0, b0 = self.dec.cells(r, 0)
+            a1, b1 = self.dec.cells(r, 1)
+            out[a0 * p:b0 * p, a1 * p:b1 * p] = self.local_logical(r)
+        return out
+
+    # -- tables -----------------------------------------------------------------
+    def x_tables(self, d: int, tau: float):
+        key = (d, float(tau))
+        if key not in self._xtab:
+            tab = self.ops.tables(self.vpoints[d], 0.5 * tau, self.grid.axes[d].h,
+                                  self.grid.dg_degree)
+            self._xtab[key] = (tab, halo_widths(self.ops.tables_q(tab)))
+        return self._xtab[key]
+
+    # -- sweeps -------------------------------------------------------------------
+    def _x_sweep(self, axis: int, tau: float, slot: int) -> None:
+        tab, (wl, wr) = self.x_tables(axis, tau)
+        p = self.order
+        if not self.dec.sharded(axis):
+            for sh in self.shards.values():
+                self.ops.sweep(axis, sh.f, sh.buf, sh.dims, p, tab, sh.flags[slot:slot + 1])
+                sh.swap()
+            return
+        cells_min = min(c1 - c0 for sh in self.shards.values() for (c0, c1) in [sh.cells[axis]])
+        if max(wl, wr) > cells_min:
+            raise NotImplementedError(
+                f"halo of {max(wl, wr)} cells exceeds a shard of {cells_min} cells")
+        msgs = {}
+        bufs = {}
+        for r, sh in self.shards.items():
+            left, right = self.dec.neighbours(r, axis)
+            d = sh.dims
+            cl = d[axis] // p
+            hd = list(d)
+            hd[axis] = wl * p
+            send_l = torch.empty(int(np.prod(hd)), dtype=sh.f.dtype, device=sh.f.device)
+            recv_l = torch.empty_like(send_l)
+            hd[axis] = wr * p
+            send_r = torch.empty(int(np.prod(hd)), dtype=sh.f.dtype, device=sh.f.device)
+            recv_r = torch.empty_like(send_r)
+            if wl:
+                self.ops.pack(axis, sh.f, d, p, cl - wl, wl, send_l)
+            if wr:
+                self.ops.pack(axis, sh.f, d, p, 0, wr, send_r)
+            msgs[r] = [(KIND_L, right, send_l, left, recv_l),
+                       (KIND_R, left, send_r, right, recv_r)]
+            bufs[r] = (recv_l, recv_r)
+        self.comm.exchange(msgs)
+        for r, sh in self.shards.items():
+            recv_l, recv_r = bufs[r]
+            self.ops.halo_sweep(axis, sh.f, sh.buf, sh.dims, p, recv_l, wl, recv_r, wr, tab,
+                                sh.flags[slot:slot + 1])
+            sh.swap()
+
+    def _advect_space(self, tau: float, slot: int) -> None:
+        if self.fused:
+            t1, _ = self.x_tables(0, tau)
+            t2, _ = self.x_tables(1, tau)
+            for sh in self.shards.values():
+                self.ops.xplane(sh.f, sh.buf, sh.dims, self.order, t1, t2,
+                                sh.flags[slot:slot + 1], sh.flags[slot + 1:slot + 2])
+                sh.swap()
+            return
+        self._x_sweep(0, tau, slot)
+        self._x_sweep(1, tau, slot + 1)
+
+    def _gather_rho(self) -> None:
+        """Local density slabs -> full ρ on every rank."""
+        locs = {}
+        for r, sh in self.shards.items():
+            d = sh.dims
+            rl = torch.empty(d[0] * d[1], dtype=torch.float64, device=sh.f.device)
+            work = torch.empty(self.ops.density_work(d), dtype=torch.float64, device=sh.f.device)
+            self.ops.density(sh.f, d, self.wv1, self.wv2, rl, work)
+            # pad to the largest slab so all_gather sees equal sizes
+            pad = torch.zeros(self._max_slab(), dtype=torch.float64, device=sh.f.device)
+            pad[: rl.numel()] = rl
+            locs[r] = pad
+        parts = self.comm.allgather(locs)
+        full = self.rho.view(self.n2, self.n1)
+        p = self.order
+        for r, part in enumerate(parts):
+            a0, b0 = self.dec.cells(r, 0)
+            a1, b1 = self.dec.cells(r, 1)
+            n1l, n2l = (b0 - a0) * p, (b1 - a1) * p
+            full[a1 * p:b1 * p, a0 * p:b0 * p] = part[: n1l * n2l].view(n2l, n1l)
+
+    def _max_slab(self) -> int:
+        p = self.order
+        m = 0
+        for r in range(self.dec.world):
+            a0, b0 = self.dec.cells(r, 0)
+            a1, b1 = self.dec.cells(r, 1)
+            m = max(m, (b0 - a0) * (b1 - a1) * p * p)
+        return m
+
+    def _local_e(self, sh: Shard, d: int) -> torch.Tensor:
+        p = self.order
+        (a0, b0), (a1, b1) = sh.cells
+        full = self.e[d * self.n1 * self.n2:(d + 1) * self.n1 * self.n2].view(self.n2, self.n1)
+        return full[a1 * p:b1 * p, a0 * p:b0 * p].contiguous().view(-1)
+
+    def step(self, tau: float, time_label: float | None = None) -> None:
+        from .driver import SubstepError
+
+        for sh in self.shards.values():
+            sh.flags.zero_()
+        self.solve_flag.zero_()
+        self._advect_space(tau, 0)  # x half (open); the x tables carry the tau/2
+        self._gather_rho()
+        self.ops.field_solve(self.grid, self.rho, self.e, self.stats, self.solve_flag)
+        for d in range(2):
+            axis = 2 + d
+            h = self.grid.axes[axis].h
+            for sh in self.shards.values():
+                tab = self.ops.tables(self._local_e(sh, d), tau, h, self.grid.dg_degree)
+                self.ops.sweep(axis, sh.f, sh.buf, sh.dims, self.order, tab,
+                               sh.flags[3 + d:4 + d])
+                sh.swap()
+        self._advect_space(tau, 5)
+        # flags: max over shards and ranks, field solve is redundant (slot 2)
+        for sh in self.shards.values():
+            sh.flags[2:3] = torch.maximum(sh.flags[2:3], self.solve_flag)
+        flags = self.comm.allreduce({r: sh.flags for r, sh in self.shards.items()}, "max")
+        host = flags.cpu().numpy()
+        for k, name in enumerate(self.names):
+            if host[k]:
+                raise SubstepError(name, time_label)
+
+    def diagnostics(self, time: float = 0.0) -> dict:
+        """Global conserved quantities (driver.py:279-316)."""
+        self._gather_rho()
+        self.ops.field_solve(self.grid, self.rho, self.e, None, self.solve_flag)
+        sums = {}
+        p = self.order
+        for r, sh in self.shards.items():
+            d = sh.dims
+            (a0, b0), (a1, b1) = sh.cells
+            wx = self.wx_full.view(self.n2, self.n1)[a1 * p:b1 * p, a0 * p:b0 * p].contiguous()
+            out = torch.zeros(8, dtype=torch.float64, device=sh.f.device)
+            work = torch.empty(self.ops.diag_work(d), dtype=torch.float64, device=sh.f.device)
+            self.ops.diag_sums(sh.f, d, wx.view(-1), self.wv1, self.wv2, self.v1sq, self.v2sq,
+                               out, work)
+            sums[r] = out
+        tot = self.comm.allreduce(sums, "sum").cpu().numpy()
+        ee_t = torch.zeros(1, dtype=torch.float64, device=self.device)
+        self.ops.electric_energy(self.e, self.n1 * self.n2, self.wx_full, ee_t)
+        ee = float(ee_t.cpu()[0])
+        mass, l1, l2sq, kin = (float(x) for x in tot[:4])
+        return {"time": float(time), "electric_energy": ee, "mass": mass, "l1_norm": l1,
+                "l2_norm": math.sqrt(max(l2sq, 0.0)), "kinetic_energy": kin,
+                "total_energy": kin + ee}

@@ -1,0 +1,126 @@
+"""TEST INFRASTRUCTURE: oracle-backed local compute for the sharded solver.
+
+Implements the ``CudaOps`` interface of ``paper_1803_02143_b200.dist`` on CPU
+tensors with the oracle's restatement of the reference arithmetic, so the
+multi-GPU layer's decomposition, halo packing, message pattern and ρ
+assembly can be exercised with the gloo backend (or in-process) on CPU.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from oracle import core
+
+
+class _Tab:
+    def __init__(self, a, b, q, alpha):
+        self.a, self.b, self.q, self.alpha = a, b, q, alpha
+
+
+def _box(t: torch.Tensor, dims) -> np.ndarray:
+    """flat canonical box -> logical (x1, x2, v1, v2) numpy view."""
+    n1, n2, nv1, nv2 = dims
+    return t.numpy().reshape(nv2, nv1, n2, n1).transpose(3, 2, 1, 0)
+
+
+def _line_table_index(dims, axis) -> np.ndarray:
+    """Device table row of every line of a sweep (lines in C order over the
+    other logical axes), matching the CUDA kernels' indexing."""
+    n1, n2, nv1, nv2 = dims
+    other = [a for a in range(4) if a != axis]
+    shape = [dims[a] for a in other]
+    idx = np.indices(shape)
+    coord = {a: idx[i] for i, a in enumerate(other)}
+    if axis == 0:
+        row = coord[2]
+    elif axis == 1:
+        row = coord[3]
+    else:
+        row = coord[1] * n1 + coord[0]
+    return row.reshape(-1).astype(np.int64)
+
+
+class NumpyOps:
+    def tables(self, values, scale, h, degree):
+        shifts = values.cpu().numpy() * scale
+        return _Tab(*core.projection_pairs(shifts, h, degree))
+
+    def tables_q(self, tab):
+        return tab.q
+
+    def _sweep_lines(self, arr, axis, dims, order, tab, ext=None):
+        moved = np.moveaxis(arr if ext is None else ext, axis, -1)
+        lead = moved.shape[:-1]
+        n = moved.shape[-1]
+        lines = np.ascontiguousarray(moved).reshape(-1, n)
+        idx = _line_table_index(dims, axis)
+        out = core.dg_lines(lines, idx, tab.a, tab.b, tab.q, tab.alpha, n // order, order)
+        return np.moveaxis(out.reshape(lead + (n,)), -1, axis)
+
+    def _store(self, dst, dims, logical, flag):
+        n1, n2, nv1, nv2 = dims
+        dst.copy_(torch.from_numpy(np.ascontiguousarray(logical.transpose(3, 2, 1, 0)).reshape(-1)))
+        if not np.all(np.isfinite(logical)):
+            flag.fill_(1)
+
+    def sweep(self, axis, src, dst, dims, order, tab, flag):
+        out = self._sweep_lines(_box(src, dims), axis, dims, order, tab)
+        self._store(dst, dims, out, flag)
+
+    def pack(self, axis, f, dims, order, cell0, width, buf):
+        arr = _box(f, dims)
+        sl = [slice(None)] * 4
+        sl[axis] = slice(cell0 * order, (cell0 + width) * order)
+        part = arr[tuple(sl)]
+        buf.copy_(torch.from_numpy(np.ascontiguousarray(part.transpose(3, 2, 1, 0)).reshape(-1)))
+
+    def halo_sweep(self, axis, src, dst, dims, order, left, wl, right, wr, tab, flag):
+        arr = _box(src, dims)
+        pieces = []
+        for buf, w in ((left, wl), (right, wr)):
+            d = list(dims)
+            d[axis] = w * order
+            pieces.append(_box(buf, d) if w else None)
+        ext = np.concatenate([p for p in (pieces[0], arr, pieces[1]) if p is not None], axis=axis)
+        out = self._sweep_lines(None, axis, dims, order, tab, ext=ext)
+        sl = [slice(None)] * 4
+        sl[axis] = slice(wl * order, wl * order + dims[axis])
+        self._store(dst, dims, out[tuple(sl)], flag)
+
+    def density_work(self, dims):
+        return 1
+
+    def density(self, f, dims, wv1, wv2, rho, work):
+        arr = _box(f, dims)
+        r = np.einsum("abcd,c,d->ab", arr, wv1.numpy(), wv2.numpy(), optimize=False)
+        rho.copy_(torch.from_numpy(np.ascontiguousarray(r.T).reshape(-1)))
+
+    def field_solve(self, grid, rho, e, stats, flag):
+        og = core.OGrid(tuple(a.lower for a in grid.axes), tuple(a.upper for a in grid.axes),
+                        tuple(a.count for a in grid.axes), grid.method, grid.dg_degree)
+        n1, n2 = grid.dof(0), grid.dof(1)
+        logical = rho.numpy().reshape(n2, n1).T
+        comps, mean = core.solve_poisson(logical, og)
+        e.copy_(torch.from_numpy(np.concatenate([c.T.reshape(-1) for c in comps])))
+        if stats is not None:
+            stats[0] = mean
+
+    def diag_work(self, dims):
+        return 1
+
+    def diag_sums(self, f, dims, wx, wv1, wv2, v1sq, v2sq, out, work):
+        arr = _box(f, dims)
+        n1, n2 = dims[0], dims[1]
+        wxl = wx.numpy().reshape(n2, n1).T
+        w = wxl[:, :, None, None] * (wv1.numpy()[:, None] * wv2.numpy()[None, :])[None, None]
+        out[0] = float(np.sum(arr * w))
+        out[1] = float(np.sum(np.abs(arr) * w))
+        out[2] = float(np.sum(arr * arr * w))
+        vsq = v1sq.numpy()[:, None] + v2sq.numpy()[None, :]
+        out[3] = 0.5 * float(np.sum(arr * w * vsq[None, None]))
+
+    def electric_energy(self, e, nx, wx, out):
+        ev = e.numpy()
+        out[0] = 0.5 * float(np.sum(ev * ev * np.tile(wx.numpy(), 2)))

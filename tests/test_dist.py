@@ -1,0 +1,150 @@
+"""Multi-GPU layer, exercised on CPU: decomposition, halo widths and message
+pattern, ρ assembly, flag/diagnostic reductions.
+
+The local compute is the oracle (tests/dist_oracle_ops.py), so these tests
+check the sharding logic itself: a sharded Strang step must reproduce the
+unsharded oracle step.  Two-rank runs use torch.distributed with gloo over
+127.0.0.1; the 4 x 2 layout of 8 GPUs runs in-process (VirtualComm).
+"""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+import paper_1803_02143_b200 as vpb
+from dist_oracle_ops import NumpyOps
+from oracle import core
+from paper_1803_02143_b200 import dist
+from vpb_testutil import max_rel
+
+PROB = "landau4d"
+DOFS = (24, 18, 12, 12)  # dg_order 3: 8 x 6 x 4 x 4 cells
+ORDER = 3
+TAU = 0.4  # large enough that x shifts reach |q| = 1
+
+
+def grids():
+    grid = vpb.make_grid(vpb.problem_spec(PROB), "dg", DOFS, dg_order=ORDER)
+    og = core.OGrid(tuple(a.lower for a in grid.axes), tuple(a.upper for a in grid.axes),
+                    tuple(a.count for a in grid.axes), grid.method, grid.dg_degree)
+    return grid, og
+
+
+def oracle_run(nsteps):
+    grid, og = grids()
+    f = core.initialize(PROB, og)
+    for _ in range(nsteps):
+        f = core.strang_step(f, og, TAU)
+    return f, core.diagnostics(f, og, nsteps * TAU)
+
+
+def test_process_grid_and_cell_split():
+    assert dist.process_grid(1) == (1, 1)
+    assert dist.process_grid(2) == (2, 1)
+    assert dist.process_grid(4) == (4, 1)
+    assert dist.process_grid(8) == (4, 2)
+    cells = [dist.split_cells(10, 3, r) for r in range(3)]
+    assert cells == [(0, 4), (4, 7), (7, 10)]
+    grid, _ = grids()
+    dec = dist.Decomposition(grid, 4, 2)
+    assert dec.world == 8
+    assert dec.local_dims(0) == (6, 9, 12, 12)
+    assert dec.neighbours(0, 0) == (6, 2)  # x1 left/right of rank (0, 0)
+    assert dec.neighbours(1, 1) == (0, 0)  # x2 neighbours wrap on a 2-wide axis
+    with pytest.raises(ValueError):
+        dist.Decomposition(grid, 9, 1)
+
+
+def test_halo_widths_are_one_sided():
+    assert dist.halo_widths(np.array([0, 0])) == (1, 0)
+    assert dist.halo_widths(np.array([-1, 0])) == (1, 1)
+    assert dist.halo_widths(np.array([-2, -1])) == (0, 2)
+    assert dist.halo_widths(np.array([1, 3])) == (4, 0)
+    assert dist.halo_widths(np.array([], dtype=np.int64)) == (0, 0)
+
+
+@pytest.mark.parametrize("p1,p2", [(2, 1), (1, 2), (4, 2), (3, 1), (2, 3)])
+def test_virtual_sharded_step_matches_unsharded_oracle(p1, p2):
+    grid, og = grids()
+    dec = dist.Decomposition(grid, p1, p2)
+    solver = dist.ShardedSolver(grid, dec, dist.VirtualComm(dec.world), range(dec.world),
+                                ops=NumpyOps(), device=torch.device("cpu"))
+    solver.scatter(core.initialize(PROB, og))
+    for m in range(2):
+        solver.step(TAU, time_label=(m + 1) * TAU)
+    ref, rec = oracle_run(2)
+    assert max_rel(solver.gather(), ref) <= 1e-14
+    got = solver.diagnostics(2 * TAU)
+    for k in ("mass", "l1_norm", "l2_norm", "kinetic_energy", "electric_energy"):
+        assert got[k] == pytest.approx(rec[k], rel=1e-12), k
+
+
+def test_x_shifts_need_halos_in_this_setup():
+    grid, _ = grids()
+    q1 = core.projection_pairs(grid.axis_points(2) * (0.5 * TAU), grid.axes[0].h, ORDER - 1)[2]
+    wl, wr = dist.halo_widths(q1)
+    assert wl >= 1 and wr >= 1  # both directions are exercised
+
+
+def test_sharded_step_reports_nonfinite_on_every_shard():
+    grid, og = grids()
+    dec = dist.Decomposition(grid, 2, 1)
+    solver = dist.ShardedSolver(grid, dec, dist.VirtualComm(2), range(2), ops=NumpyOps(),
+                                device=torch.device("cpu"))
+    f = core.initialize(PROB, og).copy()
+    f[20, 3, 4, 5] = np.nan  # lives on rank 1
+    solver.scatter(f)
+    with pytest.raises(vpb.SubstepError, match=r"x1 half \(open\)"):
+        solver.step(TAU)
+
+
+# ---- two real processes over gloo ---------------------------------------
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, p1, p2, outdir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as tdist
+
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        grid, og = grids()
+        dec = dist.Decomposition(grid, p1, p2)
+        solver = dist.ShardedSolver(grid, dec, dist.TorchComm(), [rank], ops=NumpyOps(),
+                                    device=torch.device("cpu"))
+        solver.scatter(core.initialize(PROB, og))
+        for _ in range(2):
+            solver.step(TAU)
+        rec = solver.diagnostics(2 * TAU)
+        np.save(os.path.join(outdir, f"f{rank}.npy"), solver.local_logical(rank))
+        np.save(os.path.join(outdir, f"d{rank}.npy"),
+                np.array([rec["mass"], rec["electric_energy"], rec["l2_norm"]]))
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("p1,p2", [(2, 1), (1, 2)])
+def test_two_rank_gloo_sharded_step(tmp_path, p1, p2):
+    port = _free_port()
+    mp.start_processes(_worker, args=(2, port, p1, p2, str(tmp_path)), nprocs=2, join=True,
+                       start_method="spawn")
+    grid, _ = grids()
+    dec = dist.Decomposition(grid, p1, p2)
+    ref, rec = oracle_run(2)
+    for r in range(2):
+        got = np.load(tmp_path / f"f{r}.npy")
+        assert max_rel(got, dec.local_slice(r, ref)) <= 1e-14 * 10
+        d = np.load(tmp_path / f"d{r}.npy")
+        assert d[0] == pytest.approx(rec["mass"], rel=1e-12)
+        assert d[1] == pytest.approx(rec["electric_energy"], rel=1e-12)
+        assert d[2] == pytest.approx(rec["l2_norm"], rel=1e-12)
