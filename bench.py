@@ -30,9 +30,10 @@ kernels (built into oracle/_ref from _kernels.pyx) driven like the
 reference's strang_step on every host thread, on a bounded scaled sample of
 the same configuration (oracle/refarm.py).
 
-Multi-GPU (torchrun, N > 1): each rank runs the full configuration on its
-own GPU as an independent replica (``scaling: weak``); the sharded strong
-scaling path lives in paper_1803_02143_b200.dist.
+Multi-GPU (torchrun, N > 1): the dG field is sharded along x1 (x1 x x2 on
+8 GPUs) with NCCL halo exchange and a rho all-gather
+(paper_1803_02143_b200.dist); the global grid is fixed (``scaling:
+strong``).  ``--replicas`` runs N independent full-size replicas instead.
 """
 
 from __future__ import annotations
@@ -221,12 +222,93 @@ def run_reference_arm(args, cfg_name: str, cfg: dict) -> None:
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+def run_sharded(args, cfg_name: str, cfg: dict, d, world: int, rank: int, local: int) -> None:
+    """N > 1: one shard of the field per GPU (x1, or x1 x x2 at 8 GPUs), NCCL
+    halo exchange + rho all-gather (paper_1803_02143_b200.dist); strong
+    scaling (the global grid is fixed)."""
+    import torch
+
+    import paper_1803_02143_b200 as vpb
+    from paper_1803_02143_b200 import dist
+
+    problem = vpb.problem_spec(cfg["problem"])
+    grid = vpb.make_grid(problem, cfg["method"], cfg["dofs"], dg_order=cfg["order"])
+    N = grid.total_dof
+    tau = cfg["tau"]
+    p1, p2 = dist.process_grid(world)
+    dec = dist.Decomposition(grid, p1, p2)
+    solver = dist.ShardedSolver(grid, dec, dist.TorchComm(), [rank])
+    solver.initialize(problem)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        solver.step(tau)
+    barrier(d, local)
+    torch.cuda.synchronize()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        start.record(stream)
+        for _ in range(args.steps):
+            solver.step(tau)
+        end.record(stream)
+        torch.cuda.synchronize()
+    barrier(d, local)
+    total_ms = allreduce_max(d, start.elapsed_time(end))
+    ms_per_step = total_ms / args.steps
+    value = N * args.steps / (total_ms * 1e-3)
+    # e2e: each rank's slab from pinned host memory, step, back to the host
+    e2e = None
+    if not args.no_e2e:
+        sh = solver.shards[rank]
+        host = torch.empty(sh.f.numel(), dtype=torch.float64, pin_memory=True)
+        host.copy_(sh.f)
+        k_e2e = max(1, min(args.steps, args.e2e_steps))
+        barrier(d, local)
+        torch.cuda.synchronize()
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(k_e2e):
+            solver.shards[rank].f.copy_(host, non_blocking=True)
+            solver.step(tau)
+            host.copy_(solver.shards[rank].f, non_blocking=True)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = allreduce_max(d, s0.elapsed_time(s1))
+        nbytes = 8 * sh.f.numel()
+        e2e = {"value": N * k_e2e / (e2e_ms * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": nbytes * world, "d2h_bytes_per_step": nbytes * world,
+               "steps": k_e2e, "ms_per_step": e2e_ms / k_e2e,
+               "path": "per-rank pinned host slab -> H2D -> sharded step -> D2H"}
+    peak, peak_kind = load_peaks()
+    step_gbs = 6 * BYTES_PER_DOF_SWEEP * N / (ms_per_step * 1e-3) / 1e9
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (BASELINE initial condition on the named grid; no dataset)",
+            "config": {"workload": cfg_name, "description": cfg["label"], "dofs": N,
+                       "parallelism": f"x-shard {p1}x{p2} (NCCL halos + rho allgather)",
+                       "l2": "inputs >> 126 MB L2; no flush"},
+            "roofline": {"bound": "hbm", "achieved": step_gbs / world, "peak": peak,
+                         "unit": "GB/s", "frac": step_gbs / world / peak, "traffic": None,
+                         "kernel": "whole step per GPU (96 B/dof)", "peak_source": peak_kind},
+            "e2e": e2e, "cpu_baseline": None, "clocks": clocks.summary(),
+            "gpu_launches": None,
+        }), flush=True)
+    if d is not None:
+        d.destroy_process_group()
+
+
 def run_vpb(args, cfg_name: str, cfg: dict) -> None:
     import torch
 
     world, rank, local = dist_env()
     d = maybe_init(world, local, "nccl")
     torch.cuda.set_device(local)
+    if world > 1 and cfg["method"] == "dg" and not args.replicas:
+        return run_sharded(args, cfg_name, cfg, d, world, rank, local)
     import paper_1803_02143_b200 as vpb
     from paper_1803_02143_b200 import driver
 
@@ -368,6 +450,8 @@ def main() -> None:
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent replicas instead of the sharded field")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per launch of the dominant kernel (from profiles/)")
     args = ap.parse_args()

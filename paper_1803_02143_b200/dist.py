@@ -330,6 +330,26 @@ class ShardedSolver:
                       and (n1 * self.order) % 2 == 0 and hasattr(self.ops, "xplane"))
 
     # -- data movement helpers (tests / I/O) ----------------------------------
+    def initialize(self, problem) -> None:
+        """Initial data of every local shard, built on the device from the
+        separable factors (driver.py:182-198) restricted to the shard's x box."""
+        from . import _device, _lib
+        from .driver import separable_factors
+
+        g1, g2, space = separable_factors(problem, self.grid)
+        space = np.asarray(space).reshape(self.n2, self.n1)
+        p = self.order
+        lib = _lib.load()
+        dg1 = torch.as_tensor(g1, dtype=torch.float64).to(self.device)
+        dg2 = torch.as_tensor(g2, dtype=torch.float64).to(self.device)
+        for sh in self.shards.values():
+            (a0, b0), (a1, b1) = sh.cells
+            sp = torch.as_tensor(np.ascontiguousarray(space[a1 * p:b1 * p, a0 * p:b0 * p]),
+                                 dtype=torch.float64).to(self.device).reshape(-1)
+            _lib.check(lib.vpb_fill_separable(sh.f.data_ptr(), _lib.dims(sh.dims),
+                                              dg1.data_ptr(), dg2.data_ptr(), sp.data_ptr(),
+                                              _device.stream()), "vpb_fill_separable")
+
     def scatter(self, logical: np.ndarray) -> None:
         for r, sh in self.shards.items():
             box = np.ascontiguousarray(self.dec.local_slice(r, logical).transpose(3, 2, 1, 0))

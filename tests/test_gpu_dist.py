@@ -55,3 +55,9 @@ def test_sharded_steps_match_single_gpu_step(p1, p2):
     rec = vpb.diagnostics(f, 3 * TAU)
     for k in ("mass", "l1_norm", "l2_norm", "kinetic_energy", "electric_energy"):
         assert got[k] == pytest.approx(getattr(rec, k), rel=1e-12), k
+
+
+def test_sharded_initialize_is_the_shard_of_the_global_initial_state():
+    prob, grid, solver, f0 = setup(4, 2)
+    solver.initialize(prob)
+    assert np.array_equal(solver.gather(), f0.numpy())
