@@ -86,24 +86,41 @@ REASONS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_powe
 
 
 class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons.  Started before
+    the warm-up (the tool takes a while to come up); only samples whose
+    timestamps fall inside [begin, end] of the timed region are summarised."""
+
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.proc = None
         self.path = Path(os.environ.get("TMPDIR", "/tmp")) / f"vpb_clocks_{os.getpid()}.csv"
+        self.t0 = self.t1 = None
 
-    def __enter__(self):
-        q = "clocks.sm,clocks.max.sm," + ",".join(f"clocks_event_reasons.{r}" for r in REASONS)
+    def start(self):
+        q = ("timestamp,clocks.sm,clocks.max.sm,"
+             + ",".join(f"clocks_event_reasons.{r}" for r in REASONS))
         try:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=self.fh, stderr=subprocess.DEVNULL)
         except (OSError, FileNotFoundError):
             self.proc = None
+            return self
+        deadline = time.time() + 10.0
+        while time.time() < deadline and self.path.stat().st_size == 0:
+            time.sleep(0.05)
         return self
 
-    def __exit__(self, *exc):
+    def begin(self):
+        self.t0 = time.time()
+
+    def end(self):
+        self.t1 = time.time()
+        time.sleep(0.12)  # let the last in-window sample land
+
+    def stop(self):
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -112,30 +129,43 @@ class ClockSampler:
                 self.proc.kill()
             self.fh.close()
 
+    def __enter__(self):
+        return self.start()
+
+    def __exit__(self, *exc):
+        self.stop()
+
     def summary(self) -> dict | None:
         if self.proc is None or not self.path.exists():
             return None
-        sm, mx, active = [], [], set()
+        from datetime import datetime
+
+        rows = []
         for line in self.path.read_text().splitlines():
             parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 2 + len(REASONS):
+            if len(parts) < 3 + len(REASONS):
                 continue
             try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
+                ts = datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((ts, float(parts[1]), float(parts[2]), parts[3:]))
             except ValueError:
                 continue
-            for r, v in zip(REASONS, parts[2:]):
-                if v.lower().startswith("active"):
-                    active.add(r)
         try:
             self.path.unlink()
         except OSError:
             pass
-        if not sm:
+        if not rows:
             return None
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
-                "reasons": sorted(active), "samples": len(sm)}
+        inside = [r for r in rows if self.t0 is not None and self.t0 <= r[0] <= (self.t1 or r[0])]
+        use = inside or sorted(rows, key=lambda r: abs(r[0] - (self.t0 or r[0])))[:3]
+        active = set()
+        for r in use:
+            for name, v in zip(REASONS, r[3]):
+                if v.lower().startswith("active"):
+                    active.add(name)
+        return {"sm_mhz": float(np.median([r[1] for r in use])),
+                "sm_max_mhz": float(max(r[2] for r in use)), "reasons": sorted(active),
+                "samples": len(use), "in_window": bool(inside)}
 
 
 # ---------------------------------------------------------------------------
@@ -240,18 +270,21 @@ def run_sharded(args, cfg_name: str, cfg: dict, d, world: int, rank: int, local:
     solver = dist.ShardedSolver(grid, dec, dist.TorchComm(), [rank])
     solver.initialize(problem)
     stream = torch.cuda.current_stream()
+    clocks = ClockSampler(local).start()
     for _ in range(args.warmup):
         solver.step(tau)
     barrier(d, local)
     torch.cuda.synchronize()
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
-        start.record(stream)
-        for _ in range(args.steps):
-            solver.step(tau)
-        end.record(stream)
-        torch.cuda.synchronize()
+    clocks.begin()
+    start.record(stream)
+    for _ in range(args.steps):
+        solver.step(tau)
+    end.record(stream)
+    torch.cuda.synchronize()
+    clocks.end()
+    clocks.stop()
     barrier(d, local)
     total_ms = allreduce_max(d, start.elapsed_time(end))
     ms_per_step = total_ms / args.steps
@@ -320,6 +353,7 @@ def run_vpb(args, cfg_name: str, cfg: dict) -> None:
     st = driver.step_state(grid)
     stream = torch.cuda.current_stream()
 
+    clocks = ClockSampler(local).start()
     for _ in range(args.warmup):
         driver.enqueue_step(field, tau, st)
         driver.check_step(st, None)
@@ -338,13 +372,15 @@ def run_vpb(args, cfg_name: str, cfg: dict) -> None:
     torch.cuda.synchronize()
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
-        start.record(stream)
-        for _ in range(args.steps):
-            driver.enqueue_step(field, tau, st, timer=mark)
-            driver.check_step(st, None)
-        end.record(stream)
-        torch.cuda.synchronize()
+    clocks.begin()
+    start.record(stream)
+    for _ in range(args.steps):
+        driver.enqueue_step(field, tau, st, timer=mark)
+        driver.check_step(st, None)
+    end.record(stream)
+    torch.cuda.synchronize()
+    clocks.end()
+    clocks.stop()
     barrier(d, local)
     total_ms = start.elapsed_time(end)
     total_ms = allreduce_max(d, total_ms)
@@ -443,7 +479,7 @@ def run_vpb(args, cfg_name: str, cfg: dict) -> None:
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="vpb", choices=["vpb", "reference"])
