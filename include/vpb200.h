@@ -108,6 +108,16 @@ int vpb_dg_sweep_xplane(const double* src, double* dst, const int64_t dims[4], i
                         const int64_t* q2, const double* alpha2, int32_t* flag1,
                         int32_t* flag2, void* stream);
 
+/* Both velocity sweeps of a Strang step, v1 then v2, in ONE pass over f
+ * (driver.py:231-242 _advect_velocity): the tables of both are indexed by the
+ * x position ix2*dims[0]+ix1.  Bitwise equal to vpb_dg_sweep_axis(2) then
+ * vpb_dg_sweep_axis(3); half the HBM traffic. */
+int vpb_dg_sweep_vplane(const double* src, double* dst, const int64_t dims[4], int32_t order,
+                        const double* a1, const double* b1, const int64_t* q1,
+                        const double* alpha1, const double* a2, const double* b2,
+                        const int64_t* q2, const double* alpha2, int32_t* flag1,
+                        int32_t* flag2, void* stream);
+
 /* One spline sweep along `axis`; shift of line = values[table row]*scale. */
 int vpb_spline_sweep_axis(int32_t axis, const double* src, double* dst, const int64_t dims[4],
                           const double* values, double scale, double h, int32_t* flag,

@@ -65,6 +65,9 @@ SIGNATURES = {
     "vpb_dg_sweep_xplane": (c_int, [c_void_p, c_void_p, POINTER(c_int64), c_int32, c_void_p,
                                     c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                     c_void_p, c_void_p, c_void_p, c_void_p]),
+    "vpb_dg_sweep_vplane": (c_int, [c_void_p, c_void_p, POINTER(c_int64), c_int32, c_void_p,
+                                    c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                    c_void_p, c_void_p, c_void_p, c_void_p]),
     "vpb_spline_sweep_axis": (c_int, [c_int32, c_void_p, c_void_p, POINTER(c_int64), c_void_p,
                                       c_double, c_double, c_void_p, c_void_p]),
     "vpb_density_work_len": (c_int64, [POINTER(c_int64)]),

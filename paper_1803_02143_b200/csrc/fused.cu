@@ -330,9 +330,168 @@ static int launch_xplane(const double* src, double* dst, const int64_t dims[4], 
   return check_launch("dg_xplane_kernel");
 }
 
+// ---------------------------------------------------------------------------
+// Fused velocity sweeps: v1 then v2 (driver.py:231-242 _advect_velocity) in
+// one HBM pass.  Both shifts are constant over the (v1, v2) plane of one x
+// position (E1(x) tau, E2(x) tau), so thread (x, v1 cell c1) streams the
+// plane along v2: for every source v2 cell s it loads the two v1 cells it
+// needs (coalesced across the 32 consecutive x of a warp), sweeps them along
+// v1 into the P x P block g(s) (v2 rows x v1 dofs of cell c1), and applies
+// the v2 pair to g(s-1), g(s), producing output v2 cell s + q2(x).  The
+// source order starts at (-q2-1) mod C2 and visits C2+1 cells.  Identical
+// operations to the two separate sweeps, so bitwise equal to them.
+// Grid: x-fastest is the v1-cell group so the blocks sharing source cells
+// (neighbouring c1) run together and hit L1/L2.
+// ---------------------------------------------------------------------------
+constexpr int kVCells = 4;  // v1 cells (warps) per CTA
+
+template <int P>
+__global__ void __launch_bounds__(32 * kVCells)
+    dg_vplane_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t nx, int C1,
+                     int C2, const double* __restrict__ a1, const double* __restrict__ b1,
+                     const int64_t* __restrict__ q1, const double* __restrict__ al1,
+                     const double* __restrict__ a2, const double* __restrict__ b2,
+                     const int64_t* __restrict__ q2, const double* __restrict__ al2,
+                     int32_t* __restrict__ flag1, int32_t* __restrict__ flag2) {
+  const int lane = threadIdx.x & 31;
+  const int c1 = blockIdx.x * kVCells + (threadIdx.x >> 5);
+  const int64_t x = (int64_t)blockIdx.y * 32 + lane;
+  if (c1 >= C1 || x >= nx) return;
+  const int64_t nv1 = (int64_t)C1 * P;
+  const int64_t row_stride = nv1 * nx;  // one v2 dof row
+  double A1[P][P], B1[P][P], A2[P][P], B2[P][P];
+#pragma unroll
+  for (int j = 0; j < P; ++j)
+#pragma unroll
+    for (int m = 0; m < P; ++m) {
+      A1[j][m] = __ldg(a1 + x * P * P + j * P + m);
+      B1[j][m] = __ldg(b1 + x * P * P + j * P + m);
+      A2[j][m] = __ldg(a2 + x * P * P + j * P + m);
+      B2[j][m] = __ldg(b2 + x * P * P + j * P + m);
+    }
+  const bool ex1 = (al1[x] == 0.0), ex2 = (al2[x] == 0.0);
+  const int qm1 = (int)wrap_mod(q1[x], C1);
+  const int qm2 = (int)wrap_mod(q2[x], C2);
+  int lo1 = c1 - qm1 - 1;
+  if (lo1 < 0) lo1 += C1;
+  const int up1 = lo1 + 1 == C1 ? 0 : lo1 + 1;
+  const double* lo_base = src + (int64_t)lo1 * P * nx + x;
+  const double* up_base = src + (int64_t)up1 * P * nx + x;
+  bool bad1 = false, bad2 = false;
+
+  // v1 sweep of source v2 cell s: g[m2][j1] for the P v2 rows of the cell
+  auto v1_cell = [&](int s, double (&g)[P][P]) {
+    double ul[P][P], uu[P][P];
+#pragma unroll
+    for (int m2 = 0; m2 < P; ++m2) {
+      const int64_t r = ((int64_t)s * P + m2) * row_stride;
+#pragma unroll
+      for (int m = 0; m < P; ++m) {
+        uu[m2][m] = __ldcs(up_base + r + m * nx);
+        if (!ex1) ul[m2][m] = __ldcs(lo_base + r + m * nx);
+      }
+    }
+#pragma unroll
+    for (int m2 = 0; m2 < P; ++m2)
+#pragma unroll
+      for (int j = 0; j < P; ++j) {
+        double v;
+        if (ex1) {
+          v = uu[m2][j];
+        } else {
+          double acc_a = dmul(A1[j][0], ul[m2][0]);
+#pragma unroll
+          for (int m = 1; m < P; ++m) acc_a = dadd(acc_a, dmul(A1[j][m], ul[m2][m]));
+          double acc_b = dmul(B1[j][0], uu[m2][0]);
+#pragma unroll
+          for (int m = 1; m < P; ++m) acc_b = dadd(acc_b, dmul(B1[j][m], uu[m2][m]));
+          v = dadd(acc_a, acc_b);
+        }
+        g[m2][j] = v;
+        bad1 |= not_finite(v);
+      }
+  };
+
+  int s = C2 - qm2 - 1;  // (-q2-1) mod C2
+  double gp[P][P];
+  v1_cell(s, gp);
+  int c2 = s + qm2;  // output cell of the first step: s+1+q2 (mod C2), kept incrementally
+  if (c2 >= C2) c2 -= C2;
+  for (int k = 0; k < C2; ++k) {
+    if (++s == C2) s = 0;
+    if (++c2 == C2) c2 = 0;
+    double g[P][P];
+    v1_cell(s, g);
+    double* out = dst + ((int64_t)c2 * P) * row_stride + (int64_t)c1 * P * nx + x;
+#pragma unroll
+    for (int j2 = 0; j2 < P; ++j2)
+#pragma unroll
+      for (int j = 0; j < P; ++j) {
+        double o;
+        if (ex2) {
+          o = g[j2][j];
+        } else {
+          double acc_a = dmul(A2[j2][0], gp[0][j]);
+#pragma unroll
+          for (int m = 1; m < P; ++m) acc_a = dadd(acc_a, dmul(A2[j2][m], gp[m][j]));
+          double acc_b = dmul(B2[j2][0], g[0][j]);
+#pragma unroll
+          for (int m = 1; m < P; ++m) acc_b = dadd(acc_b, dmul(B2[j2][m], g[m][j]));
+          o = dadd(acc_a, acc_b);
+        }
+        bad2 |= not_finite(o);
+        __stcs(out + j2 * row_stride + j * nx, o);
+      }
+#pragma unroll
+    for (int m2 = 0; m2 < P; ++m2)
+#pragma unroll
+      for (int j = 0; j < P; ++j) gp[m2][j] = g[m2][j];
+  }
+  report_flag(bad1, flag1);
+  report_flag(bad2, flag2);
+}
+
+template <int P>
+static int launch_vplane(const double* src, double* dst, const int64_t dims[4], const double* a1,
+                         const double* b1, const int64_t* q1, const double* al1,
+                         const double* a2, const double* b2, const int64_t* q2,
+                         const double* al2, int32_t* f1, int32_t* f2, cudaStream_t st) {
+  const int64_t nx = dims[0] * dims[1];
+  const int C1 = (int)(dims[2] / P);
+  const int C2 = (int)(dims[3] / P);
+  if (nx == 0 || C1 == 0 || C2 == 0) return VPB_OK;
+  dim3 grid((unsigned)((C1 + kVCells - 1) / kVCells), (unsigned)((nx + 31) / 32));
+  dg_vplane_kernel<P><<<grid, 32 * kVCells, 0, st>>>(src, dst, nx, C1, C2, a1, b1, q1, al1, a2,
+                                                     b2, q2, al2, f1, f2);
+  return check_launch("dg_vplane_kernel");
+}
+
 }  // namespace vpb
 
 using namespace vpb;
+
+extern "C" int vpb_dg_sweep_vplane(const double* src, double* dst, const int64_t dims[4],
+                                   int32_t order, const double* a1, const double* b1,
+                                   const int64_t* q1, const double* alpha1, const double* a2,
+                                   const double* b2, const int64_t* q2, const double* alpha2,
+                                   int32_t* flag1, int32_t* flag2, void* stream) {
+  VPB_REQUIRE(src != dst, "src and dst must be distinct buffers");
+  VPB_REQUIRE(order >= 1 && order <= kMaxOrder, "order %d outside 1..9", order);
+  VPB_REQUIRE(dims[2] % order == 0 && dims[3] % order == 0, "v axes not whole cells");
+  VPB_REQUIRE(dims[3] > 1, "fused v sweep needs a 2x2v field");
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (order) {
+    case 1: return launch_vplane<1>(src, dst, dims, a1, b1, q1, alpha1, a2, b2, q2, alpha2, flag1, flag2, st);
+    case 2: return launch_vplane<2>(src, dst, dims, a1, b1, q1, alpha1, a2, b2, q2, alpha2, flag1, flag2, st);
+    case 3: return launch_vplane<3>(src, dst, dims, a1, b1, q1, alpha1, a2, b2, q2, alpha2, flag1, flag2, st);
+    case 4: return launch_vplane<4>(src, dst, dims, a1, b1, q1, alpha1, a2, b2, q2, alpha2, flag1, flag2, st);
+    case 5: return launch_vplane<5>(src, dst, dims, a1, b1, q1, alpha1, a2, b2, q2, alpha2, flag1, flag2, st);
+    case 6: return launch_vplane<6>(src, dst, dims, a1, b1, q1, alpha1, a2, b2, q2, alpha2, flag1, flag2, st);
+    case 7: return launch_vplane<7>(src, dst, dims, a1, b1, q1, alpha1, a2, b2, q2, alpha2, flag1, flag2, st);
+    case 8: return launch_vplane<8>(src, dst, dims, a1, b1, q1, alpha1, a2, b2, q2, alpha2, flag1, flag2, st);
+    default: return launch_vplane<9>(src, dst, dims, a1, b1, q1, alpha1, a2, b2, q2, alpha2, flag1, flag2, st);
+  }
+}
 
 extern "C" int vpb_dg_sweep_xplane(const double* src, double* dst, const int64_t dims[4],
                                    int32_t order, const double* a1, const double* b1,

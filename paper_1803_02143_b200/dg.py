@@ -194,3 +194,18 @@ def xplane_dg(grid, src: torch.Tensor, dst: torch.Tensor, t1: DeviceTables, t2: 
                                 None if flag2 is None else flag2.data_ptr(), _device.stream()),
         "vpb_dg_sweep_xplane",
     )
+
+
+def vplane_dg(grid, src: torch.Tensor, dst: torch.Tensor, t1: DeviceTables, t2: DeviceTables,
+              flag1: torch.Tensor | None, flag2: torch.Tensor | None) -> None:
+    """v1 then v2 sweep of a 2x2v field in one pass (``vpb_dg_sweep_vplane``)."""
+    lib = _lib.load()
+    _lib.check(
+        lib.vpb_dg_sweep_vplane(src.data_ptr(), dst.data_ptr(), _lib.dims(grid.dims4), t1.order,
+                                t1.a.data_ptr(), t1.b.data_ptr(), t1.q.data_ptr(),
+                                t1.alpha.data_ptr(), t2.a.data_ptr(), t2.b.data_ptr(),
+                                t2.q.data_ptr(), t2.alpha.data_ptr(),
+                                None if flag1 is None else flag1.data_ptr(),
+                                None if flag2 is None else flag2.data_ptr(), _device.stream()),
+        "vpb_dg_sweep_vplane",
+    )

@@ -25,7 +25,7 @@ import numpy as np
 import torch
 
 from . import _device, _lib
-from .dg import DeviceTables, sweep_dg, xplane_dg
+from .dg import DeviceTables, sweep_dg, vplane_dg, xplane_dg
 from .field import DEFAULT_STRATEGY, DistributionField, LayoutDescriptor, write_snapshot
 from .grid import DG, SPACE, SPLINE, VELOCITY, Axis, GridSpec
 from .poisson import (
@@ -40,9 +40,10 @@ from .poisson import (
 from .spline import sweep_spline
 
 
-# Fused x1+x2 plane sweeps (set False to run the two sweeps separately; the
-# results are bitwise identical either way).
+# Fused x1+x2 plane sweeps and fused v1+v2 column sweeps (set False to run
+# the sweeps separately; the results are bitwise identical either way).
 FUSE_X = True
+FUSE_V = True
 
 
 class SubstepError(RuntimeError):
@@ -243,6 +244,8 @@ class StepState:
         # both x sweeps of a half step in one pass (bitwise-identical result)
         self.fused_x = (grid.method == DG and grid.ndim == 4
                         and (grid.dof(0) * grid.order) % 2 == 0 and FUSE_X)
+        # both v sweeps in one pass (bitwise-identical result)
+        self.fused_v = grid.method == DG and grid.ndim == 4 and FUSE_V
         lib = _lib.load()
         self.diag_work = torch.empty(int(lib.vpb_diag_work_len(_lib.dims(grid.dims4))),
                                      dtype=torch.float64, device=dev)
@@ -351,10 +354,21 @@ def enqueue_step(field: DistributionField, tau: float, state: StepState | None =
     mark("field_solve")
     solve_into(st.rho, grid, st.e, st.stats, st.flags[k:k + 1])  # solve_poisson
     k += 1
-    for d in range(grid.ndim_x):  # _advect_velocity(tau)  driver.py:231-242
-        mark(f"tables_{vn[d]}")
-        tab = st.v_tables(d, tau)
-        sweep(grid.ndim_x + d, tab, tau, f"sweep_{vn[d]}")
+    if st.fused_v:  # _advect_velocity(tau) in one pass  driver.py:231-242
+        mark("tables_v12")
+        t1 = st.v_tables(0, tau)
+        t2 = st.v_tables(1, tau)
+        out = st.buf
+        mark("sweep_v12")
+        vplane_dg(grid, field._phys.view(-1), out, t1, t2, st.flags[k:k + 1],
+                  st.flags[k + 1:k + 2])
+        st.buf = field._swap(out.view(field._phys.shape)).view(-1)
+        k += 2
+    else:
+        for d in range(grid.ndim_x):  # _advect_velocity(tau)  driver.py:231-242
+            mark(f"tables_{vn[d]}")
+            tab = st.v_tables(d, tau)
+            sweep(grid.ndim_x + d, tab, tau, f"sweep_{vn[d]}")
     advect_space()  # "close"
     mark(None)
 

@@ -282,6 +282,42 @@ def test_fused_x_planes_bitwise_equal_to_separate_sweeps(monkeypatch, order, dof
     assert np.array_equal(outs[0], outs[1])
 
 
+@pytest.mark.parametrize("order,dofs", [(3, (24, 18, 12, 15)), (2, (16, 12, 8, 10)),
+                                        (4, (16, 20, 12, 8)), (1, (12, 10, 8, 6))])
+def test_fused_v_columns_bitwise_equal_to_separate_sweeps(monkeypatch, order, dofs):
+    """vpb_dg_sweep_vplane == v1 sweep then v2 sweep, bit for bit, over steps."""
+    prob = vpb.problem_spec("landau4d")
+    grid = vpb.make_grid(prob, "dg", dofs, dg_order=order)
+    outs = []
+    for fused in (False, True):
+        monkeypatch.setattr(driver, "FUSE_V", fused)
+        driver._state_cached.cache_clear()
+        f = vpb.initialize(prob, grid)
+        for _ in range(3):
+            f = vpb.strang_step(f, 0.37, consume=True)
+        assert driver.step_state(grid).fused_v == fused
+        outs.append(f.numpy())
+    driver._state_cached.cache_clear()
+    assert np.array_equal(outs[0], outs[1])
+
+
+def test_fused_v_reports_nonfinite_field_in_v1():
+    prob = vpb.problem_spec("landau4d")
+    grid = vpb.make_grid(prob, "dg", 12, dg_order=3)
+    f = vpb.initialize(prob, grid)
+    st = driver.step_state(grid)
+    assert st.fused_v
+    out = torch.empty_like(f.data)
+    flags = torch.zeros(2, dtype=torch.int32, device="cuda")
+    e = torch.full((144,), 0.3, dtype=torch.float64, device="cuda")
+    t1 = driver.DeviceTables(e, 0.1, grid.axes[2].h, 2)
+    t2 = driver.DeviceTables(e, 0.1, grid.axes[3].h, 2)
+    bad = f.data.clone()
+    bad[1000] = math.inf
+    driver.vplane_dg(grid, bad, out, t1, t2, flags[0:1], flags[1:2])
+    assert flags.tolist() == [1, 1]
+
+
 def test_fused_x_reports_nonfinite_in_x1_and_x2():
     prob = vpb.problem_spec("landau4d")
     grid = vpb.make_grid(prob, "dg", 12, dg_order=3)
