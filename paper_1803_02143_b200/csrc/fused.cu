@@ -29,6 +29,7 @@
 
 #include "async_copy.cuh"
 #include "common.cuh"
+#include "tensormap.cuh"
 
 namespace vpb {
 
@@ -451,6 +452,214 @@ __global__ void __launch_bounds__(32 * kVCells)
   report_flag(bad2, flag2);
 }
 
+// TMA-staged variant.  A CTA owns 32 consecutive x (one per lane) and kVCells
+// v1 cells (one per warp).  All lanes stream the same source v2 cells s =
+// 0..C2 (each lane's output cell is s + q2(x)); for every s a TMA 3-D tensor
+// copy brings the P v2 rows x the block's v1 source window (kVCells+kVSpan
+// cells starting at c1a - max(q1) - 1) x 32 x into a kVStages-deep ring.
+// Lanes read their own two source cells from the tile: [row][v1 dof][lane]
+// keeps every warp access conflict-free whatever the per-lane q1.  Blocks
+// whose q1 spread exceeds the window fall back to direct global loads.
+constexpr int kVSpan = 3;    // window = kVCells + kVSpan cells (q1 spread <= 2)
+constexpr int kVStages = 4;
+
+template <int P>
+__global__ void __launch_bounds__(32 * kVCells)
+    dg_vplane_tma_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t nx,
+                         int C1, int C2, const double* __restrict__ a1,
+                         const double* __restrict__ b1, const int64_t* __restrict__ q1,
+                         const double* __restrict__ al1, const double* __restrict__ a2,
+                         const double* __restrict__ b2, const int64_t* __restrict__ q2,
+                         const double* __restrict__ al2, int32_t* __restrict__ flag1,
+                         int32_t* __restrict__ flag2, const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr int W = kVCells + kVSpan;       // window cells
+  constexpr int WP = W * P;                 // window v1 dofs
+  constexpr int stage = P * WP * 32;        // doubles per stage
+  double* ring = reinterpret_cast<double*>(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kVStages * stage);
+  __shared__ int s_qmax, s_qmin;
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c1a = blockIdx.x * kVCells;
+  const int c1 = c1a + warp;
+  const int64_t x0 = (int64_t)blockIdx.y * 32;
+  const int64_t x = x0 + lane;
+  const int64_t nv1 = (int64_t)C1 * P;
+  const int64_t row_stride = nv1 * nx;
+  const bool active = c1 < C1;
+
+  const int qm1 = (int)wrap_mod(q1[x], C1);
+  const int qm2 = (int)wrap_mod(q2[x], C2);
+  // block-wide window of source v1 cells (q1 in [qmin, qmax], taken mod C1
+  // relative to the warp-0 lane-0 value so the spread is the true spread)
+  if (threadIdx.x == 0) {
+    s_qmax = -(1 << 30);
+    s_qmin = 1 << 30;
+  }
+  __syncthreads();
+  {
+    const int q0 = (int)wrap_mod(q1[x0], C1);
+    int d = qm1 - q0;  // relative offset in (-C1, C1); fold to the nearest
+    if (d > C1 / 2) d -= C1;
+    if (d < -C1 / 2) d += C1;
+    if (warp == 0) {
+      int mx = d, mn = d;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      }
+      if (lane == 0) {
+        s_qmax = q0 + mx;
+        s_qmin = q0 + mn;
+      }
+    }
+  }
+  __syncthreads();
+  const int qmax = s_qmax;
+  const bool use_tma = (qmax - s_qmin) <= kVSpan - 1;
+  int wstart = c1a - qmax - 1;  // first window cell (mod C1)
+  wstart %= C1;
+  if (wstart < 0) wstart += C1;
+
+  double A1[P][P], B1[P][P], A2[P][P], B2[P][P];
+#pragma unroll
+  for (int j = 0; j < P; ++j)
+#pragma unroll
+    for (int m = 0; m < P; ++m) {
+      A1[j][m] = __ldg(a1 + x * P * P + j * P + m);
+      B1[j][m] = __ldg(b1 + x * P * P + j * P + m);
+      A2[j][m] = __ldg(a2 + x * P * P + j * P + m);
+      B2[j][m] = __ldg(b2 + x * P * P + j * P + m);
+    }
+  const bool ex1 = (al1[x] == 0.0), ex2 = (al2[x] == 0.0);
+  int lo1 = c1 - qm1 - 1;
+  lo1 %= C1;
+  if (lo1 < 0) lo1 += C1;
+  const int up1 = lo1 + 1 == C1 ? 0 : lo1 + 1;
+  // window-relative cell indices (valid when use_tma)
+  int wlo = lo1 - wstart;
+  if (wlo < 0) wlo += C1;
+  int wup = wlo + 1;
+  const double* lo_base = src + (int64_t)lo1 * P * nx + x;
+  const double* up_base = src + (int64_t)up1 * P * nx + x;
+  bool bad1 = false, bad2 = false;
+
+  auto issue = [&](int k) {  // source v2 cell k (0..C2) into slot k % kVStages
+    const int s = k == C2 ? 0 : k;
+    const int sl = k % kVStages;
+    double* dstp = ring + sl * stage;
+    mbar_arrive_expect_tx(bars + sl, (uint32_t)stage * 8u);
+    int cell = wstart;
+    for (int w = 0; w < W; ++w) {  // one {32 x, P dofs, P rows} box per window cell
+      tma_load_3d(dstp + w * (P * P * 32), &tmap, (int)x0, cell * P, s * P, bars + sl);
+      if (++cell == C1) cell = 0;
+    }
+  };
+  if (use_tma && threadIdx.x == 0) {
+#pragma unroll
+    for (int sl = 0; sl < kVStages; ++sl) mbar_init(bars + sl, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (use_tma && threadIdx.x == 0)
+    for (int k = 0; k < kVStages && k <= C2; ++k) issue(k);
+
+  auto v1_cell = [&](int k, double (&g)[P][P]) {
+    double ul[P][P], uu[P][P];
+    if (use_tma) {
+      const int sl = k % kVStages;
+      const double* t = ring + sl * stage + lane;
+#pragma unroll
+      for (int m2 = 0; m2 < P; ++m2)
+#pragma unroll
+        for (int m = 0; m < P; ++m) {
+          uu[m2][m] = t[((wup * P + m2) * P + m) * 32];  // [cell][row][dof][lane]
+          ul[m2][m] = t[((wlo * P + m2) * P + m) * 32];
+        }
+    } else {
+      const int s = k == C2 ? 0 : k;
+#pragma unroll
+      for (int m2 = 0; m2 < P; ++m2) {
+        const int64_t r = ((int64_t)s * P + m2) * row_stride;
+#pragma unroll
+        for (int m = 0; m < P; ++m) {
+          uu[m2][m] = __ldcs(up_base + r + m * nx);
+          ul[m2][m] = __ldcs(lo_base + r + m * nx);
+        }
+      }
+    }
+#pragma unroll
+    for (int m2 = 0; m2 < P; ++m2)
+#pragma unroll
+      for (int j = 0; j < P; ++j) {
+        double v;
+        if (ex1) {
+          v = uu[m2][j];
+        } else {
+          double acc_a = dmul(A1[j][0], ul[m2][0]);
+#pragma unroll
+          for (int m = 1; m < P; ++m) acc_a = dadd(acc_a, dmul(A1[j][m], ul[m2][m]));
+          double acc_b = dmul(B1[j][0], uu[m2][0]);
+#pragma unroll
+          for (int m = 1; m < P; ++m) acc_b = dadd(acc_b, dmul(B1[j][m], uu[m2][m]));
+          v = dadd(acc_a, acc_b);
+        }
+        g[m2][j] = v;
+        bad1 |= not_finite(v);
+      }
+  };
+  auto release = [&](int k) {  // every thread is done with slot k % kVStages
+    __syncthreads();
+    if (use_tma && threadIdx.x == 0 && k + kVStages <= C2) issue(k + kVStages);
+  };
+
+  double gp[P][P];
+  uint32_t phase = 0;
+  if (use_tma) mbar_wait(bars + 0, 0);
+  if (active) v1_cell(0, gp);
+  release(0);
+  int c2 = qm2;  // output cell of source cell s: s + q2 (mod C2); s = 1 first
+  for (int k = 1; k <= C2; ++k) {
+    const int sl = k % kVStages;
+    if (sl == 0) phase ^= 1u;
+    if (use_tma) mbar_wait(bars + sl, phase);
+    if (++c2 == C2) c2 = 0;
+    if (active) {
+      double g[P][P];
+      v1_cell(k, g);
+      double* out = dst + ((int64_t)c2 * P) * row_stride + (int64_t)c1 * P * nx + x;
+#pragma unroll
+      for (int j2 = 0; j2 < P; ++j2)
+#pragma unroll
+        for (int j = 0; j < P; ++j) {
+          double o;
+          if (ex2) {
+            o = g[j2][j];
+          } else {
+            double acc_a = dmul(A2[j2][0], gp[0][j]);
+#pragma unroll
+            for (int m = 1; m < P; ++m) acc_a = dadd(acc_a, dmul(A2[j2][m], gp[m][j]));
+            double acc_b = dmul(B2[j2][0], g[0][j]);
+#pragma unroll
+            for (int m = 1; m < P; ++m) acc_b = dadd(acc_b, dmul(B2[j2][m], g[m][j]));
+            o = dadd(acc_a, acc_b);
+          }
+          bad2 |= not_finite(o);
+          __stcs(out + j2 * row_stride + j * nx, o);
+        }
+#pragma unroll
+      for (int m2 = 0; m2 < P; ++m2)
+#pragma unroll
+        for (int j = 0; j < P; ++j) gp[m2][j] = g[m2][j];
+    }
+    release(k);
+  }
+  report_flag(bad1, flag1);
+  report_flag(bad2, flag2);
+}
+
 template <int P>
 static int launch_vplane(const double* src, double* dst, const int64_t dims[4], const double* a1,
                          const double* b1, const int64_t* q1, const double* al1,
@@ -461,6 +670,27 @@ static int launch_vplane(const double* src, double* dst, const int64_t dims[4], 
   const int C2 = (int)(dims[3] / P);
   if (nx == 0 || C1 == 0 || C2 == 0) return VPB_OK;
   dim3 grid((unsigned)((C1 + kVCells - 1) / kVCells), (unsigned)((nx + 31) / 32));
+  static const bool no_tma = getenv("VPB_VPLANE_DIRECT") != nullptr;
+  if (!no_tma && nx % 32 == 0 && C1 >= kVCells + kVSpan && P * P * 32 * 8 <= 65536 &&
+      (reinterpret_cast<uintptr_t>(src) & 15) == 0 && (nx * 8) % 16 == 0) {
+    CUtensorMap tmap;
+    const uint64_t nv1 = (uint64_t)C1 * P, nv2 = (uint64_t)C2 * P;
+    if (encode_tmap_3d(&tmap, src, (uint64_t)nx, nv1, nv2, (uint64_t)nx * 8,
+                       (uint64_t)nx * nv1 * 8, 32, P, P)) {
+      const size_t smem = (size_t)kVStages * P * (kVCells + kVSpan) * P * 32 * 8 + kVStages * 8;
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(dg_vplane_tma_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024);
+        attr = true;
+      }
+      if (smem <= 200 * 1024) {
+        dg_vplane_tma_kernel<P><<<grid, 32 * kVCells, smem, st>>>(
+            src, dst, nx, C1, C2, a1, b1, q1, al1, a2, b2, q2, al2, f1, f2, tmap);
+        return check_launch("dg_vplane_tma_kernel");
+      }
+    }
+  }
   dg_vplane_kernel<P><<<grid, 32 * kVCells, 0, st>>>(src, dst, nx, C1, C2, a1, b1, q1, al1, a2,
                                                      b2, q2, al2, f1, f2);
   return check_launch("dg_vplane_kernel");
