@@ -118,6 +118,22 @@ int vpb_dg_sweep_vplane(const double* src, double* dst, const int64_t dims[4], i
                         const int64_t* q2, const double* alpha2, int32_t* flag1,
                         int32_t* flag2, void* stream);
 
+/* vpb_dg_sweep_xplane plus the density of its OUTPUT, collapsed to cell
+ * centres (poisson.py:85-95 then :129-139): rc_out[c2][c1] (C2 x C1) and
+ * stats[0] = weighted density mean / volume (poisson.py:143-160).  Each CTA
+ * accumulates its own planes into `work` (vpb_dg_xplane_density_work_len
+ * doubles); a fixed-order pass sums the CTA partials.  Feed rc_out to
+ * vpb_field_solve with a geometry whose r1, r2 = C1, C2 and g = DFT. */
+int64_t vpb_dg_xplane_density_work_len(const int64_t dims[4], int32_t order);
+int vpb_dg_sweep_xplane_density(const double* src, double* dst, const int64_t dims[4],
+                                int32_t order, const double* a1, const double* b1,
+                                const int64_t* q1, const double* alpha1, const double* a2,
+                                const double* b2, const int64_t* q2, const double* alpha2,
+                                int32_t* flag1, int32_t* flag2, const double* wv1,
+                                const double* wv2, const double* mid, const double* wx1,
+                                const double* wx2, double volume, double* work, double* rc_out,
+                                double* stats, void* stream);
+
 /* One spline sweep along `axis`; shift of line = values[table row]*scale. */
 int vpb_spline_sweep_axis(int32_t axis, const double* src, double* dst, const int64_t dims[4],
                           const double* values, double scale, double h, int32_t* flag,
@@ -146,6 +162,8 @@ typedef struct {
   const double* wx1;    /* [n1] quadrature weights */
   const double* wx2;    /* [n2] */
   double volume;        /* spatial measure */
+  int64_t r1, r2;       /* input density grid (0: the nodal n1, n2; c1, c2 when the
+                           input is already collapsed to cell centres and g = DFT) */
 } vpb_field_geom;
 
 int64_t vpb_field_work_len(const vpb_field_geom* geom);

@@ -38,6 +38,8 @@ class FieldGeom(ctypes.Structure):
         ("wx1", c_void_p),
         ("wx2", c_void_p),
         ("volume", c_double),
+        ("r1", c_int64),
+        ("r2", c_int64),
     ]
 
 
@@ -68,6 +70,12 @@ SIGNATURES = {
     "vpb_dg_sweep_vplane": (c_int, [c_void_p, c_void_p, POINTER(c_int64), c_int32, c_void_p,
                                     c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                     c_void_p, c_void_p, c_void_p, c_void_p]),
+    "vpb_dg_xplane_density_work_len": (c_int64, [POINTER(c_int64), c_int32]),
+    "vpb_dg_sweep_xplane_density": (c_int, [c_void_p, c_void_p, POINTER(c_int64), c_int32,
+                                            c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                            c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                            c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                            c_double, c_void_p, c_void_p, c_void_p, c_void_p]),
     "vpb_spline_sweep_axis": (c_int, [c_int32, c_void_p, c_void_p, POINTER(c_int64), c_void_p,
                                       c_double, c_double, c_void_p, c_void_p]),
     "vpb_density_work_len": (c_int64, [POINTER(c_int64)]),

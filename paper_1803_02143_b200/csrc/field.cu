@@ -288,20 +288,21 @@ extern "C" int vpb_field_solve(const double* rho, const vpb_field_geom* g, doubl
   VPB_REQUIRE(g->ncomp == 1 || g->ncomp == 2, "ncomp must be 1 or 2");
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t n1 = g->n1, n2 = g->n2, c1 = g->c1, c2 = g->c2;
+  const int64_t r1 = g->r1 > 0 ? g->r1 : n1, r2 = g->r2 > 0 ? g->r2 : n2;  // input grid
   double* T = work;
   double* Rh = T + 2 * c1 * n2;
   double* U = Rh + 2 * c1 * c2;
   int rc;
-  if (stats) {
+  if (stats && r1 == n1 && r2 == n2) {
     density_mean_kernel<<<1, 1024, 0, st>>>(rho, n1, n2, g->wx1, g->wx2, g->volume, stats);
     if ((rc = check_launch("density_mean_kernel"))) return rc;
   }
-  // T[k1][i2] = sum_i1 G1[k1][i1] R[i1][i2],  R[i1][i2] = rho[i2*n1+i1]
-  rc = zgemm(c1, n2, n1, 1, ZOp{g->g1, n1, 1, 1, 0}, ZOp{rho, 1, n1, 0, 0}, nullptr, T, n2, 1, 0,
+  // T[k1][i2] = sum_i1 G1[k1][i1] R[i1][i2],  R[i1][i2] = rho[i2*r1+i1]
+  rc = zgemm(c1, r2, r1, 1, ZOp{g->g1, r1, 1, 1, 0}, ZOp{rho, 1, r1, 0, 0}, nullptr, T, r2, 1, 0,
              0, nullptr, st);
   if (rc) return rc;
   // Rh[k1][k2] = sum_i2 T[k1][i2] G2[k2][i2]
-  rc = zgemm(c1, c2, n2, 1, ZOp{T, n2, 1, 1, 0}, ZOp{g->g2, 1, n2, 1, 0}, nullptr, Rh, c2, 1, 0,
+  rc = zgemm(c1, c2, r2, 1, ZOp{T, r2, 1, 1, 0}, ZOp{g->g2, 1, r2, 1, 0}, nullptr, Rh, c2, 1, 0,
              0, nullptr, st);
   if (rc) return rc;
   // U_d[i1][k2] = sum_k1 M1[i1][k1] (K_d[k1][k2] Rh[k1][k2])

@@ -91,7 +91,23 @@ __device__ __forceinline__ void lds_row_cell(const double* p, double (&u)[P]) {
   }
 }
 
-template <int P>
+// Optional density epilogue of the x-plane pass (poisson.py:85-95 followed by
+// the cell-centre collapse of poisson.py:129-139): every output P x P cell
+// block is collapsed with the Lagrange weights at the cell centre, weighted by
+// the plane's velocity weight, and accumulated into the CTA's own partial
+// slab [C2][C1] (thread c owns column c: no atomics, fixed order).  The
+// neutrality mean (poisson.py:143-160) rides along as a per-CTA scalar.
+struct XDensity {
+  const double* wv1;   // [nv1] velocity weights
+  const double* wv2;   // [nv2]
+  const double* mid;   // [P] Lagrange basis at xi = 1/2
+  const double* wx1;   // [n1] space weights
+  const double* wx2;   // [n2]
+  double* rc_part;     // [grid][C2][C1] or nullptr (epilogue off)
+  double* mean_part;   // [grid]
+};
+
+template <int P, bool DENS>
 __global__ void __launch_bounds__(128)
     dg_xplane_kernel(const double* __restrict__ src, double* __restrict__ dst, int n1, int C2,
                      int G, int64_t nv1, int64_t nplanes, int64_t planes_per_block,
@@ -99,7 +115,8 @@ __global__ void __launch_bounds__(128)
                      const int64_t* __restrict__ q1, const double* __restrict__ al1,
                      const double* __restrict__ a2, const double* __restrict__ b2,
                      const int64_t* __restrict__ q2, const double* __restrict__ al2,
-                     int32_t* __restrict__ flag1, int32_t* __restrict__ flag2) {
+                     int32_t* __restrict__ flag1, int32_t* __restrict__ flag2,
+                     const XDensity dn) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int cell = P * n1;          // one x2 cell: P rows of n1 dofs
   const int slot = G * cell;        // ring slot
@@ -156,12 +173,26 @@ __global__ void __launch_bounds__(128)
   cur.start(pl_begin, C2, q2, nv1);
   int st = 0;
   uint32_t phase = 0;
+  // density epilogue state
+  constexpr bool dens = DENS;
+  double midw[P], wxc[P];
+  double wplane = 0.0, meanacc = 0.0;
+  double* mypart = dens ? dn.rc_part + (int64_t)blockIdx.x * C2 * C1 : nullptr;
+  if (dens && active) {
+#pragma unroll
+    for (int m = 0; m < P; ++m) {
+      midw[m] = dn.mid[m];
+      wxc[m] = dn.wx1[tid * P + m];
+    }
+    for (int c2 = 0; c2 < C2; ++c2) mypart[c2 * C1 + tid] = 0.0;
+  }
 
   for (int64_t j = 0; j < nchunks; ++j) {
     const XChunk c = cur.chunk(G, C2);
     const int64_t plane = cur.plane;
     if (active && cur.i == 0) {
       const int64_t iv2 = plane / nv1, iv1 = plane - iv2 * nv1;
+      if (dens) wplane = dn.wv1[iv1] * dn.wv2[iv2];
       ex1 = (al1[iv1] == 0.0);
       ex2 = (al2[iv2] == 0.0);
 #pragma unroll
@@ -215,6 +246,7 @@ __global__ void __launch_bounds__(128)
         if (c.nout > 0) {
           // x2 sweep for output x2 cell c.first + sc: rows j2, dofs jj of this cell
           double* otile = out + sc * cell + tid * P;
+          double rrow[P], mrow[P];
 #pragma unroll
           for (int j2 = 0; j2 < P; ++j2) {
             double o[P];
@@ -241,6 +273,27 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
               for (int jj = 0; jj < P; ++jj) otile[j2 * n1 + jj] = o[jj];
             }
+            if (dens) {
+              double r = 0.0, mw = 0.0;
+#pragma unroll
+              for (int jj = 0; jj < P; ++jj) {
+                r += midw[jj] * o[jj];
+                mw += wxc[jj] * o[jj];
+              }
+              rrow[j2] = r;
+              mrow[j2] = mw;
+            }
+          }
+          if (dens) {
+            const int oc = c.first + sc;
+            double rcv = 0.0, mv = 0.0;
+#pragma unroll
+            for (int j2 = 0; j2 < P; ++j2) {
+              rcv += midw[j2] * rrow[j2];
+              mv += dn.wx2[oc * P + j2] * mrow[j2];
+            }
+            mypart[oc * C1 + tid] += wplane * rcv;
+            meanacc += wplane * mv;
           }
         }
 #pragma unroll
@@ -269,6 +322,37 @@ __global__ void __launch_bounds__(128)
   if (tid == 0) bulk_wait<0>();
   report_flag(bad1, flag1);
   report_flag(bad2, flag2);
+  if (dens) {  // fixed-order block sum of the neutrality-mean partials
+    __shared__ double red[4];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) meanacc += __shfl_down_sync(0xffffffffu, meanacc, o);
+    if ((tid & 31) == 0) red[tid >> 5] = meanacc;
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+      dn.mean_part[blockIdx.x] = s;
+    }
+  }
+}
+
+// rc[c2][c1] = sum over CTAs (in order) of the partial slabs; stats[0] =
+// weighted density mean / volume.
+__global__ void xdens_reduce_kernel(const double* __restrict__ part,
+                                    const double* __restrict__ mean_part, int64_t nblocks,
+                                    int64_t cc, double volume, double* __restrict__ rc,
+                                    double* __restrict__ stats) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < cc) {
+    double s = 0.0;
+    for (int64_t b = 0; b < nblocks; ++b) s += part[b * cc + e];
+    rc[e] = s;
+  }
+  if (e == 0 && stats != nullptr) {
+    double s = 0.0;
+    for (int64_t b = 0; b < nblocks; ++b) s += mean_part[b];
+    stats[0] = s / volume;
+  }
 }
 
 static int xplane_sm_count() {
@@ -282,17 +366,18 @@ static int xplane_sm_count() {
   return cached;
 }
 
-template <int P>
-static int launch_xplane(const double* src, double* dst, const int64_t dims[4], const double* a1,
-                         const double* b1, const int64_t* q1, const double* al1,
-                         const double* a2, const double* b2, const int64_t* q2,
-                         const double* al2, int32_t* f1, int32_t* f2, cudaStream_t st) {
+struct XLaunch {
+  int threads, G;
+  size_t smem;
+  int64_t ppb, blocks;
+};
+
+template <int P, bool DENS>
+static int plan_xplane(const int64_t dims[4], XLaunch* L) {
   const int n1 = (int)dims[0];
   const int C1 = n1 / P;
   const int C2 = (int)(dims[1] / P);
-  const int64_t nv1 = dims[2];
   const int64_t nplanes = dims[2] * dims[3];
-  if (nplanes == 0) return VPB_OK;
   if (C1 > 128) {
     set_error("x1 lines of %d cells exceed one CTA", C1);
     return VPB_ERR_UNSUPPORTED;
@@ -301,7 +386,7 @@ static int launch_xplane(const double* src, double* dst, const int64_t dims[4], 
       getenv("VPB_XPLANE_CHUNK") ? atoi(getenv("VPB_XPLANE_CHUNK")) : 4608;
   static const int env_smem =
       getenv("VPB_XPLANE_SMEM") ? atoi(getenv("VPB_XPLANE_SMEM")) : 56 * 1024;
-  const int threads = ((C1 + 31) / 32) * 32;
+  L->threads = ((C1 + 31) / 32) * 32;
   const size_t cell_bytes = (size_t)P * n1 * 8;
   auto smem_for = [&](int g) {
     return (size_t)kXStages * g * cell_bytes + 2 * (size_t)g * cell_bytes + kXStages * 8;
@@ -309,27 +394,136 @@ static int launch_xplane(const double* src, double* dst, const int64_t dims[4], 
   int G = std::max<int>(1, (int)(env_chunk / cell_bytes));
   G = std::min(G, C2);
   while (G > 1 && (int)smem_for(G) > env_smem) --G;
-  const size_t smem = smem_for(G);
-  if (smem > 220 * 1024) {
+  L->G = G;
+  L->smem = smem_for(G);
+  if (L->smem > 220 * 1024) {
     set_error("x plane chunk of %d dofs does not fit shared memory", P * n1);
     return VPB_ERR_UNSUPPORTED;
   }
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(dg_xplane_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(dg_xplane_kernel<P, DENS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          220 * 1024);
     attr = true;
   }
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dg_xplane_kernel<P>, threads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dg_xplane_kernel<P, DENS>, L->threads,
+                                                L->smem);
   if (occ < 1) occ = 1;
-  const int64_t grid = std::min<int64_t>(nplanes, (int64_t)occ * xplane_sm_count());
-  const int64_t ppb = (nplanes + grid - 1) / grid;
-  const int64_t blocks = (nplanes + ppb - 1) / ppb;
-  dg_xplane_kernel<P><<<(unsigned)blocks, threads, smem, st>>>(
-      src, dst, n1, C2, G, nv1, nplanes, ppb, a1, b1, q1, al1, a2, b2, q2, al2, f1, f2);
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(nplanes, (int64_t)occ * xplane_sm_count()));
+  L->ppb = (nplanes + grid - 1) / grid;
+  L->blocks = (nplanes + L->ppb - 1) / L->ppb;
+  return VPB_OK;
+}
+
+template <int P, bool DENS>
+static int launch_xplane(const double* src, double* dst, const int64_t dims[4], const double* a1,
+                         const double* b1, const int64_t* q1, const double* al1,
+                         const double* a2, const double* b2, const int64_t* q2,
+                         const double* al2, int32_t* f1, int32_t* f2, const XDensity& dn,
+                         cudaStream_t st, int64_t* nblocks_out) {
+  const int64_t nplanes = dims[2] * dims[3];
+  if (nplanes == 0) return VPB_OK;
+  XLaunch L;
+  int rc = plan_xplane<P, DENS>(dims, &L);
+  if (rc) return rc;
+  dg_xplane_kernel<P, DENS><<<(unsigned)L.blocks, L.threads, L.smem, st>>>(
+      src, dst, (int)dims[0], (int)(dims[1] / P), L.G, dims[2], nplanes, L.ppb, a1, b1, q1, al1,
+      a2, b2, q2, al2, f1, f2, dn);
+  if (nblocks_out) *nblocks_out = L.blocks;
   return check_launch("dg_xplane_kernel");
 }
+
+template <int P>
+static int xplane_density_len(const int64_t dims[4], int64_t* len) {
+  XLaunch L;
+  int rc = plan_xplane<P, true>(dims, &L);
+  if (rc) return rc;
+  const int64_t cc = (dims[0] / P) * (dims[1] / P);
+  *len = L.blocks * (cc + 1);
+  return VPB_OK;
+}
+
+}  // namespace vpb
+
+using namespace vpb;
+
+#define VPB_XPLANE_SWITCH(order, ...)                                              \
+  switch (order) {                                                                 \
+    case 1: { constexpr int PP = 1; __VA_ARGS__; } break;                                 \
+    case 2: { constexpr int PP = 2; __VA_ARGS__; } break;                                 \
+    case 3: { constexpr int PP = 3; __VA_ARGS__; } break;                                 \
+    case 4: { constexpr int PP = 4; __VA_ARGS__; } break;                                 \
+    case 5: { constexpr int PP = 5; __VA_ARGS__; } break;                                 \
+    case 6: { constexpr int PP = 6; __VA_ARGS__; } break;                                 \
+    case 7: { constexpr int PP = 7; __VA_ARGS__; } break;                                 \
+    case 8: { constexpr int PP = 8; __VA_ARGS__; } break;                                 \
+    default: { constexpr int PP = 9; __VA_ARGS__; } break;                                \
+  }
+
+static int xplane_args_ok(const double* src, const double* dst, const int64_t dims[4],
+                          int32_t order) {
+  VPB_REQUIRE(src != dst, "src and dst must be distinct buffers");
+  VPB_REQUIRE(order >= 1 && order <= kMaxOrder, "order %d outside 1..9", order);
+  VPB_REQUIRE(dims[0] % order == 0 && dims[1] % order == 0, "x axes not whole cells");
+  VPB_REQUIRE(dims[1] > 1, "fused x sweep needs a 2x2v field");
+  VPB_REQUIRE((dims[0] * order) % 2 == 0, "a cell row block must be a multiple of 16 bytes");
+  VPB_REQUIRE((reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
+                  (reinterpret_cast<uintptr_t>(dst) & 15) == 0,
+              "field buffers must be 16-byte aligned");
+  return VPB_OK;
+}
+
+extern "C" int vpb_dg_sweep_xplane(const double* src, double* dst, const int64_t dims[4],
+                                   int32_t order, const double* a1, const double* b1,
+                                   const int64_t* q1, const double* alpha1, const double* a2,
+                                   const double* b2, const int64_t* q2, const double* alpha2,
+                                   int32_t* flag1, int32_t* flag2, void* stream) {
+  int rc = xplane_args_ok(src, dst, dims, order);
+  if (rc) return rc;
+  const XDensity none{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  VPB_XPLANE_SWITCH(order, rc = launch_xplane<PP, false>(src, dst, dims, a1, b1, q1, alpha1, a2,
+                                                  b2, q2, alpha2, flag1, flag2, none,
+                                                  (cudaStream_t)stream, nullptr));
+  return rc;
+}
+
+extern "C" int64_t vpb_dg_xplane_density_work_len(const int64_t dims[4], int32_t order) {
+  if (order < 1 || order > kMaxOrder || dims[0] % order || dims[1] % order) return -1;
+  int64_t len = -1;
+  int rc = VPB_OK;
+  VPB_XPLANE_SWITCH(order, rc = xplane_density_len<PP>(dims, &len));
+  return rc == VPB_OK ? len : -1;
+}
+
+extern "C" int vpb_dg_sweep_xplane_density(
+    const double* src, double* dst, const int64_t dims[4], int32_t order, const double* a1,
+    const double* b1, const int64_t* q1, const double* alpha1, const double* a2,
+    const double* b2, const int64_t* q2, const double* alpha2, int32_t* flag1, int32_t* flag2,
+    const double* wv1, const double* wv2, const double* mid, const double* wx1,
+    const double* wx2, double volume, double* work, double* rc_out, double* stats,
+    void* stream) {
+  int rc = xplane_args_ok(src, dst, dims, order);
+  if (rc) return rc;
+  VPB_REQUIRE(wv1 && wv2 && mid && wx1 && wx2 && work && rc_out, "null pointer");
+  const int64_t cc = (dims[0] / order) * (dims[1] / order);
+  int64_t len = vpb_dg_xplane_density_work_len(dims, order);
+  VPB_REQUIRE(len > 0, "cannot plan the x-plane launch");
+  const int64_t nblk = len / (cc + 1);
+  const XDensity dn{wv1, wv2, mid, wx1, wx2, work, work + nblk * cc};
+  int64_t used = 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  VPB_XPLANE_SWITCH(order, rc = launch_xplane<PP, true>(src, dst, dims, a1, b1, q1, alpha1, a2,
+                                                  b2, q2, alpha2, flag1, flag2, dn, st, &used));
+  if (rc) return rc;
+  VPB_REQUIRE(used == nblk, "x-plane launch plan changed (%lld vs %lld CTAs)", (long long)used,
+              (long long)nblk);
+  xdens_reduce_kernel<<<(unsigned)((cc + 255) / 256), 256, 0, st>>>(work, work + nblk * cc, nblk,
+                                                                    cc, volume, rc_out, stats);
+  return check_launch("xdens_reduce_kernel");
+}
+
+namespace vpb {
 
 // ---------------------------------------------------------------------------
 // Fused velocity sweeps: v1 then v2 (driver.py:231-242 _advect_velocity) in
@@ -723,29 +917,3 @@ extern "C" int vpb_dg_sweep_vplane(const double* src, double* dst, const int64_t
   }
 }
 
-extern "C" int vpb_dg_sweep_xplane(const double* src, double* dst, const int64_t dims[4],
-                                   int32_t order, const double* a1, const double* b1,
-                                   const int64_t* q1, const double* alpha1, const double* a2,
-                                   const double* b2, const int64_t* q2, const double* alpha2,
-                                   int32_t* flag1, int32_t* flag2, void* stream) {
-  VPB_REQUIRE(src != dst, "src and dst must be distinct buffers");
-  VPB_REQUIRE(order >= 1 && order <= kMaxOrder, "order %d outside 1..9", order);
-  VPB_REQUIRE(dims[0] % order == 0 && dims[1] % order == 0, "x axes not whole cells");
-  VPB_REQUIRE(dims[1] > 1, "fused x sweep needs a 2x2v field");
-  VPB_REQUIRE((dims[0] * order) % 2 == 0, "a cell row block must be a multiple of 16 bytes");
-  VPB_REQUIRE((reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
-                  (reinterpret_cast<uintptr_t>(dst) & 15) == 0,
-              "field buffers must be 16-byte aligned");
-  cudaStream_t st = (cudaStream_t)stream;
-  switch (order) {
-    case 1: return launch_xplane<1>(src, dst, dims, a1, b1, q1, alpha1, a2, b2, q2, alpha2, flag1, flag2, st);
-    case 2: return launch_xplane<2>(src, dst, dims, a1, b1, q1, alpha1, a2, b2, q2, alpha2, flag1, flag2, st);
-    case 3: return launch_xplane<3>(src, dst, dims, a1, b1, q1, alpha1, a2, b2, q2, alpha2, flag1, flag2, st);
-    case 4: return launch_xplane<4>(src, dst, dims, a1, b1, q1, alpha1, a2, b2, q2, alpha2, flag1, flag2, st);
-    case 5: return launch_xplane<5>(src, dst, dims, a1, b1, q1, alpha1, a2, b2, q2, alpha2, flag1, flag2, st);
-    case 6: return launch_xplane<6>(src, dst, dims, a1, b1, q1, alpha1, a2, b2, q2, alpha2, flag1, flag2, st);
-    case 7: return launch_xplane<7>(src, dst, dims, a1, b1, q1, alpha1, a2, b2, q2, alpha2, flag1, flag2, st);
-    case 8: return launch_xplane<8>(src, dst, dims, a1, b1, q1, alpha1, a2, b2, q2, alpha2, flag1, flag2, st);
-    default: return launch_xplane<9>(src, dst, dims, a1, b1, q1, alpha1, a2, b2, q2, alpha2, flag1, flag2, st);
-  }
-}

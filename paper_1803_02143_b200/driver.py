@@ -44,6 +44,7 @@ from .spline import sweep_spline
 # the sweeps separately; the results are bitwise identical either way).
 FUSE_X = True
 FUSE_V = True
+FUSE_RHO = True  # density as an epilogue of the opening x pass (dG)
 
 
 class SubstepError(RuntimeError):
@@ -258,6 +259,16 @@ class StepState:
             vsq.append(np.zeros(1))
         self.wv1, self.wv2 = (_device.to_device(w) for w in wv)
         self.v1sq, self.v2sq = (_device.to_device(v) for v in vsq)
+        # density as an epilogue of the opening fused x pass (dG, 2x2v)
+        self.fused_rho = self.fused_x and FUSE_RHO and self.geom.struct_c is not None
+        if self.fused_rho:
+            n = int(lib.vpb_dg_xplane_density_work_len(_lib.dims(grid.dims4), grid.order))
+            if n <= 0:
+                self.fused_rho = False
+            else:
+                self.rho_work = torch.empty(n, dtype=torch.float64, device=dev)
+                self.rc = torch.empty(grid.axes[0].count * grid.axes[1].count,
+                                      dtype=torch.float64, device=dev)
 
     def x_tables(self, d: int, tau: float):
         """Tables for the half x-sweep along space axis d: shift = v_d * (tau/2)."""
@@ -333,13 +344,21 @@ def enqueue_step(field: DistributionField, tau: float, state: StepState | None =
         st.buf = field._swap(out.view(field._phys.shape)).view(-1)
         k += 1
 
-    def advect_space() -> None:  # _advect_space(tau/2)  driver.py:220-228
+    def advect_space(with_density: bool) -> None:  # _advect_space(tau/2)  driver.py:220-228
         nonlocal k
         if st.fused_x:
             out = st.buf
-            mark("sweep_x12")
-            xplane_dg(grid, field._phys.view(-1), out, st.x_tables(0, tau), st.x_tables(1, tau),
-                      st.flags[k:k + 1], st.flags[k + 1:k + 2])
+            if with_density:
+                # x1+x2 sweeps with the cell-centre density of the result as an
+                # epilogue (compute_density + centre collapse, poisson.py:85-139)
+                mark("sweep_x12_rho")
+                xplane_density_dg(grid, field._phys.view(-1), out, st.x_tables(0, tau),
+                                  st.x_tables(1, tau), st.flags[k:k + 1], st.flags[k + 1:k + 2],
+                                  st)
+            else:
+                mark("sweep_x12")
+                xplane_dg(grid, field._phys.view(-1), out, st.x_tables(0, tau),
+                          st.x_tables(1, tau), st.flags[k:k + 1], st.flags[k + 1:k + 2])
             st.buf = field._swap(out.view(field._phys.shape)).view(-1)
             k += 2
             return
@@ -348,11 +367,15 @@ def enqueue_step(field: DistributionField, tau: float, state: StepState | None =
 
     xn = ["x"] if grid.ndim_x == 1 else ["x1", "x2"]
     vn = ["v"] if grid.ndim_x == 1 else ["v1", "v2"]
-    advect_space()  # "open"
-    mark("density")
-    density_into(field.data, grid, st.rho)  # compute_density  poisson.py:85-95
-    mark("field_solve")
-    solve_into(st.rho, grid, st.e, st.stats, st.flags[k:k + 1])  # solve_poisson
+    advect_space(st.fused_rho)  # "open"
+    if st.fused_rho:
+        mark("field_solve")
+        solve_into(st.rc, grid, st.e, None, st.flags[k:k + 1], centred=True)
+    else:
+        mark("density")
+        density_into(field.data, grid, st.rho)  # compute_density  poisson.py:85-95
+        mark("field_solve")
+        solve_into(st.rho, grid, st.e, st.stats, st.flags[k:k + 1])  # solve_poisson
     k += 1
     if st.fused_v:  # _advect_velocity(tau) in one pass  driver.py:231-242
         mark("tables_v12")
@@ -369,8 +392,26 @@ def enqueue_step(field: DistributionField, tau: float, state: StepState | None =
             mark(f"tables_{vn[d]}")
             tab = st.v_tables(d, tau)
             sweep(grid.ndim_x + d, tab, tau, f"sweep_{vn[d]}")
-    advect_space()  # "close"
+    advect_space(False)  # "close"
     mark(None)
+
+
+def xplane_density_dg(grid, src, dst, t1, t2, flag1, flag2, st: StepState) -> None:
+    """Fused x pass whose epilogue writes the cell-centre density of its
+    output to ``st.rc`` and the neutrality mean to ``st.stats[0]``."""
+    lib = _lib.load()
+    g = st.geom
+    _lib.check(
+        lib.vpb_dg_sweep_xplane_density(
+            src.data_ptr(), dst.data_ptr(), _lib.dims(grid.dims4), t1.order, t1.a.data_ptr(),
+            t1.b.data_ptr(), t1.q.data_ptr(), t1.alpha.data_ptr(), t2.a.data_ptr(),
+            t2.b.data_ptr(), t2.q.data_ptr(), t2.alpha.data_ptr(), flag1.data_ptr(),
+            flag2.data_ptr(), st.wv1.data_ptr(), st.wv2.data_ptr(),
+            g.tensors["mid"].data_ptr(), g.tensors["wx1"].data_ptr(),
+            g.tensors["wx2"].data_ptr(), g.volume, st.rho_work.data_ptr(), st.rc.data_ptr(),
+            st.stats.data_ptr(), _device.stream()),
+        "vpb_dg_sweep_xplane_density",
+    )
 
 
 def check_step(state: StepState, time_label: float | None) -> None:

@@ -62,6 +62,8 @@ class FieldGeometry:
     ncomp: int
     tensors: dict
     struct: _lib.FieldGeom
+    struct_c: _lib.FieldGeom | None = None  # cell-centre input variant (dG)
+    volume: float = 0.0
 
     @property
     def work_len(self) -> int:
@@ -135,9 +137,24 @@ def field_geometry(grid: GridSpec, device_index: int) -> FieldGeometry:
         n1, n2, c1, c2, len(comps),
         tensors["g1"].data_ptr(), tensors["g2"].data_ptr(), tensors["m1"].data_ptr(),
         tensors["m2"].data_ptr(), tensors["kmul"].data_ptr(), tensors["wx1"].data_ptr(),
-        tensors["wx2"].data_ptr(), volume,
+        tensors["wx2"].data_ptr(), volume, 0, 0,
     )
-    return FieldGeometry(grid, n1, n2, c1, c2, len(comps), tensors, st)
+    geo = FieldGeometry(grid, n1, n2, c1, c2, len(comps), tensors, st)
+    geo.volume = volume
+    if grid.method == DG and grid.ndim_x == 2:
+        # same solve fed with the density already collapsed to cell centres
+        # (produced by the fused x-plane pass): G = plain DFT on the C grid
+        nodes, _ = gauss_nodes(grid.dg_degree + 1)
+        tensors["f1"] = cplx(_dft_matrix(c1, -1.0))
+        tensors["f2"] = cplx(_dft_matrix(c2, -1.0))
+        tensors["mid"] = _device.to_device(_lagrange_row(nodes, 0.5))
+        geo.struct_c = _lib.FieldGeom(
+            n1, n2, c1, c2, len(comps),
+            tensors["f1"].data_ptr(), tensors["f2"].data_ptr(), tensors["m1"].data_ptr(),
+            tensors["m2"].data_ptr(), tensors["kmul"].data_ptr(), tensors["wx1"].data_ptr(),
+            tensors["wx2"].data_ptr(), volume, c1, c2,
+        )
+    return geo
 
 
 def geometry(grid: GridSpec) -> FieldGeometry:
@@ -215,11 +232,15 @@ def density_into(field_data: torch.Tensor, grid: GridSpec, rho: torch.Tensor) ->
     )
 
 
-def solve_into(rho: torch.Tensor, grid: GridSpec, e: torch.Tensor, stats, flag) -> None:
+def solve_into(rho: torch.Tensor, grid: GridSpec, e: torch.Tensor, stats, flag,
+               centred: bool = False) -> None:
+    """Field from a nodal density, or (``centred``) from the density already
+    collapsed to cell centres by the fused x-plane pass."""
     s = scratch(grid)
     lib = _lib.load()
+    geo = s.geom.struct_c if centred else s.geom.struct
     _lib.check(
-        lib.vpb_field_solve(rho.data_ptr(), s.geom.struct, e.data_ptr(),
+        lib.vpb_field_solve(rho.data_ptr(), geo, e.data_ptr(),
                             None if stats is None else stats.data_ptr(),
                             s.field_work.data_ptr(), None if flag is None else flag.data_ptr(),
                             _device.stream()),

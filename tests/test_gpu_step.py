@@ -301,6 +301,39 @@ def test_fused_v_columns_bitwise_equal_to_separate_sweeps(monkeypatch, order, do
     assert np.array_equal(outs[0], outs[1])
 
 
+@pytest.mark.parametrize("order,dofs", [(3, (24, 18, 12, 15)), (2, (16, 12, 8, 10)),
+                                        (4, (16, 20, 12, 8))])
+def test_density_epilogue_matches_separate_density(monkeypatch, order, dofs):
+    """The opening x pass's cell-centre density epilogue replaces compute_density +
+    collapse; only the summation order changes (<= 1e-14 after several steps)."""
+    prob = vpb.problem_spec("landau4d")
+    grid = vpb.make_grid(prob, "dg", dofs, dg_order=order)
+    outs, e = [], []
+    for fused in (False, True):
+        monkeypatch.setattr(driver, "FUSE_RHO", fused)
+        driver._state_cached.cache_clear()
+        f = vpb.initialize(prob, grid)
+        for _ in range(4):
+            f = vpb.strang_step(f, 0.37, consume=True)
+        st = driver.step_state(grid)
+        assert st.fused_rho == fused
+        outs.append(f.numpy())
+        e.append(st.e.cpu().numpy())
+    driver._state_cached.cache_clear()
+    assert max_rel(outs[1], outs[0]) <= 1e-14
+    assert max_rel(e[1], e[0]) <= 1e-13
+
+
+def test_density_epilogue_keeps_neutrality_warning(monkeypatch):
+    prob = vpb.problem_spec("landau4d")
+    grid = vpb.make_grid(prob, "dg", 12, dg_order=3)
+    driver._state_cached.cache_clear()
+    f = vpb.DistributionField.from_values(grid, np.full(grid.dofs, 0.25))
+    assert driver.step_state(grid).fused_rho
+    with pytest.warns(RuntimeWarning, match="unit background"):
+        vpb.strang_step(f, 0.1)
+
+
 def test_fused_v_reports_nonfinite_field_in_v1():
     prob = vpb.problem_spec("landau4d")
     grid = vpb.make_grid(prob, "dg", 12, dg_order=3)
