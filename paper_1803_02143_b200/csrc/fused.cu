@@ -211,6 +211,15 @@ __global__ void __launch_bounds__(128)
       lo_off = lo * P;
       up_off = up * P;
     }
+    // density epilogue: fetch this chunk's partial-slab entries now so the
+    // load latency hides behind the wait and the sweep arithmetic
+    constexpr int kPre = 4;
+    double pre[kPre];
+    if (dens && active) {
+#pragma unroll
+      for (int i = 0; i < kPre; ++i)
+        pre[i] = i < c.nout ? mypart[(c.first + i) * C1 + tid] : 0.0;
+    }
     mbar_wait(bars + st, phase);
     const double* in = inb + st * slot;
     double* out = outb + (j & 1) * (G * cell);
@@ -292,7 +301,12 @@ __global__ void __launch_bounds__(128)
               rcv += midw[j2] * rrow[j2];
               mv += dn.wx2[oc * P + j2] * mrow[j2];
             }
-            mypart[oc * C1 + tid] += wplane * rcv;
+            double prev = 0.0;
+#pragma unroll
+            for (int i = 0; i < kPre; ++i)
+              if (i == sc) prev = pre[i];
+            if (sc >= kPre) prev = mypart[oc * C1 + tid];
+            mypart[oc * C1 + tid] = prev + wplane * rcv;
             meanacc += wplane * mv;
           }
         }

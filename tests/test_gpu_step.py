@@ -164,8 +164,8 @@ def test_step_reports_broken_field_solve(monkeypatch):
     f = vpb.initialize(prob, grid)
     real = driver.solve_into
 
-    def poisoned(rho, grid_, e, stats, flag):
-        real(rho, grid_, e, stats, flag)
+    def poisoned(rho, grid_, e, stats, flag, **kw):
+        real(rho, grid_, e, stats, flag, **kw)
         e.fill_(math.nan)
         if flag is not None:
             flag.fill_(1)
