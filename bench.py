@@ -273,8 +273,11 @@ def run_sharded(args, cfg_name: str, cfg: dict, d, world: int, rank: int, local:
     clocks = ClockSampler(local).start()
     for _ in range(args.warmup):
         solver.step(tau)
+    from paper_1803_02143_b200 import _lib
+
     barrier(d, local)
     torch.cuda.synchronize()
+    n_launch0 = _lib.load().vpb_launch_count()
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
     clocks.begin()
@@ -285,6 +288,7 @@ def run_sharded(args, cfg_name: str, cfg: dict, d, world: int, rank: int, local:
     torch.cuda.synchronize()
     clocks.end()
     clocks.stop()
+    gpu_launches = _lib.load().vpb_launch_count() - n_launch0  # rank 0's kernels
     barrier(d, local)
     total_ms = allreduce_max(d, start.elapsed_time(end))
     ms_per_step = total_ms / args.steps
@@ -328,7 +332,7 @@ def run_sharded(args, cfg_name: str, cfg: dict, d, world: int, rank: int, local:
                          "unit": "GB/s", "frac": step_gbs / world / peak, "traffic": None,
                          "kernel": "whole step per GPU (96 B/dof)", "peak_source": peak_kind},
             "e2e": e2e, "cpu_baseline": None, "clocks": clocks.summary(),
-            "gpu_launches": None,
+            "gpu_launches": int(gpu_launches),
         }), flush=True)
     if d is not None:
         d.destroy_process_group()
@@ -368,6 +372,27 @@ def run_vpb(args, cfg_name: str, cfg: dict) -> None:
         ev.append(e)
         labels.append(label)
 
+    from paper_1803_02143_b200 import _lib
+
+    lib = _lib.load()
+    graph = None
+    n_launch0 = lib.vpb_launch_count()
+    if args.graph:
+        # --graph: the per-kernel breakdown comes from an eager pass of K steps;
+        # the headline timing replays the whole step from CUDA graphs.
+        e0 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            driver.enqueue_step(field, tau, st, timer=mark)
+            driver.check_step(st, None)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        eager_ms = e0.elapsed_time(e1)
+        eager_launches = lib.vpb_launch_count() - n_launch0
+        graph = driver.StepGraph(field, tau)
+        for _ in range(args.warmup):
+            graph.step()
     barrier(d, local)
     torch.cuda.synchronize()
     start = torch.cuda.Event(enable_timing=True)
@@ -375,17 +400,24 @@ def run_vpb(args, cfg_name: str, cfg: dict) -> None:
     clocks.begin()
     start.record(stream)
     for _ in range(args.steps):
-        driver.enqueue_step(field, tau, st, timer=mark)
-        driver.check_step(st, None)
+        if graph is not None:
+            graph.step()
+        else:
+            driver.enqueue_step(field, tau, st, timer=mark)
+            driver.check_step(st, None)
     end.record(stream)
     torch.cuda.synchronize()
     clocks.end()
     clocks.stop()
+    # kernels launched through libvpb200 in the timed steps (graph replays
+    # launch the same kernels the eager pass counted)
+    gpu_launches = eager_launches if graph is not None else lib.vpb_launch_count() - n_launch0
     barrier(d, local)
     total_ms = start.elapsed_time(end)
     total_ms = allreduce_max(d, total_ms)
     ms_per_step = total_ms / args.steps
     value = world * N * args.steps / (total_ms * 1e-3)
+    breakdown_ms = eager_ms if graph is not None else total_ms
 
     # per-group device time
     groups: dict = {}
@@ -403,7 +435,7 @@ def run_vpb(args, cfg_name: str, cfg: dict) -> None:
     achieved = BYTES_PER_DOF_SWEEP * N / (dom_avg_ms * 1e-3) / 1e9
     step_gbs = 6 * BYTES_PER_DOF_SWEEP * N / (ms_per_step * 1e-3) / 1e9
     per_kernel = {k: {"avg_ms": v[0] / v[1], "launch_groups": v[1],
-                      "share_of_step": v[0] / total_ms}
+                      "share_of_step": v[0] / breakdown_ms}
                   for k, v in sorted(groups.items())}
     for k, v in per_kernel.items():
         if k.startswith("sweep_"):
@@ -441,7 +473,6 @@ def run_vpb(args, cfg_name: str, cfg: dict) -> None:
         cpu = {"value": r["dof_per_s"], "unit": UNIT, "cores": r["threads"], "kind": r["kind"],
                "sample": r["sample"]}
 
-    launches_per_step = {"dg": 6 + 2 + 2 + 5, "spline": 6 + 2 + 5}[cfg["method"]]
     if rank == 0:
         line = {
             "metric": METRIC,
@@ -469,7 +500,8 @@ def run_vpb(args, cfg_name: str, cfg: dict) -> None:
             "e2e": e2e,
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
-            "gpu_launches": launches_per_step * args.steps,
+            "gpu_launches": int(gpu_launches),
+            "cuda_graph": bool(args.graph),
         }
         print(json.dumps(line), flush=True)
     if d is not None:
@@ -486,6 +518,8 @@ def main() -> None:
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", action="store_true",
+                    help="time the step replayed from CUDA graphs (driver.StepGraph)")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent replicas instead of the sharded field")
     ap.add_argument("--traffic", type=float, default=None,

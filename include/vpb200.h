@@ -51,6 +51,9 @@ enum {
 const char* vpb_version(void);
 const char* vpb_strerror(int code);
 const char* vpb_last_error(void);
+/* Kernels launched by this library since load (process-wide, all threads).
+ * Instrumentation for bench.py's gpu_launches; no reference counterpart. */
+unsigned long long vpb_launch_count(void);
 
 /* ------------------------------------------------------------------------
  * Reference plugin API: the four line-kernel entry points.

@@ -50,6 +50,7 @@ SIGNATURES = {
     "vpb_version": (c_char_p, []),
     "vpb_strerror": (c_char_p, [c_int]),
     "vpb_last_error": (c_char_p, []),
+    "vpb_launch_count": (ctypes.c_ulonglong, []),
     "vpb_dg_sweep_contig": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p,
                                     c_void_p, c_void_p, c_void_p, c_int64, c_int32, c_int32,
                                     c_void_p]),

@@ -1,4 +1,5 @@
 // C-ABI error plumbing and version strings.
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 
@@ -24,7 +25,16 @@ int check_launch(const char* what) {
   return VPB_OK;
 }
 
+static std::atomic<unsigned long long> g_launches{0};
+
+int launched(const char* what, int n) {
+  g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed);
+  return check_launch(what);
+}
+
 }  // namespace vpb
+
+extern "C" unsigned long long vpb_launch_count(void) { return vpb::g_launches.load(); }
 
 extern "C" const char* vpb_version(void) { return "vpb200 0.1.0 sm_100a"; }
 

@@ -43,6 +43,8 @@ __device__ __forceinline__ void report_flag(bool bad, int32_t* flag) {
 // ---------------------------------------------------------------------------
 void set_error(const char* fmt, ...);
 int check_launch(const char* what);
+// check_launch + count `n` kernel launches (vpb_launch_count, bench.py gpu_launches)
+int launched(const char* what, int n = 1);
 
 }  // namespace vpb
 

@@ -582,7 +582,7 @@ static int launch_rows(const RowsArgs& g, cudaStream_t st) {
     int64_t blocks = (items + 255) / 256;
     dg_rows_simple_kernel<P><<<(unsigned)blocks, 256, 0, st>>>(
         g.src, g.dst, g.nrows, g.C, g.idx, g.tdiv, g.tmod, g.a, g.b, g.q, g.alpha, g.flag);
-    return check_launch("dg_rows_simple_kernel");
+    return launched("dg_rows_simple_kernel");
   }
   const int target_bytes = 12288;
   int R = (int)std::max<int64_t>(1, target_bytes / (n * 8));
@@ -611,7 +611,7 @@ static int launch_rows(const RowsArgs& g, cudaStream_t st) {
   dg_rows_kernel<P><<<(unsigned)blocks, threads, smem, st>>>(
       g.src, g.dst, g.nrows, g.C, rpb, R, cpp, rpp, g.idx, g.tdiv, g.tmod, g.a, g.b, g.q,
       g.alpha, g.flag);
-  return check_launch("dg_rows_kernel");
+  return launched("dg_rows_kernel");
 }
 
 struct ColsArgs {
@@ -644,7 +644,7 @@ static int launch_cols(const ColsArgs& g, cudaStream_t st) {
     dg_cols_kernel<P, 1><<<(unsigned)blocks, 256, 0, st>>>(
         g.src, g.dst, g.S, g.O, g.C, g.tdiv, g.tmod, g.a, g.b, g.q, g.alpha, g.flag);
   }
-  return check_launch("dg_cols_kernel");
+  return launched("dg_cols_kernel");
 }
 
 #define VPB_DISPATCH_ORDER(P_, FN, ...)                                \
@@ -669,7 +669,7 @@ static int launch_tables(const double* values, int64_t T, double scale, double h
   if (T == 0) return VPB_OK;
   int64_t blocks = (T + 127) / 128;
   dg_tables_kernel<P><<<(unsigned)blocks, 128, 0, st>>>(values, T, scale, h, a, b, q, alpha);
-  return check_launch("dg_tables_kernel");
+  return launched("dg_tables_kernel");
 }
 
 }  // namespace vpb
@@ -724,7 +724,7 @@ extern "C" int vpb_dg_sweep_strided(double* view, const int64_t shape[4],
                                                       shape[2], shape[3], strides[0],
                                                       strides[1], strides[2], strides[3], 1,
                                                       view);
-    rc = check_launch("scatter4d");
+    rc = launched("gather4d_kernel", 2);
   }
   cudaFreeAsync(tmp, st);
   return rc;

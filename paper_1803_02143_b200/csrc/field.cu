@@ -153,7 +153,7 @@ static int zgemm(int64_t M, int64_t N, int64_t K, int batch, ZOp A, ZOp B, const
   ZOp s0 = S ? *S : ZOp{nullptr, 0, 0, 0, 0};
   zgemm_kernel<<<grd, blk, 0, st>>>(M, N, K, A, B, s0, S != nullptr, C, crs, ccs, czs, real_out,
                                     flag);
-  return check_launch("zgemm_kernel");
+  return launched("zgemm_kernel");
 }
 
 // Weighted mean of rho for the neutrality warning (poisson.py:143-160).
@@ -271,10 +271,10 @@ extern "C" int vpb_density(const double* f, const int64_t dims[4], const double*
     density_partial_kernel<2><<<grd, 256, 0, st>>>(f, nx, dims[2], nplanes, per, wv1, wv2, work);
   else
     density_partial_kernel<1><<<grd, 256, 0, st>>>(f, nx, dims[2], nplanes, per, wv1, wv2, work);
-  int rc = check_launch("density_partial_kernel");
+  int rc = launched("density_partial_kernel");
   if (rc) return rc;
   density_final_kernel<<<(unsigned)((nx + 255) / 256), 256, 0, st>>>(work, nch, nx, rho);
-  return check_launch("density_final_kernel");
+  return launched("density_final_kernel");
 }
 
 extern "C" int64_t vpb_field_work_len(const vpb_field_geom* g) {
@@ -295,7 +295,7 @@ extern "C" int vpb_field_solve(const double* rho, const vpb_field_geom* g, doubl
   int rc;
   if (stats && r1 == n1 && r2 == n2) {
     density_mean_kernel<<<1, 1024, 0, st>>>(rho, n1, n2, g->wx1, g->wx2, g->volume, stats);
-    if ((rc = check_launch("density_mean_kernel"))) return rc;
+    if ((rc = launched("density_mean_kernel"))) return rc;
   }
   // T[k1][i2] = sum_i1 G1[k1][i1] R[i1][i2],  R[i1][i2] = rho[i2*r1+i1]
   rc = zgemm(c1, r2, r1, 1, ZOp{g->g1, r1, 1, 1, 0}, ZOp{rho, 1, r1, 0, 0}, nullptr, T, r2, 1, 0,
@@ -328,11 +328,11 @@ extern "C" int vpb_diagnostics(const double* f, const int64_t dims[4], const dou
   const int64_t nplanes = dims[2] * dims[3];
   diag_planes_kernel<<<(unsigned)diag_blocks(dims), kRedThreads, 0, st>>>(f, nx, nplanes, wx,
                                                                             work);
-  int rc = check_launch("diag_planes_kernel");
+  int rc = launched("diag_planes_kernel");
   if (rc) return rc;
   diag_final_kernel<<<1, 1024, 0, st>>>(work, dims[2], dims[3], wv1, wv2, v1sq, v2sq, e, ncomp,
                                         nx, wx, out);
-  return check_launch("diag_final_kernel");
+  return launched("diag_final_kernel");
 }
 
 __global__ void __launch_bounds__(1024)
@@ -352,7 +352,7 @@ extern "C" int vpb_electric_energy(const double* e, int32_t ncomp, int64_t nx, c
   VPB_REQUIRE(e && wx && out, "null pointer");
   VPB_REQUIRE(ncomp == 1 || ncomp == 2, "ncomp must be 1 or 2");
   electric_energy_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(e, ncomp, nx, wx, out);
-  return check_launch("electric_energy_kernel");
+  return launched("electric_energy_kernel");
 }
 
 extern "C" int vpb_fill_separable(double* f, const int64_t dims[4], const double* g1,
@@ -363,5 +363,5 @@ extern "C" int vpb_fill_separable(double* f, const int64_t dims[4], const double
   if (total == 0) return VPB_OK;
   fill_separable_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
       f, nx, dims[2], total, g1, g2, space);
-  return check_launch("fill_separable_kernel");
+  return launched("fill_separable_kernel");
 }

@@ -445,7 +445,7 @@ static int launch_xplane(const double* src, double* dst, const int64_t dims[4], 
       src, dst, (int)dims[0], (int)(dims[1] / P), L.G, dims[2], nplanes, L.ppb, a1, b1, q1, al1,
       a2, b2, q2, al2, f1, f2, dn);
   if (nblocks_out) *nblocks_out = L.blocks;
-  return check_launch("dg_xplane_kernel");
+  return launched("dg_xplane_kernel");
 }
 
 template <int P>
@@ -534,7 +534,7 @@ extern "C" int vpb_dg_sweep_xplane_density(
               (long long)nblk);
   xdens_reduce_kernel<<<(unsigned)((cc + 255) / 256), 256, 0, st>>>(work, work + nblk * cc, nblk,
                                                                     cc, volume, rc_out, stats);
-  return check_launch("xdens_reduce_kernel");
+  return launched("xdens_reduce_kernel");
 }
 
 namespace vpb {
@@ -895,13 +895,13 @@ static int launch_vplane(const double* src, double* dst, const int64_t dims[4], 
       if (smem <= 200 * 1024) {
         dg_vplane_tma_kernel<P><<<grid, 32 * kVCells, smem, st>>>(
             src, dst, nx, C1, C2, a1, b1, q1, al1, a2, b2, q2, al2, f1, f2, tmap);
-        return check_launch("dg_vplane_tma_kernel");
+        return launched("dg_vplane_tma_kernel");
       }
     }
   }
   dg_vplane_kernel<P><<<grid, 32 * kVCells, 0, st>>>(src, dst, nx, C1, C2, a1, b1, q1, al1, a2,
                                                      b2, q2, al2, f1, f2);
-  return check_launch("dg_vplane_kernel");
+  return launched("dg_vplane_kernel");
 }
 
 }  // namespace vpb

@@ -131,7 +131,7 @@ static int launch_halo(const double* src, double* dst, int64_t inner, int64_t ou
   if (total == 0) return VPB_OK;
   dg_halo_kernel<P><<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
       src, dst, inner, outer, C, left, wl, right, wr, tdiv, tmod, a, b, q, alpha, flag);
-  return check_launch("dg_halo_kernel");
+  return launched("dg_halo_kernel");
 }
 
 }  // namespace vpb
@@ -151,7 +151,7 @@ extern "C" int vpb_halo_pack(int32_t axis, const double* f, const int64_t dims[4
   if (total == 0) return VPB_OK;
   halo_pack_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
       f, buf, inner, nax, outer, cell0 * order, width * order);
-  return check_launch("halo_pack_kernel");
+  return launched("halo_pack_kernel");
 }
 
 extern "C" int vpb_dg_sweep_axis_halo(int32_t axis, const double* src, double* dst,

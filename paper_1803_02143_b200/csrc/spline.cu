@@ -541,7 +541,7 @@ static int launch_spline(SplineTileArgs a, bool contig, bool exact, cudaStream_t
     else
       spline_tile_kernel<false, false><<<(unsigned)blocks, kSplineT, smem, st>>>(a, tmap);
   }
-  return check_launch("spline_tile_kernel");
+  return launched("spline_tile_kernel");
 }
 
 __global__ void spline_gather4d_kernel(const double* __restrict__ view, double* __restrict__ lines,
@@ -600,7 +600,7 @@ extern "C" int vpb_spline_sweep_strided(double* view, const int64_t shape[4],
     spline_gather4d_kernel<<<(unsigned)blocks, 256, 0, st>>>(
         nullptr, tmp + total, shape[0], shape[1], shape[2], shape[3], strides[0], strides[1],
         strides[2], strides[3], 1, view);
-    rc = check_launch("spline scatter4d");
+    rc = launched("spline_gather4d_kernel", 2);
   }
   cudaFreeAsync(tmp, st);
   return rc;

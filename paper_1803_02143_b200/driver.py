@@ -44,7 +44,10 @@ from .spline import sweep_spline
 # the sweeps separately; the results are bitwise identical either way).
 FUSE_X = True
 FUSE_V = True
-FUSE_RHO = True  # density as an epilogue of the opening x pass (dG)
+# Density as an epilogue of the opening x pass (dG).  Measured slower on B200
+# than the standalone density pass (which already runs at the HBM roofline):
+# the per-cell partial-slab update adds register pressure to the x pass.
+FUSE_RHO = False
 
 
 class SubstepError(RuntimeError):
@@ -424,6 +427,50 @@ def check_step(state: StepState, time_label: float | None) -> None:
     for k, name in enumerate(state.names):
         if flags[k]:
             raise SubstepError(name, time_label)
+
+
+class StepGraph:
+    """Repeated Strang steps of one field replayed from CUDA graphs.
+
+    The device work of :func:`enqueue_step` (sweeps, tables, density, field
+    solve) is captured once; every :meth:`step` replays it and performs the
+    same per-step non-finite check as :func:`strang_step`.  The field's two
+    buffers ping-pong, so when a step swaps an odd number of times two graphs
+    are captured (one per parity).  Results are bitwise those of
+    ``strang_step(field, tau, consume=True)``.
+    """
+
+    def __init__(self, field: DistributionField, tau: float):
+        self.field = field
+        self.tau = float(tau)
+        self.st = step_state(field.grid)
+        # eager warm-up: caches x tables, allocates v tables, sets kernel attributes
+        enqueue_step(field, tau, self.st)
+        check_step(self.st, None)
+        self.graphs = []
+        self.bufs = []  # (field buffer, scratch buffer) before each graph
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        for _ in range(2):
+            self.bufs.append((field._phys, self.st.buf))
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                enqueue_step(field, tau, self.st)
+            self.graphs.append(g)
+            if field._phys is self.bufs[0][0]:
+                break  # even number of swaps: one graph suffices
+        torch.cuda.current_stream().wait_stream(side)
+        # capture executed nothing: restore the pre-capture buffer roles
+        field._phys, self.st.buf = self.bufs[0]
+        self.parity = 0
+
+    def step(self, time_label: float | None = None) -> DistributionField:
+        self.graphs[self.parity].replay()
+        nxt = (self.parity + 1) % len(self.graphs)  # one graph: roles unchanged
+        self.field._phys, self.st.buf = self.bufs[nxt]
+        self.parity = nxt
+        check_step(self.st, time_label)
+        return self.field
 
 
 def strang_step(field: DistributionField, tau: float, workers: int = 1, consume: bool = False,

@@ -270,6 +270,7 @@ def test_fused_x_planes_bitwise_equal_to_separate_sweeps(monkeypatch, order, dof
     prob = vpb.problem_spec("landau4d")
     grid = vpb.make_grid(prob, "dg", dofs, dg_order=order)
     outs = []
+    monkeypatch.setattr(driver, "FUSE_RHO", False)  # same density path in both runs
     for fused in (False, True):
         monkeypatch.setattr(driver, "FUSE_X", fused)
         driver._state_cached.cache_clear()
@@ -327,11 +328,33 @@ def test_density_epilogue_matches_separate_density(monkeypatch, order, dofs):
 def test_density_epilogue_keeps_neutrality_warning(monkeypatch):
     prob = vpb.problem_spec("landau4d")
     grid = vpb.make_grid(prob, "dg", 12, dg_order=3)
+    monkeypatch.setattr(driver, "FUSE_RHO", True)
     driver._state_cached.cache_clear()
     f = vpb.DistributionField.from_values(grid, np.full(grid.dofs, 0.25))
     assert driver.step_state(grid).fused_rho
     with pytest.warns(RuntimeWarning, match="unit background"):
         vpb.strang_step(f, 0.1)
+    driver._state_cached.cache_clear()
+
+
+@pytest.mark.parametrize("prob,method,dofs,order", [
+    ("landau4d", "dg", 24, 3), ("landau4d", "spline", 16, 0), ("landau2d", "dg", 32, 4),
+    ("twostream4d_baseline", "dg", 16, 2)])
+def test_step_graph_replays_bitwise_equal_to_eager_steps(prob, method, dofs, order):
+    problem = vpb.problem_spec(prob)
+    grid = vpb.make_grid(problem, method, dofs, dg_order=order)
+    f_eager = vpb.initialize(problem, grid)
+    f_graph = vpb.initialize(problem, grid)
+    for _ in range(1):  # StepGraph's constructor performs one eager step
+        f_eager = vpb.strang_step(f_eager, 0.1, consume=True)
+    g = driver.StepGraph(f_graph, 0.1)
+    for m in range(4):
+        f_eager = vpb.strang_step(f_eager, 0.1, consume=True)
+        g.step()
+        assert np.array_equal(f_graph.numpy(), f_eager.numpy()), m
+    f_graph.data[7] = math.nan
+    with pytest.raises(vpb.SubstepError):
+        g.step()
 
 
 def test_fused_v_reports_nonfinite_field_in_v1():
