@@ -126,16 +126,20 @@ int vpb_dg_sweep_vplane(const double* src, double* dst, const int64_t dims[4], i
  * stats[0] = weighted density mean / volume (poisson.py:143-160).  Each CTA
  * accumulates its own planes into `work` (vpb_dg_xplane_density_work_len
  * doubles); a fixed-order pass sums the CTA partials.  Feed rc_out to
- * vpb_field_solve with a geometry whose r1, r2 = C1, C2 and g = DFT. */
+ * vpb_field_solve with a geometry whose r1, r2 = C1, C2 and g = DFT.
+ * wv1, wv2: DEVICE velocity weights.  mid_host: HOST, the `order` Lagrange
+ * weights at the cell centre; wcell1_host / wcell2_host: HOST, the `order`
+ * space quadrature weights of one x1 / x2 cell (uniform grid). */
 int64_t vpb_dg_xplane_density_work_len(const int64_t dims[4], int32_t order);
 int vpb_dg_sweep_xplane_density(const double* src, double* dst, const int64_t dims[4],
                                 int32_t order, const double* a1, const double* b1,
                                 const int64_t* q1, const double* alpha1, const double* a2,
                                 const double* b2, const int64_t* q2, const double* alpha2,
                                 int32_t* flag1, int32_t* flag2, const double* wv1,
-                                const double* wv2, const double* mid, const double* wx1,
-                                const double* wx2, double volume, double* work, double* rc_out,
-                                double* stats, void* stream);
+                                const double* wv2, const double* mid_host,
+                                const double* wcell1_host, const double* wcell2_host,
+                                double volume, double* work, double* rc_out, double* stats,
+                                void* stream);
 
 /* One spline sweep along `axis`; shift of line = values[table row]*scale. */
 int vpb_spline_sweep_axis(int32_t axis, const double* src, double* dst, const int64_t dims[4],

@@ -8,6 +8,7 @@ every compute entry point raises.
 from __future__ import annotations
 
 import ctypes
+import os
 from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_int64, c_void_p
 from pathlib import Path
 
@@ -109,7 +110,8 @@ def load(path: Path | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    p = Path(path) if path else _LIB_PATH
+    # VPB_LIB: load another build of the same ABI (A/B timing of kernel variants)
+    p = Path(path) if path else Path(os.environ.get("VPB_LIB") or _LIB_PATH)
     if not p.exists():
         raise VpbError(
             f"vpb200 CUDA library not found at {p}; build it with "

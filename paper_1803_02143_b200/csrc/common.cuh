@@ -32,6 +32,17 @@ __device__ __forceinline__ bool not_finite(double x) {
   return (__double_as_longlong(x) & 0x7ff0000000000000LL) == 0x7ff0000000000000LL;
 }
 
+// Running non-finite test on the integer pipe: the maximum exponent field
+// seen.  (ptxas turns the compare form above into one DSETP per value on
+// the fp64 pipe, which the hot sweeps need for their arithmetic.)
+struct ExpMax {
+  uint32_t m = 0;
+  __device__ __forceinline__ void add(double x) {
+    m = max(m, (uint32_t)__double2hiint(x) & 0x7ff00000u);
+  }
+  __device__ __forceinline__ bool bad() const { return m == 0x7ff00000u; }
+};
+
 // Non-finite report into a device flag word (the per-sub-step finite check
 // of driver.py:209-211, moved into the producing kernel's epilogue).
 __device__ __forceinline__ void report_flag(bool bad, int32_t* flag) {

@@ -26,6 +26,7 @@
 // contiguous run of planes; the load ring runs ahead across planes.
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "async_copy.cuh"
 #include "common.cuh"
@@ -91,20 +92,78 @@ __device__ __forceinline__ void lds_row_cell(const double* p, double (&u)[P]) {
   }
 }
 
+// x1 sweep of one source x2 cell (P rows) for this thread's x1 cell
+// (_kernels.pyx:113-123): g[m2][j] = sum_m A1[j][m] u_lo[m] + sum_m B1[j][m] u_up[m].
+template <int P, bool EX1>
+__device__ __forceinline__ void xplane_x1_cell(const double* rows, int n1, int lo_off,
+                                               int up_off, const double (&A1)[P][P],
+                                               const double (&B1)[P][P], double (&g)[P][P]) {
+#pragma unroll
+  for (int m2 = 0; m2 < P; ++m2) {
+    const double* row = rows + m2 * n1;
+    double uu[P];
+    lds_row_cell<P>(row + up_off, uu);
+    if constexpr (EX1) {
+#pragma unroll
+      for (int jj = 0; jj < P; ++jj) g[m2][jj] = uu[jj];
+    } else {
+      double ul[P];
+      lds_row_cell<P>(row + lo_off, ul);
+#pragma unroll
+      for (int jj = 0; jj < P; ++jj) {
+        double acc_a = dmul(A1[jj][0], ul[0]);
+#pragma unroll
+        for (int m = 1; m < P; ++m) acc_a = dadd(acc_a, dmul(A1[jj][m], ul[m]));
+        double acc_b = dmul(B1[jj][0], uu[0]);
+#pragma unroll
+        for (int m = 1; m < P; ++m) acc_b = dadd(acc_b, dmul(B1[jj][m], uu[m]));
+        g[m2][jj] = dadd(acc_a, acc_b);
+      }
+    }
+  }
+}
+
+// x2 sweep of one output cell from the x1-swept source cells gp (= s-1) and
+// g (= s): o[j2][jj] = sum_m A2[j2][m] gp[m][jj] + sum_m B2[j2][m] g[m][jj].
+template <int P, bool EX2>
+__device__ __forceinline__ void xplane_x2_cell(const double (&A2)[P][P], const double (&B2)[P][P],
+                                               const double (&gp)[P][P], const double (&g)[P][P],
+                                               double (&o)[P][P]) {
+#pragma unroll
+  for (int j2 = 0; j2 < P; ++j2)
+#pragma unroll
+    for (int jj = 0; jj < P; ++jj) {
+      if constexpr (EX2) {
+        o[j2][jj] = g[j2][jj];
+      } else {
+        double acc_a = dmul(A2[j2][0], gp[0][jj]);
+#pragma unroll
+        for (int m = 1; m < P; ++m) acc_a = dadd(acc_a, dmul(A2[j2][m], gp[m][jj]));
+        double acc_b = dmul(B2[j2][0], g[0][jj]);
+#pragma unroll
+        for (int m = 1; m < P; ++m) acc_b = dadd(acc_b, dmul(B2[j2][m], g[m][jj]));
+        o[j2][jj] = dadd(acc_a, acc_b);
+      }
+    }
+}
+
 // Optional density epilogue of the x-plane pass (poisson.py:85-95 followed by
 // the cell-centre collapse of poisson.py:129-139): every output P x P cell
-// block is collapsed with the Lagrange weights at the cell centre, weighted by
-// the plane's velocity weight, and accumulated into the CTA's own partial
-// slab [C2][C1] (thread c owns column c: no atomics, fixed order).  The
-// neutrality mean (poisson.py:143-160) rides along as a per-CTA scalar.
+// block is collapsed with the Lagrange weights at the cell centre (for odd P
+// the centre is the middle Gauss node and the collapse is a selection),
+// weighted by the plane's velocity weight, and added into the CTA's own
+// partial slab [C2][C1] with a fire-and-forget reduction (RED; only thread c
+// touches column c of its CTA's slab, so the order is program order and the
+// result deterministic).  The neutrality mean (poisson.py:143-160) rides
+// along as a per-thread scalar.  The cell weight tables live in the kernel
+// parameters (constant bank operands, no registers).
 struct XDensity {
   const double* wv1;   // [nv1] velocity weights
   const double* wv2;   // [nv2]
-  const double* mid;   // [P] Lagrange basis at xi = 1/2
-  const double* wx1;   // [n1] space weights
-  const double* wx2;   // [n2]
   double* rc_part;     // [grid][C2][C1] or nullptr (epilogue off)
   double* mean_part;   // [grid]
+  double mm[kMaxOrder * kMaxOrder];  // mid[j2] * mid[jj]
+  double ww[kMaxOrder * kMaxOrder];  // cell space weights wcell2[j2] * wcell1[jj]
 };
 
 template <int P, bool DENS>
@@ -175,17 +234,10 @@ __global__ void __launch_bounds__(128)
   uint32_t phase = 0;
   // density epilogue state
   constexpr bool dens = DENS;
-  double midw[P], wxc[P];
   double wplane = 0.0, meanacc = 0.0;
   double* mypart = dens ? dn.rc_part + (int64_t)blockIdx.x * C2 * C1 : nullptr;
-  if (dens && active) {
-#pragma unroll
-    for (int m = 0; m < P; ++m) {
-      midw[m] = dn.mid[m];
-      wxc[m] = dn.wx1[tid * P + m];
-    }
+  if (dens && active)
     for (int c2 = 0; c2 < C2; ++c2) mypart[c2 * C1 + tid] = 0.0;
-  }
 
   for (int64_t j = 0; j < nchunks; ++j) {
     const XChunk c = cur.chunk(G, C2);
@@ -211,103 +263,69 @@ __global__ void __launch_bounds__(128)
       lo_off = lo * P;
       up_off = up * P;
     }
-    // density epilogue: fetch this chunk's partial-slab entries now so the
-    // load latency hides behind the wait and the sweep arithmetic
-    constexpr int kPre = 4;
-    double pre[kPre];
-    if (dens && active) {
-#pragma unroll
-      for (int i = 0; i < kPre; ++i)
-        pre[i] = i < c.nout ? mypart[(c.first + i) * C1 + tid] : 0.0;
-    }
     mbar_wait(bars + st, phase);
     const double* in = inb + st * slot;
     double* out = outb + (j & 1) * (G * cell);
-    if (active) {
+    // One body per (ex1, ex2) combination: the alpha == 0 exact-shift cases
+    // are uniform over a plane, so the branch is hoisted out of the cell loop.
+    auto run_cells = [&](auto ex1c, auto ex2c) {
+      constexpr bool E1 = decltype(ex1c)::value, E2 = decltype(ex2c)::value;
       for (int sc = 0; sc < c.nsrc; ++sc) {
         double g[P][P];
-#pragma unroll
-        for (int m2 = 0; m2 < P; ++m2) {
-          // x1 sweep of row m2 of source cell sc, this thread's cell (_kernels.pyx:113-123)
-          const double* row = in + (sc * P + m2) * n1;
-          double uu[P];
-          lds_row_cell<P>(row + up_off, uu);
-          if (ex1) {
-#pragma unroll
-            for (int jj = 0; jj < P; ++jj) g[m2][jj] = uu[jj];
-          } else {
-            double ul[P];
-            lds_row_cell<P>(row + lo_off, ul);
-#pragma unroll
-            for (int jj = 0; jj < P; ++jj) {
-              double acc_a = dmul(A1[jj][0], ul[0]);
-#pragma unroll
-              for (int m = 1; m < P; ++m) acc_a = dadd(acc_a, dmul(A1[jj][m], ul[m]));
-              double acc_b = dmul(B1[jj][0], uu[0]);
-#pragma unroll
-              for (int m = 1; m < P; ++m) acc_b = dadd(acc_b, dmul(B1[jj][m], uu[m]));
-              g[m2][jj] = dadd(acc_a, acc_b);
-            }
-          }
-#pragma unroll
-          for (int jj = 0; jj < P; ++jj) bad1 |= not_finite(g[m2][jj]);
-        }
+        xplane_x1_cell<P, E1>(in + sc * cell, n1, lo_off, up_off, A1, B1, g);
         if (c.nout > 0) {
-          // x2 sweep for output x2 cell c.first + sc: rows j2, dofs jj of this cell
+          // x2 sweep for output x2 cell c.first + sc
+          double o[P][P];
+          xplane_x2_cell<P, E2>(A2, B2, gp, g, o);
+          ExpMax eo;
+#pragma unroll
+          for (int j2 = 0; j2 < P; ++j2)
+#pragma unroll
+            for (int jj = 0; jj < P; ++jj) eo.add(o[j2][jj]);
+          if (eo.bad()) {
+            // Every x1 value enters the output cell it is the B-side source
+            // of through a product, so a non-finite x1 result always shows up
+            // here: only then look at g to name the sub-step (x1 vs x2).
+            bad2 = true;
+            ExpMax eg;
+#pragma unroll
+            for (int m2 = 0; m2 < P; ++m2)
+#pragma unroll
+              for (int jj = 0; jj < P; ++jj) eg.add(g[m2][jj]);
+            bad1 |= eg.bad();
+          }
           double* otile = out + sc * cell + tid * P;
-          double rrow[P], mrow[P];
 #pragma unroll
           for (int j2 = 0; j2 < P; ++j2) {
-            double o[P];
-#pragma unroll
-            for (int jj = 0; jj < P; ++jj) {
-              if (ex2) {
-                o[jj] = g[j2][jj];
-              } else {
-                double acc_a = dmul(A2[j2][0], gp[0][jj]);
-#pragma unroll
-                for (int m = 1; m < P; ++m) acc_a = dadd(acc_a, dmul(A2[j2][m], gp[m][jj]));
-                double acc_b = dmul(B2[j2][0], g[0][jj]);
-#pragma unroll
-                for (int m = 1; m < P; ++m) acc_b = dadd(acc_b, dmul(B2[j2][m], g[m][jj]));
-                o[jj] = dadd(acc_a, acc_b);
-              }
-              bad2 |= not_finite(o[jj]);
-            }
             if constexpr (P % 2 == 0) {
 #pragma unroll
               for (int jj = 0; jj < P; jj += 2)
-                *reinterpret_cast<double2*>(otile + j2 * n1 + jj) = make_double2(o[jj], o[jj + 1]);
+                *reinterpret_cast<double2*>(otile + j2 * n1 + jj) =
+                    make_double2(o[j2][jj], o[j2][jj + 1]);
             } else {
 #pragma unroll
-              for (int jj = 0; jj < P; ++jj) otile[j2 * n1 + jj] = o[jj];
-            }
-            if (dens) {
-              double r = 0.0, mw = 0.0;
-#pragma unroll
-              for (int jj = 0; jj < P; ++jj) {
-                r += midw[jj] * o[jj];
-                mw += wxc[jj] * o[jj];
-              }
-              rrow[j2] = r;
-              mrow[j2] = mw;
+              for (int jj = 0; jj < P; ++jj) otile[j2 * n1 + jj] = o[j2][jj];
             }
           }
-          if (dens) {
-            const int oc = c.first + sc;
-            double rcv = 0.0, mv = 0.0;
+          if constexpr (DENS) {
+            double rcv, mv = 0.0;
+            if constexpr (P % 2 == 1) {
+              rcv = o[P / 2][P / 2];  // mid = e_centre exactly (checked on the host)
+            } else {
+              // the density feeds a spectral solve that is not bitwise anyway:
+              // contracted arithmetic is fine here
+              rcv = 0.0;
 #pragma unroll
-            for (int j2 = 0; j2 < P; ++j2) {
-              rcv += midw[j2] * rrow[j2];
-              mv += dn.wx2[oc * P + j2] * mrow[j2];
+              for (int j2 = 0; j2 < P; ++j2)
+#pragma unroll
+                for (int jj = 0; jj < P; ++jj) rcv = fma(dn.mm[j2 * P + jj], o[j2][jj], rcv);
             }
-            double prev = 0.0;
 #pragma unroll
-            for (int i = 0; i < kPre; ++i)
-              if (i == sc) prev = pre[i];
-            if (sc >= kPre) prev = mypart[oc * C1 + tid];
-            mypart[oc * C1 + tid] = prev + wplane * rcv;
-            meanacc += wplane * mv;
+            for (int j2 = 0; j2 < P; ++j2)
+#pragma unroll
+              for (int jj = 0; jj < P; ++jj) mv = fma(dn.ww[j2 * P + jj], o[j2][jj], mv);
+            atomicAdd(mypart + (c.first + sc) * C1 + tid, dmul(wplane, rcv));
+            meanacc = fma(wplane, mv, meanacc);
           }
         }
 #pragma unroll
@@ -315,6 +333,14 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
           for (int jj = 0; jj < P; ++jj) gp[m2][jj] = g[m2][jj];
       }
+    };
+    if (active) {
+      using F = std::false_type;
+      using T = std::true_type;
+      if (!ex1 && !ex2) run_cells(F{}, F{});
+      else if (!ex1) run_cells(F{}, T{});
+      else if (!ex2) run_cells(T{}, F{});
+      else run_cells(T{}, T{});
     }
     fence_proxy_async_smem();
     if (tid == 0) bulk_wait_read<0>();  // store of chunk j-1 released the other tile
@@ -495,7 +521,7 @@ extern "C" int vpb_dg_sweep_xplane(const double* src, double* dst, const int64_t
                                    int32_t* flag1, int32_t* flag2, void* stream) {
   int rc = xplane_args_ok(src, dst, dims, order);
   if (rc) return rc;
-  const XDensity none{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  const XDensity none{nullptr, nullptr, nullptr, nullptr, {}, {}};
   VPB_XPLANE_SWITCH(order, rc = launch_xplane<PP, false>(src, dst, dims, a1, b1, q1, alpha1, a2,
                                                   b2, q2, alpha2, flag1, flag2, none,
                                                   (cudaStream_t)stream, nullptr));
@@ -514,17 +540,27 @@ extern "C" int vpb_dg_sweep_xplane_density(
     const double* src, double* dst, const int64_t dims[4], int32_t order, const double* a1,
     const double* b1, const int64_t* q1, const double* alpha1, const double* a2,
     const double* b2, const int64_t* q2, const double* alpha2, int32_t* flag1, int32_t* flag2,
-    const double* wv1, const double* wv2, const double* mid, const double* wx1,
-    const double* wx2, double volume, double* work, double* rc_out, double* stats,
+    const double* wv1, const double* wv2, const double* mid_host, const double* wcell1_host,
+    const double* wcell2_host, double volume, double* work, double* rc_out, double* stats,
     void* stream) {
   int rc = xplane_args_ok(src, dst, dims, order);
   if (rc) return rc;
-  VPB_REQUIRE(wv1 && wv2 && mid && wx1 && wx2 && work && rc_out, "null pointer");
+  VPB_REQUIRE(wv1 && wv2 && mid_host && wcell1_host && wcell2_host && work && rc_out,
+              "null pointer");
+  if (order % 2 == 1)
+    for (int j = 0; j < order; ++j)
+      VPB_REQUIRE(mid_host[j] == (j == order / 2 ? 1.0 : 0.0),
+                  "odd-order centre weights must select the middle node");
   const int64_t cc = (dims[0] / order) * (dims[1] / order);
   int64_t len = vpb_dg_xplane_density_work_len(dims, order);
   VPB_REQUIRE(len > 0, "cannot plan the x-plane launch");
   const int64_t nblk = len / (cc + 1);
-  const XDensity dn{wv1, wv2, mid, wx1, wx2, work, work + nblk * cc};
+  XDensity dn{wv1, wv2, work, work + nblk * cc, {}, {}};
+  for (int j2 = 0; j2 < order; ++j2)
+    for (int jj = 0; jj < order; ++jj) {
+      dn.mm[j2 * order + jj] = mid_host[j2] * mid_host[jj];
+      dn.ww[j2 * order + jj] = wcell2_host[j2] * wcell1_host[jj];
+    }
   int64_t used = 0;
   cudaStream_t st = (cudaStream_t)stream;
   VPB_XPLANE_SWITCH(order, rc = launch_xplane<PP, true>(src, dst, dims, a1, b1, q1, alpha1, a2,
@@ -586,7 +622,7 @@ __global__ void __launch_bounds__(32 * kVCells)
   const int up1 = lo1 + 1 == C1 ? 0 : lo1 + 1;
   const double* lo_base = src + (int64_t)lo1 * P * nx + x;
   const double* up_base = src + (int64_t)up1 * P * nx + x;
-  bool bad1 = false, bad2 = false;
+  ExpMax e1, e2;  // integer-pipe non-finite tracking
 
   // v1 sweep of source v2 cell s: g[m2][j1] for the P v2 rows of the cell
   auto v1_cell = [&](int s, double (&g)[P][P]) {
@@ -617,7 +653,7 @@ __global__ void __launch_bounds__(32 * kVCells)
           v = dadd(acc_a, acc_b);
         }
         g[m2][j] = v;
-        bad1 |= not_finite(v);
+        e1.add(v);
       }
   };
 
@@ -648,7 +684,7 @@ __global__ void __launch_bounds__(32 * kVCells)
           for (int m = 1; m < P; ++m) acc_b = dadd(acc_b, dmul(B2[j2][m], g[m][j]));
           o = dadd(acc_a, acc_b);
         }
-        bad2 |= not_finite(o);
+        e2.add(o);
         __stcs(out + j2 * row_stride + j * nx, o);
       }
 #pragma unroll
@@ -656,8 +692,8 @@ __global__ void __launch_bounds__(32 * kVCells)
 #pragma unroll
       for (int j = 0; j < P; ++j) gp[m2][j] = g[m2][j];
   }
-  report_flag(bad1, flag1);
-  report_flag(bad2, flag2);
+  report_flag(e1.bad(), flag1);
+  report_flag(e2.bad(), flag2);
 }
 
 // TMA-staged variant.  A CTA owns 32 consecutive x (one per lane) and kVCells
@@ -774,7 +810,10 @@ __global__ void __launch_bounds__(32 * kVCells)
   if (use_tma && threadIdx.x == 0)
     for (int k = 0; k < kVStages && k <= C2; ++k) issue(k);
 
-  auto v1_cell = [&](int k, double (&g)[P][P]) {
+  // GEN: per-lane alpha == 0 exact-shift branches; otherwise the common
+  // all-lanes-interpolate body without them.
+  auto v1_cell = [&](int k, double (&g)[P][P], auto genc) {
+    constexpr bool GEN = decltype(genc)::value;
     double ul[P][P], uu[P][P];
     if (use_tma) {
       const int sl = k % kVStages;
@@ -803,7 +842,7 @@ __global__ void __launch_bounds__(32 * kVCells)
 #pragma unroll
       for (int j = 0; j < P; ++j) {
         double v;
-        if (ex1) {
+        if (GEN && ex1) {
           v = uu[m2][j];
         } else {
           double acc_a = dmul(A1[j][0], ul[m2][0]);
@@ -815,7 +854,6 @@ __global__ void __launch_bounds__(32 * kVCells)
           v = dadd(acc_a, acc_b);
         }
         g[m2][j] = v;
-        bad1 |= not_finite(v);
       }
   };
   auto release = [&](int k) {  // every thread is done with slot k % kVStages
@@ -823,10 +861,61 @@ __global__ void __launch_bounds__(32 * kVCells)
     if (use_tma && threadIdx.x == 0 && k + kVStages <= C2) issue(k + kVStages);
   };
 
+  // Non-finite values: only the outputs are tested in the common path; an
+  // x1 (v1) result always reaches the output cell it is the B-side source of
+  // through a product, so g is examined (to name the sub-step) only when that
+  // output cell is bad.
+  auto step = [&](int k, double (&gp)[P][P], int c2, auto genc) {
+    constexpr bool GEN = decltype(genc)::value;
+    double g[P][P];
+    v1_cell(k, g, genc);
+    double* out = dst + ((int64_t)c2 * P) * row_stride + (int64_t)c1 * P * nx + x;
+    ExpMax eo;
+#pragma unroll
+    for (int j2 = 0; j2 < P; ++j2)
+#pragma unroll
+      for (int j = 0; j < P; ++j) {
+        double o;
+        if (GEN && ex2) {
+          o = g[j2][j];
+        } else {
+          double acc_a = dmul(A2[j2][0], gp[0][j]);
+#pragma unroll
+          for (int m = 1; m < P; ++m) acc_a = dadd(acc_a, dmul(A2[j2][m], gp[m][j]));
+          double acc_b = dmul(B2[j2][0], g[0][j]);
+#pragma unroll
+          for (int m = 1; m < P; ++m) acc_b = dadd(acc_b, dmul(B2[j2][m], g[m][j]));
+          o = dadd(acc_a, acc_b);
+        }
+        eo.add(o);
+        __stcs(out + j2 * row_stride + j * nx, o);
+      }
+    if (eo.bad()) {
+      bad2 = true;
+      ExpMax eg;
+#pragma unroll
+      for (int m2 = 0; m2 < P; ++m2)
+#pragma unroll
+        for (int j = 0; j < P; ++j) eg.add(g[m2][j]);
+      bad1 |= eg.bad();
+    }
+#pragma unroll
+    for (int m2 = 0; m2 < P; ++m2)
+#pragma unroll
+      for (int j = 0; j < P; ++j) gp[m2][j] = g[m2][j];
+  };
+  // the exact-shift branches are needed only if some lane of the block has them
+  const bool gen = __syncthreads_or(active && (ex1 || ex2)) != 0;
+
   double gp[P][P];
   uint32_t phase = 0;
   if (use_tma) mbar_wait(bars + 0, 0);
-  if (active) v1_cell(0, gp);
+  if (active) {
+    if (gen)
+      v1_cell(0, gp, std::true_type{});
+    else
+      v1_cell(0, gp, std::false_type{});
+  }
   release(0);
   int c2 = qm2;  // output cell of source cell s: s + q2 (mod C2); s = 1 first
   for (int k = 1; k <= C2; ++k) {
@@ -835,32 +924,10 @@ __global__ void __launch_bounds__(32 * kVCells)
     if (use_tma) mbar_wait(bars + sl, phase);
     if (++c2 == C2) c2 = 0;
     if (active) {
-      double g[P][P];
-      v1_cell(k, g);
-      double* out = dst + ((int64_t)c2 * P) * row_stride + (int64_t)c1 * P * nx + x;
-#pragma unroll
-      for (int j2 = 0; j2 < P; ++j2)
-#pragma unroll
-        for (int j = 0; j < P; ++j) {
-          double o;
-          if (ex2) {
-            o = g[j2][j];
-          } else {
-            double acc_a = dmul(A2[j2][0], gp[0][j]);
-#pragma unroll
-            for (int m = 1; m < P; ++m) acc_a = dadd(acc_a, dmul(A2[j2][m], gp[m][j]));
-            double acc_b = dmul(B2[j2][0], g[0][j]);
-#pragma unroll
-            for (int m = 1; m < P; ++m) acc_b = dadd(acc_b, dmul(B2[j2][m], g[m][j]));
-            o = dadd(acc_a, acc_b);
-          }
-          bad2 |= not_finite(o);
-          __stcs(out + j2 * row_stride + j * nx, o);
-        }
-#pragma unroll
-      for (int m2 = 0; m2 < P; ++m2)
-#pragma unroll
-        for (int j = 0; j < P; ++j) gp[m2][j] = g[m2][j];
+      if (gen)
+        step(k, gp, c2, std::true_type{});
+      else
+        step(k, gp, c2, std::false_type{});
     }
     release(k);
   }

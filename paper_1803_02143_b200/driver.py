@@ -18,6 +18,7 @@ sub-steps of a failing step still execute before the error is raised.)
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 from functools import lru_cache
 
@@ -27,10 +28,11 @@ import torch
 from . import _device, _lib
 from .dg import DeviceTables, sweep_dg, vplane_dg, xplane_dg
 from .field import DEFAULT_STRATEGY, DistributionField, LayoutDescriptor, write_snapshot
-from .grid import DG, SPACE, SPLINE, VELOCITY, Axis, GridSpec
+from .grid import DG, SPACE, SPLINE, VELOCITY, Axis, GridSpec, gauss_nodes
 from .poisson import (
     ElectricField,
     _device_x,
+    _lagrange_row,
     _warn_if_not_neutral,
     density_into,
     geometry,
@@ -44,10 +46,9 @@ from .spline import sweep_spline
 # the sweeps separately; the results are bitwise identical either way).
 FUSE_X = True
 FUSE_V = True
-# Density as an epilogue of the opening x pass (dG).  Measured slower on B200
-# than the standalone density pass (which already runs at the HBM roofline):
-# the per-cell partial-slab update adds register pressure to the x pass.
-FUSE_RHO = False
+# Density as an epilogue of the opening x pass (dG): saves the 8 B/dof read
+# of the standalone density pass.  VPB_FUSE_RHO=0/1 overrides the default.
+FUSE_RHO = os.environ.get("VPB_FUSE_RHO", "1") != "0"
 
 
 class SubstepError(RuntimeError):
@@ -272,6 +273,19 @@ class StepState:
                 self.rho_work = torch.empty(n, dtype=torch.float64, device=dev)
                 self.rc = torch.empty(grid.axes[0].count * grid.axes[1].count,
                                       dtype=torch.float64, device=dev)
+                # host constants of the epilogue: centre Lagrange weights and
+                # the space quadrature weights of one cell per axis
+                p = grid.order
+                nodes, _ = gauss_nodes(p)
+                self.dens_mid = np.ascontiguousarray(_lagrange_row(nodes, 0.5))
+                cells = []
+                for a in (0, 1):
+                    w = np.asarray(grid.axis_weights(a), dtype=np.float64)
+                    cell = np.ascontiguousarray(w[:p])
+                    if not np.array_equal(w.reshape(-1, p), np.broadcast_to(cell, (w.size // p, p))):
+                        self.fused_rho = False  # non-uniform cells: keep the separate density
+                    cells.append(cell)
+                self.dens_w1, self.dens_w2 = cells
 
     def x_tables(self, d: int, tau: float):
         """Tables for the half x-sweep along space axis d: shift = v_d * (tau/2)."""
@@ -410,8 +424,8 @@ def xplane_density_dg(grid, src, dst, t1, t2, flag1, flag2, st: StepState) -> No
             t1.b.data_ptr(), t1.q.data_ptr(), t1.alpha.data_ptr(), t2.a.data_ptr(),
             t2.b.data_ptr(), t2.q.data_ptr(), t2.alpha.data_ptr(), flag1.data_ptr(),
             flag2.data_ptr(), st.wv1.data_ptr(), st.wv2.data_ptr(),
-            g.tensors["mid"].data_ptr(), g.tensors["wx1"].data_ptr(),
-            g.tensors["wx2"].data_ptr(), g.volume, st.rho_work.data_ptr(), st.rc.data_ptr(),
+            st.dens_mid.ctypes.data, st.dens_w1.ctypes.data, st.dens_w2.ctypes.data,
+            g.volume, st.rho_work.data_ptr(), st.rc.data_ptr(),
             st.stats.data_ptr(), _device.stream()),
         "vpb_dg_sweep_xplane_density",
     )
