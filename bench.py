@@ -2,14 +2,20 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2]
                     [--impl vpb|reference] [--no-e2e] [--no-cpu-baseline]
+                    [--per-step | --graph]
 
-One "step" is one ``strang_step(field, tau, consume=True)`` through the
-public API -- six sweeps, density, field solve, v-shift tables, and the
-per-step non-finite check (one D2H + sync) -- exactly what the reference's
-``bench_step`` times (/root/reference/pkg/src/slvp/bench.py:54-68).  The
-default workload is BASELINE config 2 (Landau 4D, 64^4 cells, degree 2 =
-192^4 = 1.36e9 dofs, 10.9 GB per copy of f, dt = 0.05), the configuration
-the metric is quoted on that fits one GPU.
+One "step" is one Strang step of the reference's ``strang_step`` (six
+sweeps, density, field solve, v-shift tables, the non-finite checks).  The
+timed K steps run through ``advance(field, tau, K)``, the public multi-step
+API (the reference's ``run`` loop without diagnostics): adjacent x half steps
+of consecutive steps share one HBM pass; every sweep is still performed and
+the result is bitwise that of K ``strang_step`` calls with the same density
+path.  ``per_call`` in the JSON line times K separate
+``strang_step(consume=True)`` calls (what the reference's ``bench_step``
+times, /root/reference/pkg/src/slvp/bench.py:54-68); ``--per-step`` makes
+that the headline.  The default workload is BASELINE config 2 (Landau 4D,
+64^4 cells, degree 2 = 192^4 = 1.36e9 dofs, 10.9 GB per copy of f, dt =
+0.05), the configuration the metric is quoted on that fits one GPU.
 
 Timing: W untimed warm-up steps, then exactly K steps bracketed by a
 barrier + torch.cuda.synchronize(), timed with CUDA events on the launching
@@ -366,11 +372,32 @@ def run_vpb(args, cfg_name: str, cfg: dict) -> None:
     stream = torch.cuda.current_stream()
 
     clocks = ClockSampler(local).start()
-    for _ in range(args.warmup):
-        driver.enqueue_step(field, tau, st)
-        driver.check_step(st, None)
+    from paper_1803_02143_b200 import _lib
 
-    # --- timed region: K public-API steps, events per step and per kernel group
+    lib = _lib.load()
+    mode = "graph" if args.graph else ("per-step" if args.per_step else "merged")
+    dev = torch.device("cuda", local)
+    nslot = st.flags.numel()
+
+    def flags_for(k):
+        return (torch.zeros((k, nslot), dtype=torch.int32, device=dev),
+                torch.zeros((k, st.stats.numel()), dtype=torch.float64, device=dev))
+
+    def run_steps(k, timer=None, how=None):
+        """k steps through the public step API of the selected mode."""
+        how = how or mode
+        if how == "merged":  # == driver.advance(field, tau, k, consume=True)
+            fl, sts = flags_for(k)
+            driver.enqueue_steps(field, tau, k, st, fl, sts, timer)
+            driver.check_steps(st, fl, sts, None, tau)
+        else:  # == k x strang_step(field, tau, consume=True)
+            for _ in range(k):
+                driver.enqueue_step(field, tau, st, timer=timer)
+                driver.check_step(st, None)
+
+    run_steps(args.warmup, how="merged" if mode == "merged" else "per-step")
+
+    # --- timed region: K steps, events per kernel group
     labels: list = []
     ev: list = []
 
@@ -380,19 +407,14 @@ def run_vpb(args, cfg_name: str, cfg: dict) -> None:
         ev.append(e)
         labels.append(label)
 
-    from paper_1803_02143_b200 import _lib
-
-    lib = _lib.load()
     graph = None
     n_launch0 = lib.vpb_launch_count()
-    if args.graph:
-        # --graph: the per-kernel breakdown comes from an eager pass of K steps;
-        # the headline timing replays the whole step from CUDA graphs.
+    if mode == "graph":
+        # the per-kernel breakdown comes from an eager pass of K steps; the
+        # headline timing replays the whole step from CUDA graphs
         e0 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for _ in range(args.steps):
-            driver.enqueue_step(field, tau, st, timer=mark)
-            driver.check_step(st, None)
+        run_steps(args.steps, timer=mark, how="per-step")
         e1 = torch.cuda.Event(enable_timing=True)
         e1.record(stream)
         torch.cuda.synchronize()
@@ -407,12 +429,11 @@ def run_vpb(args, cfg_name: str, cfg: dict) -> None:
     end = torch.cuda.Event(enable_timing=True)
     clocks.begin()
     start.record(stream)
-    for _ in range(args.steps):
-        if graph is not None:
+    if graph is not None:
+        for _ in range(args.steps):
             graph.step()
-        else:
-            driver.enqueue_step(field, tau, st, timer=mark)
-            driver.check_step(st, None)
+    else:
+        run_steps(args.steps, timer=mark)
     end.record(stream)
     torch.cuda.synchronize()
     clocks.end()
@@ -426,6 +447,21 @@ def run_vpb(args, cfg_name: str, cfg: dict) -> None:
     ms_per_step = total_ms / args.steps
     value = world * N * args.steps / (total_ms * 1e-3)
     breakdown_ms = eager_ms if graph is not None else total_ms
+
+    # the per-call API (one strang_step per step) for comparison
+    per_call = None
+    if mode != "per-step":
+        barrier(d, local)
+        torch.cuda.synchronize()
+        p0 = torch.cuda.Event(enable_timing=True)
+        p1 = torch.cuda.Event(enable_timing=True)
+        p0.record(stream)
+        run_steps(args.steps, how="per-step")
+        p1.record(stream)
+        torch.cuda.synchronize()
+        pc_ms = allreduce_max(d, p0.elapsed_time(p1))
+        per_call = {"api": "strang_step(consume=True) per step", "ms_per_step": pc_ms / args.steps,
+                    "value": world * N * args.steps / (pc_ms * 1e-3), "unit": UNIT}
 
     # per-group device time
     groups: dict = {}
@@ -510,6 +546,11 @@ def run_vpb(args, cfg_name: str, cfg: dict) -> None:
             "clocks": clocks.summary(),
             "gpu_launches": int(gpu_launches),
             "cuda_graph": bool(args.graph),
+            "step_api": {"merged": "advance(field, tau, K): K Strang steps, adjacent x half "
+                                   "steps share one HBM pass (bitwise the same sweeps)",
+                         "per-step": "strang_step(consume=True) per step",
+                         "graph": "strang_step per step replayed from CUDA graphs"}[mode],
+            "per_call": per_call,
         }
         print(json.dumps(line), flush=True)
     if d is not None:
@@ -527,7 +568,9 @@ def main() -> None:
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--graph", action="store_true",
-                    help="time the step replayed from CUDA graphs (driver.StepGraph)")
+                    help="time per-step calls replayed from CUDA graphs (driver.StepGraph)")
+    ap.add_argument("--per-step", action="store_true",
+                    help="time one strang_step call per step instead of advance()")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent replicas instead of the sharded field")
     ap.add_argument("--traffic", type=float, default=None,

@@ -141,6 +141,31 @@ int vpb_dg_sweep_xplane_density(const double* src, double* dst, const int64_t di
                                 double volume, double* work, double* rc_out, double* stats,
                                 void* stream);
 
+/* Two consecutive x half steps in one HBM pass: the closing x1(τ/2) x2(τ/2)
+ * of a Strang step followed by the opening x1(τ/2) x2(τ/2) of the next one
+ * (driver.py:245-265 applied twice; run loop driver.py:371-377), with the
+ * same tables for both.  Bitwise equal to four separate sweeps.  flag1a /
+ * flag2a: x1 / x2 of the first half step, flag1b / flag2b: of the second. */
+int vpb_dg_sweep_xplane2(const double* src, double* dst, const int64_t dims[4], int32_t order,
+                         const double* a1, const double* b1, const int64_t* q1,
+                         const double* alpha1, const double* a2, const double* b2,
+                         const int64_t* q2, const double* alpha2, int32_t* flag1a,
+                         int32_t* flag2a, int32_t* flag1b, int32_t* flag2b, void* stream);
+
+/* vpb_dg_sweep_xplane2 with the density epilogue of
+ * vpb_dg_sweep_xplane_density on its output (the density the next step's
+ * field solve needs). */
+int64_t vpb_dg_xplane2_density_work_len(const int64_t dims[4], int32_t order);
+int vpb_dg_sweep_xplane2_density(const double* src, double* dst, const int64_t dims[4],
+                                 int32_t order, const double* a1, const double* b1,
+                                 const int64_t* q1, const double* alpha1, const double* a2,
+                                 const double* b2, const int64_t* q2, const double* alpha2,
+                                 int32_t* flag1a, int32_t* flag2a, int32_t* flag1b,
+                                 int32_t* flag2b, const double* wv1, const double* wv2,
+                                 const double* mid_host, const double* wcell1_host,
+                                 const double* wcell2_host, double volume, double* work,
+                                 double* rc_out, double* stats, void* stream);
+
 /* One spline sweep along `axis`; shift of line = values[table row]*scale. */
 int vpb_spline_sweep_axis(int32_t axis, const double* src, double* dst, const int64_t dims[4],
                           const double* values, double scale, double h, int32_t* flag,

@@ -18,7 +18,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libvpb200.so"
-SOURCES = ["common.cu", "dg.cu", "fused.cu", "spline.cu", "field.cu", "halo.cu"]
+SOURCES = ["common.cu", "dg.cu", "fused.cu", "fused2.cu", "spline.cu", "field.cu", "halo.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -78,6 +78,11 @@ SIGNATURES = {
                                             c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                             c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                             c_double, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "vpb_dg_sweep_xplane2": (c_int, [c_void_p, c_void_p, POINTER(c_int64), c_int32]
+                             + [c_void_p] * 13),
+    "vpb_dg_xplane2_density_work_len": (c_int64, [POINTER(c_int64), c_int32]),
+    "vpb_dg_sweep_xplane2_density": (c_int, [c_void_p, c_void_p, POINTER(c_int64), c_int32]
+                                     + [c_void_p] * 17 + [c_double] + [c_void_p] * 4),
     "vpb_spline_sweep_axis": (c_int, [c_int32, c_void_p, c_void_p, POINTER(c_int64), c_void_p,
                                       c_double, c_double, c_void_p, c_void_p]),
     "vpb_density_work_len": (c_int64, [POINTER(c_int64)]),

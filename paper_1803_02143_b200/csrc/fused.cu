@@ -31,140 +31,11 @@
 #include "async_copy.cuh"
 #include "common.cuh"
 #include "tensormap.cuh"
+#include "xplane.cuh"
 
 namespace vpb {
 
 constexpr int kXStages = 6;
-
-struct XChunk {
-  int first;    // first output cell
-  int nout;     // output cells
-  int nsrc;     // source cells loaded (1 for the prologue chunk, else nout)
-  int s_begin;  // first source cell (mod C2)
-};
-
-// Walks the chunks of a run of planes with 32-bit bookkeeping only.
-struct XCursor {
-  int64_t plane;
-  int i;   // chunk index inside the plane
-  int s0;  // (-q2-1) mod C2 of the current plane
-  __device__ __forceinline__ void start(int64_t pl, int C2, const int64_t* __restrict__ q2,
-                                        int64_t nv1) {
-    plane = pl;
-    i = 0;
-    s0 = C2 - 1 - (int)wrap_mod(q2[pl / nv1], C2);
-  }
-  __device__ __forceinline__ XChunk chunk(int G, int C2) const {
-    XChunk c;
-    if (i == 0) {
-      c.first = 0;
-      c.nout = 0;
-      c.nsrc = 1;
-      c.s_begin = s0;
-      return c;
-    }
-    c.first = (i - 1) * G;
-    c.nout = min(G, C2 - c.first);
-    c.nsrc = c.nout;
-    int sb = s0 + 1 + c.first;
-    if (sb >= C2) sb -= C2;
-    c.s_begin = sb;
-    return c;
-  }
-  __device__ __forceinline__ void advance(int per_plane, int C2, const int64_t* __restrict__ q2,
-                                          int64_t nv1) {
-    if (++i == per_plane) start(plane + 1, C2, q2, nv1);
-  }
-};
-
-template <int P>
-__device__ __forceinline__ void lds_row_cell(const double* p, double (&u)[P]) {
-  if constexpr (P % 2 == 0) {
-#pragma unroll
-    for (int m = 0; m < P; m += 2) {
-      const double2 v = *reinterpret_cast<const double2*>(p + m);
-      u[m] = v.x;
-      u[m + 1] = v.y;
-    }
-  } else {
-#pragma unroll
-    for (int m = 0; m < P; ++m) u[m] = p[m];
-  }
-}
-
-// x1 sweep of one source x2 cell (P rows) for this thread's x1 cell
-// (_kernels.pyx:113-123): g[m2][j] = sum_m A1[j][m] u_lo[m] + sum_m B1[j][m] u_up[m].
-template <int P, bool EX1>
-__device__ __forceinline__ void xplane_x1_cell(const double* rows, int n1, int lo_off,
-                                               int up_off, const double (&A1)[P][P],
-                                               const double (&B1)[P][P], double (&g)[P][P]) {
-#pragma unroll
-  for (int m2 = 0; m2 < P; ++m2) {
-    const double* row = rows + m2 * n1;
-    double uu[P];
-    lds_row_cell<P>(row + up_off, uu);
-    if constexpr (EX1) {
-#pragma unroll
-      for (int jj = 0; jj < P; ++jj) g[m2][jj] = uu[jj];
-    } else {
-      double ul[P];
-      lds_row_cell<P>(row + lo_off, ul);
-#pragma unroll
-      for (int jj = 0; jj < P; ++jj) {
-        double acc_a = dmul(A1[jj][0], ul[0]);
-#pragma unroll
-        for (int m = 1; m < P; ++m) acc_a = dadd(acc_a, dmul(A1[jj][m], ul[m]));
-        double acc_b = dmul(B1[jj][0], uu[0]);
-#pragma unroll
-        for (int m = 1; m < P; ++m) acc_b = dadd(acc_b, dmul(B1[jj][m], uu[m]));
-        g[m2][jj] = dadd(acc_a, acc_b);
-      }
-    }
-  }
-}
-
-// x2 sweep of one output cell from the x1-swept source cells gp (= s-1) and
-// g (= s): o[j2][jj] = sum_m A2[j2][m] gp[m][jj] + sum_m B2[j2][m] g[m][jj].
-template <int P, bool EX2>
-__device__ __forceinline__ void xplane_x2_cell(const double (&A2)[P][P], const double (&B2)[P][P],
-                                               const double (&gp)[P][P], const double (&g)[P][P],
-                                               double (&o)[P][P]) {
-#pragma unroll
-  for (int j2 = 0; j2 < P; ++j2)
-#pragma unroll
-    for (int jj = 0; jj < P; ++jj) {
-      if constexpr (EX2) {
-        o[j2][jj] = g[j2][jj];
-      } else {
-        double acc_a = dmul(A2[j2][0], gp[0][jj]);
-#pragma unroll
-        for (int m = 1; m < P; ++m) acc_a = dadd(acc_a, dmul(A2[j2][m], gp[m][jj]));
-        double acc_b = dmul(B2[j2][0], g[0][jj]);
-#pragma unroll
-        for (int m = 1; m < P; ++m) acc_b = dadd(acc_b, dmul(B2[j2][m], g[m][jj]));
-        o[j2][jj] = dadd(acc_a, acc_b);
-      }
-    }
-}
-
-// Optional density epilogue of the x-plane pass (poisson.py:85-95 followed by
-// the cell-centre collapse of poisson.py:129-139): every output P x P cell
-// block is collapsed with the Lagrange weights at the cell centre (for odd P
-// the centre is the middle Gauss node and the collapse is a selection),
-// weighted by the plane's velocity weight, and added into the CTA's own
-// partial slab [C2][C1] with a fire-and-forget reduction (RED; only thread c
-// touches column c of its CTA's slab, so the order is program order and the
-// result deterministic).  The neutrality mean (poisson.py:143-160) rides
-// along as a per-thread scalar.  The cell weight tables live in the kernel
-// parameters (constant bank operands, no registers).
-struct XDensity {
-  const double* wv1;   // [nv1] velocity weights
-  const double* wv2;   // [nv2]
-  double* rc_part;     // [grid][C2][C1] or nullptr (epilogue off)
-  double* mean_part;   // [grid]
-  double mm[kMaxOrder * kMaxOrder];  // mid[j2] * mid[jj]
-  double ww[kMaxOrder * kMaxOrder];  // cell space weights wcell2[j2] * wcell1[jj]
-};
 
 template <int P, bool DENS>
 __global__ void __launch_bounds__(128)
@@ -209,7 +80,7 @@ __global__ void __launch_bounds__(128)
                bars + prod_st);
     ++prod_j;
     if (++prod_st == kXStages) prod_st = 0;
-    prod.advance(per_plane, C2, q2, nv1);
+    prod.advance(per_plane, C2, q2, nv1, pl_end);
   };
 
   if (tid == 0) {
@@ -353,7 +224,7 @@ __global__ void __launch_bounds__(128)
       }
       if (prod_j < nchunks) issue_next();
     }
-    cur.advance(per_plane, C2, q2, nv1);
+    cur.advance(per_plane, C2, q2, nv1, pl_end);
     if (++st == kXStages) {
       st = 0;
       phase ^= 1u;
@@ -395,7 +266,7 @@ __global__ void xdens_reduce_kernel(const double* __restrict__ part,
   }
 }
 
-static int xplane_sm_count() {
+int xplane_sm_count() {
   static int cached = 0;
   if (cached == 0) {
     int dev = 0, v = 0;
@@ -484,25 +355,7 @@ static int xplane_density_len(const int64_t dims[4], int64_t* len) {
   return VPB_OK;
 }
 
-}  // namespace vpb
-
-using namespace vpb;
-
-#define VPB_XPLANE_SWITCH(order, ...)                                              \
-  switch (order) {                                                                 \
-    case 1: { constexpr int PP = 1; __VA_ARGS__; } break;                                 \
-    case 2: { constexpr int PP = 2; __VA_ARGS__; } break;                                 \
-    case 3: { constexpr int PP = 3; __VA_ARGS__; } break;                                 \
-    case 4: { constexpr int PP = 4; __VA_ARGS__; } break;                                 \
-    case 5: { constexpr int PP = 5; __VA_ARGS__; } break;                                 \
-    case 6: { constexpr int PP = 6; __VA_ARGS__; } break;                                 \
-    case 7: { constexpr int PP = 7; __VA_ARGS__; } break;                                 \
-    case 8: { constexpr int PP = 8; __VA_ARGS__; } break;                                 \
-    default: { constexpr int PP = 9; __VA_ARGS__; } break;                                \
-  }
-
-static int xplane_args_ok(const double* src, const double* dst, const int64_t dims[4],
-                          int32_t order) {
+int xplane_args_ok(const double* src, const double* dst, const int64_t dims[4], int32_t order) {
   VPB_REQUIRE(src != dst, "src and dst must be distinct buffers");
   VPB_REQUIRE(order >= 1 && order <= kMaxOrder, "order %d outside 1..9", order);
   VPB_REQUIRE(dims[0] % order == 0 && dims[1] % order == 0, "x axes not whole cells");
@@ -513,6 +366,35 @@ static int xplane_args_ok(const double* src, const double* dst, const int64_t di
               "field buffers must be 16-byte aligned");
   return VPB_OK;
 }
+
+int xdensity_setup(XDensity* dn, int order, const double* wv1, const double* wv2,
+                   const double* mid_host, const double* wcell1_host, const double* wcell2_host,
+                   double* work, int64_t nblk, int64_t cc) {
+  VPB_REQUIRE(wv1 && wv2 && mid_host && wcell1_host && wcell2_host && work, "null pointer");
+  if (order % 2 == 1)
+    for (int j = 0; j < order; ++j)
+      VPB_REQUIRE(mid_host[j] == (j == order / 2 ? 1.0 : 0.0),
+                  "odd-order centre weights must select the middle node");
+  *dn = XDensity{wv1, wv2, work, work + nblk * cc, {}, {}};
+  for (int j2 = 0; j2 < order; ++j2)
+    for (int jj = 0; jj < order; ++jj) {
+      dn->mm[j2 * order + jj] = mid_host[j2] * mid_host[jj];
+      dn->ww[j2 * order + jj] = wcell2_host[j2] * wcell1_host[jj];
+    }
+  return VPB_OK;
+}
+
+int launch_xdens_reduce(const double* work, int64_t nblk, int64_t cc, double volume,
+                        double* rc_out, double* stats, cudaStream_t st) {
+  xdens_reduce_kernel<<<(unsigned)((cc + 255) / 256), 256, 0, st>>>(work, work + nblk * cc, nblk,
+                                                                    cc, volume, rc_out, stats);
+  return launched("xdens_reduce_kernel");
+}
+
+}  // namespace vpb
+
+using namespace vpb;
+
 
 extern "C" int vpb_dg_sweep_xplane(const double* src, double* dst, const int64_t dims[4],
                                    int32_t order, const double* a1, const double* b1,
@@ -547,20 +429,13 @@ extern "C" int vpb_dg_sweep_xplane_density(
   if (rc) return rc;
   VPB_REQUIRE(wv1 && wv2 && mid_host && wcell1_host && wcell2_host && work && rc_out,
               "null pointer");
-  if (order % 2 == 1)
-    for (int j = 0; j < order; ++j)
-      VPB_REQUIRE(mid_host[j] == (j == order / 2 ? 1.0 : 0.0),
-                  "odd-order centre weights must select the middle node");
   const int64_t cc = (dims[0] / order) * (dims[1] / order);
   int64_t len = vpb_dg_xplane_density_work_len(dims, order);
   VPB_REQUIRE(len > 0, "cannot plan the x-plane launch");
   const int64_t nblk = len / (cc + 1);
-  XDensity dn{wv1, wv2, work, work + nblk * cc, {}, {}};
-  for (int j2 = 0; j2 < order; ++j2)
-    for (int jj = 0; jj < order; ++jj) {
-      dn.mm[j2 * order + jj] = mid_host[j2] * mid_host[jj];
-      dn.ww[j2 * order + jj] = wcell2_host[j2] * wcell1_host[jj];
-    }
+  XDensity dn;
+  rc = xdensity_setup(&dn, order, wv1, wv2, mid_host, wcell1_host, wcell2_host, work, nblk, cc);
+  if (rc) return rc;
   int64_t used = 0;
   cudaStream_t st = (cudaStream_t)stream;
   VPB_XPLANE_SWITCH(order, rc = launch_xplane<PP, true>(src, dst, dims, a1, b1, q1, alpha1, a2,
@@ -568,9 +443,7 @@ extern "C" int vpb_dg_sweep_xplane_density(
   if (rc) return rc;
   VPB_REQUIRE(used == nblk, "x-plane launch plan changed (%lld vs %lld CTAs)", (long long)used,
               (long long)nblk);
-  xdens_reduce_kernel<<<(unsigned)((cc + 255) / 256), 256, 0, st>>>(work, work + nblk * cc, nblk,
-                                                                    cc, volume, rc_out, stats);
-  return launched("xdens_reduce_kernel");
+  return launch_xdens_reduce(work, nblk, cc, volume, rc_out, stats, st);
 }
 
 namespace vpb {

@@ -196,6 +196,24 @@ def xplane_dg(grid, src: torch.Tensor, dst: torch.Tensor, t1: DeviceTables, t2: 
     )
 
 
+def xplane2_dg(grid, src: torch.Tensor, dst: torch.Tensor, t1: DeviceTables, t2: DeviceTables,
+               flags_a, flags_b) -> None:
+    """Two consecutive x half steps (x1 x2 x1 x2, same tables) in one pass
+    (``vpb_dg_sweep_xplane2``); ``flags_a`` / ``flags_b``: the (x1, x2) flag
+    words of the first / second half step (or None)."""
+    lib = _lib.load()
+    fa = [None, None] if flags_a is None else [f.data_ptr() for f in flags_a]
+    fb = [None, None] if flags_b is None else [f.data_ptr() for f in flags_b]
+    _lib.check(
+        lib.vpb_dg_sweep_xplane2(src.data_ptr(), dst.data_ptr(), _lib.dims(grid.dims4), t1.order,
+                                 t1.a.data_ptr(), t1.b.data_ptr(), t1.q.data_ptr(),
+                                 t1.alpha.data_ptr(), t2.a.data_ptr(), t2.b.data_ptr(),
+                                 t2.q.data_ptr(), t2.alpha.data_ptr(), fa[0], fa[1], fb[0], fb[1],
+                                 _device.stream()),
+        "vpb_dg_sweep_xplane2",
+    )
+
+
 def vplane_dg(grid, src: torch.Tensor, dst: torch.Tensor, t1: DeviceTables, t2: DeviceTables,
               flag1: torch.Tensor | None, flag2: torch.Tensor | None) -> None:
     """v1 then v2 sweep of a 2x2v field in one pass (``vpb_dg_sweep_vplane``)."""

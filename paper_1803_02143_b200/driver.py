@@ -26,7 +26,7 @@ import numpy as np
 import torch
 
 from . import _device, _lib
-from .dg import DeviceTables, sweep_dg, vplane_dg, xplane_dg
+from .dg import DeviceTables, sweep_dg, vplane_dg, xplane2_dg, xplane_dg
 from .field import DEFAULT_STRATEGY, DistributionField, LayoutDescriptor, write_snapshot
 from .grid import DG, SPACE, SPLINE, VELOCITY, Axis, GridSpec, gauss_nodes
 from .poisson import (
@@ -271,6 +271,7 @@ class StepState:
                 self.fused_rho = False
             else:
                 self.rho_work = torch.empty(n, dtype=torch.float64, device=dev)
+                self.rho_work2 = None  # double x pass work, allocated on first use
                 self.rc = torch.empty(grid.axes[0].count * grid.axes[1].count,
                                       dtype=torch.float64, device=dev)
                 # host constants of the epilogue: centre Lagrange weights and
@@ -346,76 +347,114 @@ def enqueue_step(field: DistributionField, tau: float, state: StepState | None =
     and once with ``None`` at the end; bench.py uses it to bracket kernels
     with CUDA events.
     """
-    grid = field.grid
-    st = state or step_state(grid)
-    mark = timer or (lambda label: None)
-    st.flags.zero_()
-    half = 0.5 * tau
-    k = 0
+    st = state or step_state(field.grid)
+    enqueue_steps(field, tau, 1, st, st.flags.view(1, -1), st.stats.view(1, -1), timer)
 
-    def sweep(axis: int, tab, scale: float, label: str) -> None:
-        nonlocal k
+
+def enqueue_steps(field: DistributionField, tau: float, nsteps: int, st: StepState,
+                  flags: torch.Tensor, stats: torch.Tensor, timer=None,
+                  merge: bool = True) -> None:
+    """Queue ``nsteps`` Strang steps (driver.py:245-265 each).
+
+    ``flags[m]`` / ``stats[m]`` receive step m's flag words (slots as
+    ``st.names``) and density mean.  With ``merge`` (and the fused x pass),
+    the closing x half step of step m and the opening one of step m+1 run as
+    one HBM pass (``vpb_dg_sweep_xplane2``: four sweeps chained in registers
+    and shared memory, bitwise equal to running them separately); the state
+    between the two steps is then never written to HBM.
+    """
+    grid = field.grid
+    mark = timer or (lambda label: None)
+    flags.zero_()
+    half = 0.5 * tau
+    nx = grid.ndim_x
+    field_k, v_k, close_k = nx, nx + 1, 2 * nx + 1
+    xn = ["x"] if nx == 1 else ["x1", "x2"]
+    vn = ["v"] if nx == 1 else ["v1", "v2"]
+
+    def swap(out) -> None:
+        st.buf = field._swap(out.view(field._phys.shape)).view(-1)
+
+    def sweep(axis: int, tab, scale: float, label: str, flag) -> None:
         out = st.buf
         mark(label)
-        _sweep_into(st, axis, field._phys.view(-1), out, tab, scale, st.flags[k:k + 1])
-        st.buf = field._swap(out.view(field._phys.shape)).view(-1)
-        k += 1
+        _sweep_into(st, axis, field._phys.view(-1), out, tab, scale, flag)
+        swap(out)
 
-    def advect_space(with_density: bool) -> None:  # _advect_space(tau/2)  driver.py:220-228
-        nonlocal k
+    def x_half(fl, k: int, with_density: bool, stats_row) -> None:
+        """_advect_space(tau/2) (driver.py:220-228) into flag slots k, k+1."""
         if st.fused_x:
             out = st.buf
+            t1, t2 = st.x_tables(0, tau), st.x_tables(1, tau)
             if with_density:
                 # x1+x2 sweeps with the cell-centre density of the result as an
                 # epilogue (compute_density + centre collapse, poisson.py:85-139)
                 mark("sweep_x12_rho")
-                xplane_density_dg(grid, field._phys.view(-1), out, st.x_tables(0, tau),
-                                  st.x_tables(1, tau), st.flags[k:k + 1], st.flags[k + 1:k + 2],
-                                  st)
+                xplane_density_dg(grid, field._phys.view(-1), out, t1, t2, fl[k:k + 1],
+                                  fl[k + 1:k + 2], st, stats_row)
             else:
                 mark("sweep_x12")
-                xplane_dg(grid, field._phys.view(-1), out, st.x_tables(0, tau),
-                          st.x_tables(1, tau), st.flags[k:k + 1], st.flags[k + 1:k + 2])
-            st.buf = field._swap(out.view(field._phys.shape)).view(-1)
-            k += 2
+                xplane_dg(grid, field._phys.view(-1), out, t1, t2, fl[k:k + 1], fl[k + 1:k + 2])
+            swap(out)
             return
-        for d in range(grid.ndim_x):
-            sweep(d, st.x_tables(d, tau), half, f"sweep_{xn[d]}")
+        for d in range(nx):
+            sweep(d, st.x_tables(d, tau), half, f"sweep_{xn[d]}", fl[k + d:k + d + 1])
 
-    xn = ["x"] if grid.ndim_x == 1 else ["x1", "x2"]
-    vn = ["v"] if grid.ndim_x == 1 else ["v1", "v2"]
-    advect_space(st.fused_rho)  # "open"
-    if st.fused_rho:
-        mark("field_solve")
-        solve_into(st.rc, grid, st.e, None, st.flags[k:k + 1], centred=True)
-    else:
-        mark("density")
-        density_into(field.data, grid, st.rho)  # compute_density  poisson.py:85-95
-        mark("field_solve")
-        solve_into(st.rho, grid, st.e, st.stats, st.flags[k:k + 1])  # solve_poisson
-    k += 1
-    if st.fused_v:  # _advect_velocity(tau) in one pass  driver.py:231-242
-        mark("tables_v12")
-        t1 = st.v_tables(0, tau)
-        t2 = st.v_tables(1, tau)
+    def x_double(fl_a, fl_b, with_density: bool, stats_row) -> None:
+        """Closing x half step of one step + opening one of the next, one pass."""
         out = st.buf
-        mark("sweep_v12")
-        vplane_dg(grid, field._phys.view(-1), out, t1, t2, st.flags[k:k + 1],
-                  st.flags[k + 1:k + 2])
-        st.buf = field._swap(out.view(field._phys.shape)).view(-1)
-        k += 2
-    else:
-        for d in range(grid.ndim_x):  # _advect_velocity(tau)  driver.py:231-242
-            mark(f"tables_{vn[d]}")
-            tab = st.v_tables(d, tau)
-            sweep(grid.ndim_x + d, tab, tau, f"sweep_{vn[d]}")
-    advect_space(False)  # "close"
+        t1, t2 = st.x_tables(0, tau), st.x_tables(1, tau)
+        fa = (fl_a[close_k:close_k + 1], fl_a[close_k + 1:close_k + 2])
+        fb = (fl_b[0:1], fl_b[1:2])
+        if with_density:
+            mark("sweep_x12x12_rho")
+            xplane2_density_dg(grid, field._phys.view(-1), out, t1, t2, fa, fb, st, stats_row)
+        else:
+            mark("sweep_x12x12")
+            xplane2_dg(grid, field._phys.view(-1), out, t1, t2, fa, fb)
+        swap(out)
+
+    def field_and_velocity(m: int) -> None:
+        fl = flags[m]
+        if st.fused_rho:
+            mark("field_solve")
+            solve_into(st.rc, grid, st.e, None, fl[field_k:field_k + 1], centred=True)
+        else:
+            mark("density")
+            density_into(field.data, grid, st.rho)  # compute_density  poisson.py:85-95
+            mark("field_solve")
+            solve_into(st.rho, grid, st.e, stats[m], fl[field_k:field_k + 1])  # solve_poisson
+        if st.fused_v:  # _advect_velocity(tau) in one pass  driver.py:231-242
+            mark("tables_v12")
+            t1 = st.v_tables(0, tau)
+            t2 = st.v_tables(1, tau)
+            out = st.buf
+            mark("sweep_v12")
+            vplane_dg(grid, field._phys.view(-1), out, t1, t2, fl[v_k:v_k + 1],
+                      fl[v_k + 1:v_k + 2])
+            swap(out)
+        else:
+            for d in range(nx):  # _advect_velocity(tau)  driver.py:231-242
+                mark(f"tables_{vn[d]}")
+                tab = st.v_tables(d, tau)
+                sweep(nx + d, tab, tau, f"sweep_{vn[d]}", fl[v_k + d:v_k + d + 1])
+
+    x_half(flags[0], 0, st.fused_rho, stats[0])  # "open" of step 0
+    for m in range(nsteps):
+        field_and_velocity(m)
+        if m + 1 == nsteps:
+            x_half(flags[m], close_k, False, None)  # "close" of the last step
+        elif merge and st.fused_x:
+            x_double(flags[m], flags[m + 1], st.fused_rho, stats[m + 1])
+        else:
+            x_half(flags[m], close_k, False, None)
+            x_half(flags[m + 1], 0, st.fused_rho, stats[m + 1])
     mark(None)
 
 
-def xplane_density_dg(grid, src, dst, t1, t2, flag1, flag2, st: StepState) -> None:
+def xplane_density_dg(grid, src, dst, t1, t2, flag1, flag2, st: StepState, stats) -> None:
     """Fused x pass whose epilogue writes the cell-centre density of its
-    output to ``st.rc`` and the neutrality mean to ``st.stats[0]``."""
+    output to ``st.rc`` and the neutrality mean to ``stats[0]``."""
     lib = _lib.load()
     g = st.geom
     _lib.check(
@@ -426,8 +465,30 @@ def xplane_density_dg(grid, src, dst, t1, t2, flag1, flag2, st: StepState) -> No
             flag2.data_ptr(), st.wv1.data_ptr(), st.wv2.data_ptr(),
             st.dens_mid.ctypes.data, st.dens_w1.ctypes.data, st.dens_w2.ctypes.data,
             g.volume, st.rho_work.data_ptr(), st.rc.data_ptr(),
-            st.stats.data_ptr(), _device.stream()),
+            stats.data_ptr(), _device.stream()),
         "vpb_dg_sweep_xplane_density",
+    )
+
+
+def xplane2_density_dg(grid, src, dst, t1, t2, fa, fb, st: StepState, stats) -> None:
+    """Two x half steps in one pass with the density epilogue on the result."""
+    lib = _lib.load()
+    g = st.geom
+    if st.rho_work2 is None:
+        n = int(lib.vpb_dg_xplane2_density_work_len(_lib.dims(grid.dims4), grid.order))
+        if n <= 0:
+            raise _lib.VpbError("cannot plan the double x pass")
+        st.rho_work2 = torch.empty(n, dtype=torch.float64, device=_device.device())
+    _lib.check(
+        lib.vpb_dg_sweep_xplane2_density(
+            src.data_ptr(), dst.data_ptr(), _lib.dims(grid.dims4), t1.order, t1.a.data_ptr(),
+            t1.b.data_ptr(), t1.q.data_ptr(), t1.alpha.data_ptr(), t2.a.data_ptr(),
+            t2.b.data_ptr(), t2.q.data_ptr(), t2.alpha.data_ptr(), fa[0].data_ptr(),
+            fa[1].data_ptr(), fb[0].data_ptr(), fb[1].data_ptr(), st.wv1.data_ptr(),
+            st.wv2.data_ptr(), st.dens_mid.ctypes.data, st.dens_w1.ctypes.data,
+            st.dens_w2.ctypes.data, g.volume, st.rho_work2.data_ptr(), st.rc.data_ptr(),
+            stats.data_ptr(), _device.stream()),
+        "vpb_dg_sweep_xplane2_density",
     )
 
 
@@ -498,6 +559,44 @@ def strang_step(field: DistributionField, tau: float, workers: int = 1, consume:
     enqueue_step(work, tau, st)
     check_step(st, time_label)
     return work
+
+
+def advance(field: DistributionField, tau: float, nsteps: int, consume: bool = False,
+            first_step: int | None = None) -> DistributionField:
+    """``nsteps`` Strang steps; the result is bitwise that of ``nsteps``
+    :func:`strang_step` calls, with the same errors and warnings.
+
+    Adjacent x half steps of consecutive steps share one HBM pass
+    (:func:`enqueue_steps`), so the states between the steps are never
+    written out; use :func:`strang_step` when every intermediate state is
+    needed.  Non-finite checks and neutrality warnings are evaluated after
+    the last step, in step order; with ``first_step`` the errors carry the
+    time label ``(first_step + m) * tau`` of step m (as run() labels them).
+    """
+    if nsteps < 0:
+        raise ValueError("nsteps must be non-negative")
+    work = field if consume else field.copy()
+    if nsteps == 0:
+        return work
+    st = step_state(work.grid)
+    dev = _device.device()
+    flags = torch.zeros((nsteps, st.flags.numel()), dtype=torch.int32, device=dev)
+    stats = torch.zeros((nsteps, st.stats.numel()), dtype=torch.float64, device=dev)
+    enqueue_steps(work, tau, nsteps, st, flags, stats)
+    check_steps(st, flags, stats, first_step, tau)
+    return work
+
+
+def check_steps(st: StepState, flags: torch.Tensor, stats: torch.Tensor,
+                first_step: int | None, tau: float) -> None:
+    """Flags / means of several steps (one D2H + sync), raised in step order."""
+    fh = flags.cpu().numpy()
+    sh = stats.cpu().numpy()
+    for m in range(fh.shape[0]):
+        _warn_if_not_neutral(float(sh[m, 0]))
+        for k, name in enumerate(st.names):
+            if fh[m, k]:
+                raise SubstepError(name, None if first_step is None else (first_step + m) * tau)
 
 
 @dataclass(frozen=True)
@@ -606,9 +705,15 @@ def run(config: RunConfig):
 
     if 0 in snap_at:
         capture(0.0)
-    for m in range(1, nsteps + 1):
+    # the states the loop must observe: diagnostics records and snapshots;
+    # the steps in between run through advance() (merged x half steps)
+    stops = sorted({m for m in range(1, nsteps + 1) if m % config.diag_every == 0}
+                   | {m for m in snap_at if m > 0} | ({nsteps} if nsteps else set()))
+    done = 0
+    for m in stops:
+        field = advance(field, config.tau, m - done, consume=True, first_step=done + 1)
+        done = m
         t = m * config.tau
-        field = strang_step(field, config.tau, workers=config.workers, consume=True, time_label=t)
         if m % config.diag_every == 0:
             records.append(diagnostics(field, time=t))
         if m in snap_at:
@@ -628,6 +733,7 @@ __all__ = [
     "initial_value",
     "initialize",
     "strang_step",
+    "advance",
     "DiagnosticsRecord",
     "diagnostics",
     "RunConfig",

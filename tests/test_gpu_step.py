@@ -381,3 +381,105 @@ def test_fused_x_reports_nonfinite_in_x1_and_x2():
     f.array[5, 6, 7, 8] = math.nan
     with pytest.raises(vpb.SubstepError, match=r"x1 half \(open\)"):
         vpb.strang_step(f, 0.1)
+
+
+# ---------------------------------------------------------------------------
+# merged x half steps of consecutive steps (vpb_dg_sweep_xplane2, advance)
+# ---------------------------------------------------------------------------
+ADVANCE_CASES = [
+    (3, (24, 18, 12, 15), 0.37),    # one output chunk per plane
+    (3, (192, 24, 6, 6), 0.37),     # G = 1: many chunks per plane
+    (3, (192, 24, 6, 6), 2.9),      # |q| of several cells, wrapped loads
+    (2, (128, 22, 4, 6), 0.37),     # G = 2 with a partial last chunk
+    (2, (128, 22, 4, 6), 5.0),
+    (4, (16, 20, 12, 8), 0.37),
+    (1, (12, 10, 8, 6), 0.37),
+]
+
+
+@pytest.mark.parametrize("order,dofs,tau", ADVANCE_CASES)
+def test_advance_bitwise_equal_to_strang_steps(monkeypatch, order, dofs, tau):
+    """K steps with merged x half steps == K separate strang_step calls, bit
+    for bit (separate density pass in both, so every reduction is the same)."""
+    prob = vpb.problem_spec("landau4d")
+    grid = vpb.make_grid(prob, "dg", dofs, dg_order=order)
+    monkeypatch.setattr(driver, "FUSE_RHO", False)
+    driver._state_cached.cache_clear()
+    f1 = vpb.initialize(prob, grid)
+    for _ in range(4):
+        f1 = vpb.strang_step(f1, tau, consume=True)
+    f2 = vpb.advance(vpb.initialize(prob, grid), tau, 4)
+    assert driver.step_state(grid).fused_x
+    driver._state_cached.cache_clear()
+    assert np.array_equal(f1.numpy(), f2.numpy())
+
+
+@pytest.mark.parametrize("order,dofs,tau", ADVANCE_CASES[:5])
+def test_advance_with_density_epilogues(monkeypatch, order, dofs, tau):
+    """With the density folded into the x passes only the density summation
+    order differs between the single and the merged pass."""
+    prob = vpb.problem_spec("landau4d")
+    grid = vpb.make_grid(prob, "dg", dofs, dg_order=order)
+    monkeypatch.setattr(driver, "FUSE_RHO", True)
+    driver._state_cached.cache_clear()
+    f1 = vpb.initialize(prob, grid)
+    for _ in range(4):
+        f1 = vpb.strang_step(f1, tau, consume=True)
+    f2 = vpb.advance(vpb.initialize(prob, grid), tau, 4)
+    assert driver.step_state(grid).fused_rho
+    driver._state_cached.cache_clear()
+    assert max_rel(f2.numpy(), f1.numpy()) <= 1e-13
+
+
+def test_advance_config1_parity_vs_oracle():
+    """BASELINE config 1, 10 merged steps vs the oracle: north-star bar."""
+    prob, method, dofs, order, tau = "landau4d", "dg", 48, 3, 0.1
+    ref = _oracle_run(prob, method, dofs, order, tau, 10)
+    problem = vpb.problem_spec(prob)
+    grid = vpb.make_grid(problem, method, dofs, dg_order=order)
+    f = vpb.advance(vpb.initialize(problem, grid), tau, 10)
+    assert max_rel(f.numpy(), ref[-1]) <= F_TOL
+
+
+def test_double_x_pass_flags_every_substep():
+    prob = vpb.problem_spec("landau4d")
+    grid = vpb.make_grid(prob, "dg", (192, 24, 6, 6), dg_order=3)
+    f = vpb.initialize(prob, grid)
+    st = driver.step_state(grid)
+    bad = f.data.clone()
+    bad[12345] = math.nan
+    out = torch.empty_like(bad)
+    flags = torch.zeros(4, dtype=torch.int32, device="cuda")
+    t1, t2 = st.x_tables(0, 0.37), st.x_tables(1, 0.37)
+    driver.xplane2_dg(grid, bad, out, t1, t2, (flags[0:1], flags[1:2]), (flags[2:3], flags[3:4]))
+    assert flags.tolist() == [1, 1, 1, 1]
+    flags.zero_()
+    driver.xplane2_dg(grid, f.data, out, t1, t2, (flags[0:1], flags[1:2]),
+                      (flags[2:3], flags[3:4]))
+    assert flags.tolist() == [0, 0, 0, 0]
+
+
+def test_advance_reports_first_nonfinite_substep_with_time_label():
+    prob = vpb.problem_spec("landau4d")
+    grid = vpb.make_grid(prob, "dg", 24, dg_order=3)
+    f = vpb.initialize(prob, grid)
+    f.array[5, 6, 7, 8] = math.nan
+    with pytest.raises(vpb.SubstepError, match=r"x1 half \(open\)") as err:
+        vpb.advance(f, 0.1, 3, first_step=4)
+    assert "0.4" in str(err.value)
+
+
+def test_run_with_sparse_diagnostics_matches_every_step_records():
+    prob = vpb.problem_spec("landau4d")
+    grid = vpb.make_grid(prob, "dg", 24, dg_order=3)
+    cfg1 = vpb.RunConfig(problem=prob, grid=grid, tau=0.1, t_end=0.6, diag_every=1)
+    cfg3 = vpb.RunConfig(problem=prob, grid=grid, tau=0.1, t_end=0.6, diag_every=3,
+                         snapshot_times=(0.5,))
+    rec1, _ = vpb.run(cfg1)
+    rec3, snaps = vpb.run(cfg3)
+    assert [r.time for r in rec3] == pytest.approx([0.0, 0.3, 0.6])
+    for r in rec3:
+        r1 = next(x for x in rec1 if abs(x.time - r.time) < 1e-12)
+        for k in KEYS[1:]:
+            assert getattr(r, k) == pytest.approx(getattr(r1, k), rel=1e-12, abs=1e-300), k
+    assert snaps[0][0] == pytest.approx(0.5)
