@@ -212,6 +212,79 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
           for (int jj = 0; jj < P; ++jj) gq[m2][jj] = g[m2][jj];
       };
+      // Steady state (all but the first three chunks and the drain of a
+      // plane): both stages on one cell each per step, in one basic block so
+      // the scheduler interleaves their independent dependency chains.
+      if (ipl >= 3 && !drain && nout_prev == c.nsrc && c.nout == c.nsrc) {
+        mbar_wait(bars + st, phase);
+        const double* in = inb + st * slot;
+        const double* hprev = hb + ((ipl - 1) & 1) * slot;
+        double* hcur = hb + (ipl & 1) * slot;
+        for (int sc = 0; sc < c.nsrc; ++sc) {
+          double g2[P][P], g1[P][P], o2[P][P], o1[P][P];
+          xplane_x1_cell<P, E1>(hprev + sc * cell, n1, lo_off, up_off, A1, B1, g2);
+          xplane_x1_cell<P, E1>(in + sc * cell, n1, lo_off, up_off, A1, B1, g1);
+          xplane_x2_cell<P, E2>(A2, B2, gq, g2, o2);
+          xplane_x2_cell<P, E2>(A2, B2, gp, g1, o1);
+          ExpMax e2, e1;
+          double* ot = out + (o_next - o_begin) * cell + tid * P;
+          double* ht = hcur + sc * cell + tid * P;
+#pragma unroll
+          for (int j2 = 0; j2 < P; ++j2)
+#pragma unroll
+            for (int jj = 0; jj < P; ++jj) {
+              e2.add(o2[j2][jj]);
+              e1.add(o1[j2][jj]);
+              ot[j2 * n1 + jj] = o2[j2][jj];
+              ht[j2 * n1 + jj] = o1[j2][jj];
+            }
+          if constexpr (DENS) {
+            double rcv, mv = 0.0;
+            if constexpr (P % 2 == 1) {
+              rcv = o2[P / 2][P / 2];
+            } else {
+              rcv = 0.0;
+#pragma unroll
+              for (int j2 = 0; j2 < P; ++j2)
+#pragma unroll
+                for (int jj = 0; jj < P; ++jj) rcv = fma(dn.mm[j2 * P + jj], o2[j2][jj], rcv);
+            }
+#pragma unroll
+            for (int j2 = 0; j2 < P; ++j2)
+#pragma unroll
+              for (int jj = 0; jj < P; ++jj) mv = fma(dn.ww[j2 * P + jj], o2[j2][jj], mv);
+            atomicAdd(mypart + o_next * C1 + tid, dmul(wplane, rcv));
+            meanacc = fma(wplane, mv, meanacc);
+          }
+          if (e2.bad()) {
+            bad2b = true;
+            ExpMax eg;
+#pragma unroll
+            for (int m2 = 0; m2 < P; ++m2)
+#pragma unroll
+              for (int jj = 0; jj < P; ++jj) eg.add(g2[m2][jj]);
+            bad1b |= eg.bad();
+          }
+          if (e1.bad()) {
+            bad2a = true;
+            ExpMax eg;
+#pragma unroll
+            for (int m2 = 0; m2 < P; ++m2)
+#pragma unroll
+              for (int jj = 0; jj < P; ++jj) eg.add(g1[m2][jj]);
+            bad1a |= eg.bad();
+          }
+          ++o_next;
+#pragma unroll
+          for (int m2 = 0; m2 < P; ++m2)
+#pragma unroll
+            for (int jj = 0; jj < P; ++jj) {
+              gq[m2][jj] = g2[m2][jj];
+              gp[m2][jj] = g1[m2][jj];
+            }
+        }
+        return;
+      }
       if (ipl >= 2) {
         if (ipl == 2) o_next = -1;  // the first cell of chunk 1 is h0 (stage-2 prologue)
         const double* hprev = hb + ((ipl - 1) & 1) * slot;
