@@ -279,9 +279,16 @@ def run_sharded(args, cfg_name: str, cfg: dict, d, world: int, rank: int, local:
     grid = vpb.make_grid(problem, cfg["method"], cfg["dofs"], dg_order=cfg["order"])
     N = grid.total_dof
     tau = cfg["tau"]
-    p1, p2 = dist.process_grid(world)
-    dec = dist.Decomposition(grid, p1, p2)
-    solver = dist.ShardedSolver(grid, dec, dist.TorchComm(), [rank])
+    if cfg["method"] == "dg":
+        p1, p2 = dist.process_grid(world)
+        dec = dist.Decomposition(grid, p1, p2)
+        solver = dist.ShardedSolver(grid, dec, dist.TorchComm(), [rank])
+        local_f = lambda: solver.shards[rank].f  # noqa: E731
+        layout = f"x-shard {p1}x{p2} (NCCL halos + rho allgather)"
+    else:
+        solver = dist.SplineShardedSolver(grid, dist.TorchComm(), [rank], world)
+        local_f = lambda: solver.a[rank][0]  # noqa: E731
+        layout = f"v2-shard x{world} <-> x2-shard (2 NCCL all-to-alls per step, rho allreduce)"
     solver.initialize(problem)
     stream = torch.cuda.current_stream()
     clocks = ClockSampler(local).start()
@@ -310,9 +317,8 @@ def run_sharded(args, cfg_name: str, cfg: dict, d, world: int, rank: int, local:
     # e2e: each rank's slab from pinned host memory, step, back to the host
     e2e = None
     if not args.no_e2e:
-        sh = solver.shards[rank]
-        host = torch.empty(sh.f.numel(), dtype=torch.float64, pin_memory=True)
-        host.copy_(sh.f)
+        host = torch.empty(local_f().numel(), dtype=torch.float64, pin_memory=True)
+        host.copy_(local_f())
         k_e2e = max(1, min(args.steps, args.e2e_steps))
         barrier(d, local)
         torch.cuda.synchronize()
@@ -320,13 +326,13 @@ def run_sharded(args, cfg_name: str, cfg: dict, d, world: int, rank: int, local:
         s1 = torch.cuda.Event(enable_timing=True)
         s0.record(stream)
         for _ in range(k_e2e):
-            solver.shards[rank].f.copy_(host, non_blocking=True)
+            local_f().copy_(host, non_blocking=True)
             solver.step(tau)
-            host.copy_(solver.shards[rank].f, non_blocking=True)
+            host.copy_(local_f(), non_blocking=True)
         s1.record(stream)
         torch.cuda.synchronize()
         e2e_ms = allreduce_max(d, s0.elapsed_time(s1))
-        nbytes = 8 * sh.f.numel()
+        nbytes = 8 * host.numel()
         e2e = {"value": N * k_e2e / (e2e_ms * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": nbytes * world, "d2h_bytes_per_step": nbytes * world,
                "steps": k_e2e, "ms_per_step": e2e_ms / k_e2e,
@@ -340,7 +346,7 @@ def run_sharded(args, cfg_name: str, cfg: dict, d, world: int, rank: int, local:
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (BASELINE initial condition on the named grid; no dataset)",
             "config": {"workload": cfg_name, "description": cfg["label"], "dofs": N,
-                       "parallelism": f"x-shard {p1}x{p2} (NCCL halos + rho allgather)",
+                       "parallelism": layout,
                        "l2": l2_note(8 * N // world)},
             "roofline": {"bound": "hbm", "achieved": step_gbs / world, "peak": peak,
                          "unit": "GB/s", "frac": step_gbs / world / peak, "traffic": None,
@@ -358,7 +364,7 @@ def run_vpb(args, cfg_name: str, cfg: dict) -> None:
     world, rank, local = dist_env()
     d = maybe_init(world, local, "nccl")
     torch.cuda.set_device(local)
-    if world > 1 and cfg["method"] == "dg" and not args.replicas:
+    if world > 1 and not args.replicas:
         return run_sharded(args, cfg_name, cfg, d, world, rank, local)
     import paper_1803_02143_b200 as vpb
     from paper_1803_02143_b200 import driver

@@ -230,6 +230,12 @@ int vpb_fill_separable(double* f, const int64_t dims[4], const double* g1, const
 int vpb_halo_pack(int32_t axis, const double* f, const int64_t dims[4], int32_t order,
                   int64_t cell0, int64_t width, double* buf, void* stream);
 
+/* Strided slab copy (the all-to-all reshard of the multi-GPU spline step):
+ * `outer` runs of `run` doubles; run k is read at src + k*src_stride and
+ * written at dst + k*dst_stride. */
+int vpb_slab_copy(const double* src, int64_t src_stride, double* dst, int64_t dst_stride,
+                  int64_t outer, int64_t run, void* stream);
+
 /* dG sweep of a shard along a sharded x axis (axis 0 or 1).  Source cells
  * outside the local range [0, cl) are read from the halo buffers (no
  * periodic wrap inside the shard): `left` holds the wl cells just below the

@@ -27,6 +27,25 @@ __global__ void halo_pack_kernel(const double* __restrict__ f, double* __restric
   buf[e] = f[(o * nax + off + k) * inner + i];
 }
 
+// Strided slab copy: run k of `run` doubles from src + k*ss to dst + k*ds.
+// blockIdx.x covers a run in 512-double pieces (double2 per thread when both
+// sides are 16-byte aligned), blockIdx.y strides over the runs.
+__global__ void slab_copy_kernel(const double* __restrict__ src, int64_t ss,
+                                 double* __restrict__ dst, int64_t ds, int64_t outer, int64_t run,
+                                 bool vec2) {
+  const int64_t i0 = (int64_t)blockIdx.x * 512 + threadIdx.x * 2;
+  for (int64_t k = blockIdx.y; k < outer; k += gridDim.y) {
+    const double* s = src + k * ss;
+    double* d = dst + k * ds;
+    if (vec2 && i0 + 1 < run) {
+      *reinterpret_cast<double2*>(d + i0) = __ldcs(reinterpret_cast<const double2*>(s + i0));
+    } else {
+      if (i0 < run) d[i0] = s[i0];
+      if (i0 + 1 < run) d[i0 + 1] = s[i0 + 1];
+    }
+  }
+}
+
 template <int P>
 struct HCoeffs {
   double A[P][P];
@@ -192,4 +211,18 @@ extern "C" int vpb_dg_sweep_axis_halo(int32_t axis, const double* src, double* d
       set_error("dG order %d outside the supported range 1..9", order);
       return VPB_ERR_UNSUPPORTED;
   }
+}
+
+extern "C" int vpb_slab_copy(const double* src, int64_t src_stride, double* dst,
+                             int64_t dst_stride, int64_t outer, int64_t run, void* stream) {
+  VPB_REQUIRE(outer >= 0 && run >= 0 && src_stride >= run && dst_stride >= run,
+              "bad slab geometry");
+  if (outer == 0 || run == 0) return VPB_OK;
+  VPB_REQUIRE(src != nullptr && dst != nullptr, "null pointer");
+  const bool vec2 = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0 &&
+                    src_stride % 2 == 0 && dst_stride % 2 == 0;
+  dim3 grid((unsigned)((run + 511) / 512), (unsigned)std::min<int64_t>(outer, 65535));
+  slab_copy_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(src, src_stride, dst, dst_stride,
+                                                           outer, run, vec2);
+  return launched("slab_copy_kernel");
 }

@@ -33,7 +33,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from .grid import DG, GridSpec
+from .grid import DG, SPLINE, GridSpec
 
 
 # ---------------------------------------------------------------------------
@@ -124,6 +124,7 @@ def halo_widths(q: np.ndarray) -> tuple[int, int]:
 # message kinds of a halo exchange: "L" becomes the receiver's LEFT halo (the
 # sender's last cells, sent to its right neighbour); "R" its RIGHT halo.
 KIND_L, KIND_R = 0, 1
+KIND_A2A = 2  # all-to-all reshard chunks (one per peer pair)
 
 
 class TorchComm:
@@ -230,6 +231,18 @@ class CudaOps:
                                              t2.q.data_ptr(), t2.alpha.data_ptr(), f1.data_ptr(),
                                              f2.data_ptr(), self._device.stream()),
                 "vpb_dg_sweep_xplane")
+
+    def spline_sweep(self, axis, src, dst, dims, values, scale, h, flag):
+        L = self._lib
+        L.check(self.lib.vpb_spline_sweep_axis(axis, src.data_ptr(), dst.data_ptr(), L.dims(dims),
+                                               values.data_ptr(), float(scale), float(h),
+                                               flag.data_ptr(), self._device.stream()),
+                "vpb_spline_sweep_axis")
+
+    def slab_copy(self, src, src_stride, dst, dst_stride, outer, run):
+        L = self._lib
+        L.check(self.lib.vpb_slab_copy(src.data_ptr(), src_stride, dst.data_ptr(), dst_stride,
+                                       outer, run, self._device.stream()), "vpb_slab_copy")
 
     def pack(self, axis, f, dims, order, cell0, width, buf):
         L = self._lib
@@ -509,6 +522,265 @@ class ShardedSolver:
             work = torch.empty(self.ops.diag_work(d), dtype=torch.float64, device=sh.f.device)
             self.ops.diag_sums(sh.f, d, wx.view(-1), self.wv1, self.wv2, self.v1sq, self.v2sq,
                                out, work)
+            sums[r] = out
+        tot = self.comm.allreduce(sums, "sum").cpu().numpy()
+        ee_t = torch.zeros(1, dtype=torch.float64, device=self.device)
+        self.ops.electric_energy(self.e, self.n1 * self.n2, self.wx_full, ee_t)
+        ee = float(ee_t.cpu()[0])
+        mass, l1, l2sq, kin = (float(x) for x in tot[:4])
+        return {"time": float(time), "electric_energy": ee, "mass": mass, "l1_norm": l1,
+                "l2_norm": math.sqrt(max(l2sq, 0.0)), "kinetic_energy": kin,
+                "total_energy": kin + ee}
+
+
+# ---------------------------------------------------------------------------
+# Sharded spline solver: all-to-all reshards (SURVEY §8e "Spline")
+# ---------------------------------------------------------------------------
+class SplineShardedSolver:
+    """Strang steps of a cubic-spline 2x2v field on W ranks.
+
+    The spline solve needs whole lines, so the field moves between two
+    layouts with an all-to-all (grouped send/recv; NCCL over NVLink) twice
+    per step:
+
+    * home layout A, split along v2: rank r holds f[v2 in V_r][v1][x2][x1],
+      a contiguous slab of the canonical buffer.  Both x sweeps are local
+      (x1 and x2 lines are whole) and so is the density partial
+      sum_{v in V_r} w f, which an all-reduce completes (every rank then
+      solves the Poisson problem redundantly).
+    * layout B, split along x2: rank s holds f[v2][v1][x2 in X_s][x1]; both
+      v sweeps are local, with tables from the local rows of E.
+
+    A -> B: rank r sends rank s the x2 rows X_s of its slab (packed with
+    vpb_slab_copy); they land as the contiguous v2 block V_r of B_s.  B -> A
+    is the reverse (received into a contiguous buffer, unpacked with
+    vpb_slab_copy).  Every line sweep is the single-GPU kernel on whole
+    lines, so f matches the single-GPU step up to the summation order of the
+    density all-reduce.
+    """
+
+    def __init__(self, grid: GridSpec, comm, ranks, world: int, ops=None, device=None):
+        if grid.method != SPLINE or grid.ndim != 4:
+            raise ValueError("the spline sharded step needs a 2x2v spline grid")
+        n1, n2, nv1, nv2 = grid.dims4
+        if world > nv2 or world > n2:
+            raise ValueError(f"cannot split {nv2} v2 / {n2} x2 points over {world} ranks")
+        self.grid = grid
+        self.comm = comm
+        self.world = world
+        self.ops = ops or CudaOps()
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.n1, self.n2, self.nv1, self.nv2 = n1, n2, nv1, nv2
+        self.vr = [split_cells(nv2, world, r) for r in range(world)]
+        self.xr = [split_cells(n2, world, r) for r in range(world)]
+        dev = self.device
+        self.ranks = list(ranks)
+        self.a = {}
+        self.b = {}
+        self.flags = {}
+        for r in self.ranks:
+            v0, v1 = self.vr[r]
+            x0, x1 = self.xr[r]
+            na = n1 * n2 * nv1 * (v1 - v0)
+            nb = n1 * (x1 - x0) * nv1 * nv2
+            self.a[r] = [torch.empty(na, dtype=torch.float64, device=dev),
+                         torch.empty(na, dtype=torch.float64, device=dev)]
+            self.b[r] = [torch.empty(nb, dtype=torch.float64, device=dev),
+                         torch.empty(nb, dtype=torch.float64, device=dev)]
+            self.flags[r] = torch.zeros(8, dtype=torch.int32, device=dev)
+        w = [torch.as_tensor(grid.axis_weights(a), dtype=torch.float64).to(dev) for a in range(4)]
+        self.wv1, self.wv2 = w[2], w[3]
+        self.wx_full = (w[1][:, None] * w[0][None, :]).reshape(-1).contiguous()
+        self.vpoints = [torch.as_tensor(grid.axis_points(a), dtype=torch.float64).to(dev)
+                        for a in (2, 3)]
+        self.v1sq = self.vpoints[0] ** 2
+        self.v2sq = self.vpoints[1] ** 2
+        self.rho = torch.empty(n1 * n2, dtype=torch.float64, device=dev)
+        self.e = torch.empty(2 * n1 * n2, dtype=torch.float64, device=dev)
+        self.stats = torch.zeros(4, dtype=torch.float64, device=dev)
+        self.solve_flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.names = ["x1 half (open)", "x2 half (open)", "field solve", "v1 full", "v2 full",
+                      "x1 half (close)", "x2 half (close)"]
+
+    # -- geometry ------------------------------------------------------------------
+    def dims_a(self, r: int):
+        v0, v1 = self.vr[r]
+        return (self.n1, self.n2, self.nv1, v1 - v0)
+
+    def dims_b(self, r: int):
+        x0, x1 = self.xr[r]
+        return (self.n1, x1 - x0, self.nv1, self.nv2)
+
+    # -- data movement helpers (tests / I/O) ----------------------------------------
+    def initialize(self, problem) -> None:
+        from . import _device, _lib
+        from .driver import separable_factors
+
+        g1, g2, space = separable_factors(problem, self.grid)
+        lib = _lib.load()
+        dg1 = torch.as_tensor(np.asarray(g1), dtype=torch.float64).to(self.device)
+        sp = torch.as_tensor(np.asarray(space).reshape(-1), dtype=torch.float64).to(self.device)
+        for r in self.ranks:
+            v0, v1 = self.vr[r]
+            dg2 = torch.as_tensor(np.asarray(g2)[v0:v1], dtype=torch.float64).to(self.device)
+            _lib.check(lib.vpb_fill_separable(self.a[r][0].data_ptr(), _lib.dims(self.dims_a(r)),
+                                              dg1.data_ptr(), dg2.data_ptr(), sp.data_ptr(),
+                                              _device.stream()), "vpb_fill_separable")
+
+    def scatter(self, logical: np.ndarray) -> None:
+        for r in self.ranks:
+            v0, v1 = self.vr[r]
+            box = np.ascontiguousarray(logical[:, :, :, v0:v1].transpose(3, 2, 1, 0))
+            self.a[r][0].copy_(torch.from_numpy(box.reshape(-1)).to(self.device))
+
+    def gather(self) -> np.ndarray:
+        out = np.empty(self.grid.dofs)
+        for r in self.ranks:
+            v0, v1 = self.vr[r]
+            d = self.dims_a(r)
+            out[:, :, :, v0:v1] = (self.a[r][0].view(d[3], d[2], d[1], d[0])
+                                   .permute(3, 2, 1, 0).cpu().numpy())
+        return out
+
+    # -- reshards ----------------------------------------------------------------------
+    def _a_to_b(self) -> None:
+        n1, nv1 = self.n1, self.nv1
+        msgs = {}
+        for r in self.ranks:
+            src = self.a[r][0]
+            v0, v1 = self.vr[r]
+            items = []
+            for s in range(self.world):
+                x0, x1 = self.xr[s]
+                run = (x1 - x0) * n1
+                outer = (v1 - v0) * nv1
+                b_off = v0 * nv1 * run  # v2 block V_r of B_s
+                if s in self.b and s == r:  # own chunk: copy straight into B
+                    dst = self.b[s][0][b_off:b_off + outer * run]
+                    self.ops.slab_copy(src[x0 * n1:], self.n2 * n1, dst, run, outer, run)
+                    continue
+                send = torch.empty(outer * run, dtype=torch.float64, device=self.device)
+                self.ops.slab_copy(src[x0 * n1:], self.n2 * n1, send, run, outer, run)
+                items.append((KIND_A2A, s, send, s, None))
+            msgs[r] = items
+        # receives: B_s gets the V_r block from every rank r != s
+        for s in self.ranks:
+            x0, x1 = self.xr[s]
+            run = (x1 - x0) * n1
+            for r in range(self.world):
+                if r == s:
+                    continue
+                v0, v1 = self.vr[r]
+                off = v0 * nv1 * run
+                recv = self.b[s][0][off:off + (v1 - v0) * nv1 * run]
+                msgs.setdefault(s, []).append((KIND_A2A, None, None, r, recv))
+        self.comm.exchange(msgs)
+
+    def _b_to_a(self) -> None:
+        n1, nv1 = self.n1, self.nv1
+        msgs = {}
+        for s in self.ranks:
+            x0, x1 = self.xr[s]
+            run = (x1 - x0) * n1
+            items = []
+            for r in range(self.world):
+                v0, v1 = self.vr[r]
+                off = v0 * nv1 * run
+                chunk = self.b[s][0][off:off + (v1 - v0) * nv1 * run]
+                if r == s:
+                    self.ops.slab_copy(chunk, run, self.a[r][0][x0 * n1:], self.n2 * n1,
+                                       (v1 - v0) * nv1, run)
+                    continue
+                items.append((KIND_A2A, r, chunk, r, None))
+            msgs[s] = items
+        recvs = {}
+        for r in self.ranks:
+            v0, v1 = self.vr[r]
+            for s in range(self.world):
+                if s == r:
+                    continue
+                x0, x1 = self.xr[s]
+                buf = torch.empty((v1 - v0) * nv1 * (x1 - x0) * n1, dtype=torch.float64,
+                                  device=self.device)
+                recvs[(r, s)] = buf
+                msgs.setdefault(r, []).append((KIND_A2A, None, None, s, buf))
+        self.comm.exchange(msgs)
+        for (r, s), buf in recvs.items():
+            v0, v1 = self.vr[r]
+            x0, x1 = self.xr[s]
+            run = (x1 - x0) * n1
+            self.ops.slab_copy(buf, run, self.a[r][0][x0 * n1:], self.n2 * n1, (v1 - v0) * nv1,
+                               run)
+
+    # -- sub-steps ---------------------------------------------------------------------
+    def _x_half(self, tau: float, slot: int) -> None:
+        """_advect_space(tau/2) on layout A (driver.py:220-228)."""
+        g = self.grid
+        for r in self.ranks:
+            v0, v1 = self.vr[r]
+            vals = (self.vpoints[0], self.vpoints[1][v0:v1].contiguous())
+            for d in range(2):
+                src, dst = self.a[r]
+                self.ops.spline_sweep(d, src, dst, self.dims_a(r), vals[d], 0.5 * tau,
+                                      g.axes[d].h, self.flags[r][slot + d:slot + d + 1])
+                self.a[r].reverse()
+
+    def _density(self) -> None:
+        parts = {}
+        for r in self.ranks:
+            d = self.dims_a(r)
+            v0, v1 = self.vr[r]
+            rl = torch.empty(self.n1 * self.n2, dtype=torch.float64, device=self.device)
+            work = torch.empty(self.ops.density_work(d), dtype=torch.float64, device=self.device)
+            self.ops.density(self.a[r][0], d, self.wv1, self.wv2[v0:v1].contiguous(), rl, work)
+            parts[r] = rl
+        self.rho.copy_(self.comm.allreduce(parts, "sum"))
+
+    def _local_e(self, s: int, d: int) -> torch.Tensor:
+        x0, x1 = self.xr[s]
+        full = self.e[d * self.n1 * self.n2:(d + 1) * self.n1 * self.n2].view(self.n2, self.n1)
+        return full[x0:x1].contiguous().view(-1)
+
+    def step(self, tau: float, time_label: float | None = None) -> None:
+        from .driver import SubstepError
+
+        g = self.grid
+        for r in self.ranks:
+            self.flags[r].zero_()
+        self.solve_flag.zero_()
+        self._x_half(tau, 0)
+        self._density()
+        self.ops.field_solve(g, self.rho, self.e, self.stats, self.solve_flag)
+        self._a_to_b()
+        for s in self.ranks:
+            for d in range(2):
+                src, dst = self.b[s]
+                self.ops.spline_sweep(2 + d, src, dst, self.dims_b(s), self._local_e(s, d), tau,
+                                      g.axes[2 + d].h, self.flags[s][3 + d:4 + d])
+                self.b[s].reverse()
+        self._b_to_a()
+        self._x_half(tau, 5)
+        for r in self.ranks:
+            self.flags[r][2:3] = torch.maximum(self.flags[r][2:3], self.solve_flag)
+        flags = self.comm.allreduce({r: self.flags[r] for r in self.ranks}, "max")
+        host = flags.cpu().numpy()
+        for k, name in enumerate(self.names):
+            if host[k]:
+                raise SubstepError(name, time_label)
+
+    def diagnostics(self, time: float = 0.0) -> dict:
+        """Global conserved quantities (driver.py:279-316) from layout A."""
+        self._density()
+        self.ops.field_solve(self.grid, self.rho, self.e, None, self.solve_flag)
+        sums = {}
+        for r in self.ranks:
+            d = self.dims_a(r)
+            v0, v1 = self.vr[r]
+            out = torch.zeros(8, dtype=torch.float64, device=self.device)
+            work = torch.empty(self.ops.diag_work(d), dtype=torch.float64, device=self.device)
+            self.ops.diag_sums(self.a[r][0], d, self.wx_full, self.wv1,
+                               self.wv2[v0:v1].contiguous(), self.v1sq,
+                               self.v2sq[v0:v1].contiguous(), out, work)
             sums[r] = out
         tot = self.comm.allreduce(sums, "sum").cpu().numpy()
         ee_t = torch.zeros(1, dtype=torch.float64, device=self.device)

@@ -69,6 +69,20 @@ class NumpyOps:
         out = self._sweep_lines(_box(src, dims), axis, dims, order, tab)
         self._store(dst, dims, out, flag)
 
+    def spline_sweep(self, axis, src, dst, dims, values, scale, h, flag):
+        arr = _box(src, dims)
+        moved = np.moveaxis(arr, axis, -1)
+        lead = moved.shape[:-1]
+        n = moved.shape[-1]
+        lines = np.ascontiguousarray(moved).reshape(-1, n)
+        idx = _line_table_index(dims, axis)
+        out = core.spline_lines(lines, idx, values.cpu().numpy() * scale, h)
+        self._store(dst, dims, np.moveaxis(out.reshape(lead + (n,)), -1, axis), flag)
+
+    def slab_copy(self, src, src_stride, dst, dst_stride, outer, run):
+        for k in range(outer):
+            dst[k * dst_stride:k * dst_stride + run] = src[k * src_stride:k * src_stride + run]
+
     def pack(self, axis, f, dims, order, cell0, width, buf):
         arr = _box(f, dims)
         sl = [slice(None)] * 4
