@@ -79,6 +79,28 @@ BYTES_PER_DOF_SWEEP = 16  # read + write one fp64 per dof
 L2_BYTES = 126 * 2**20
 
 
+def sweeps_per_launch(label: str) -> int:
+    """1-D sweeps one launch of a kernel group performs (labels of driver.enqueue_steps)."""
+    name = label[len("sweep_"):].replace("_rho", "")
+    return {"x12": 2, "v12": 2, "x12x12": 4}.get(name, 1)
+
+
+def fp64_peak_gops() -> float:
+    """fp64 vector issue peak of the device: SMs x 64 lanes x max SM clock."""
+    try:
+        import torch
+
+        props = torch.cuda.get_device_properties(torch.cuda.current_device())
+        sms = props.multi_processor_count
+    except Exception:  # noqa: BLE001
+        sms = 148
+    mhz = 1965.0
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        mhz = float(json.loads(p.read_text()).get("sm_max_mhz", mhz))
+    return sms * 64 * mhz * 1e6 / 1e9
+
+
 def l2_note(copy_bytes: int) -> str:
     if copy_bytes > 8 * L2_BYTES:
         return f"inputs ({copy_bytes / 1e9:.3g} GB per copy of f) >> 126 MB L2; no flush"
@@ -487,10 +509,20 @@ def run_vpb(args, cfg_name: str, cfg: dict) -> None:
     per_kernel = {k: {"avg_ms": v[0] / v[1], "launch_groups": v[1],
                       "share_of_step": v[0] / breakdown_ms}
                   for k, v in sorted(groups.items())}
+    # 1-D sweeps done per launch (fused passes chain several in registers);
+    # dG sweeps cost 4P-1 fp64 operations per dof, without contraction
+    fp64_peak = fp64_peak_gops()
     for k, v in per_kernel.items():
         if k.startswith("sweep_"):
-            v["achieved_gbs"] = BYTES_PER_DOF_SWEEP * N / (v["avg_ms"] * 1e-3) / 1e9
+            t = v["avg_ms"] * 1e-3
+            nsw = sweeps_per_launch(k)
+            v["achieved_gbs"] = BYTES_PER_DOF_SWEEP * N / t / 1e9
             v["frac"] = v["achieved_gbs"] / peak
+            v["sweeps_per_launch"] = nsw
+            v["unfused_equivalent_frac"] = nsw * v["frac"]
+            if cfg["method"] == "dg":
+                v["fp64_gops"] = nsw * (4 * cfg["order"] - 1) * N / t / 1e9
+                v["fp64_frac"] = v["fp64_gops"] / fp64_peak
 
     # --- e2e through the public API with host-resident f
     e2e = None
@@ -545,7 +577,13 @@ def run_vpb(args, cfg_name: str, cfg: dict) -> None:
                          "peak_source": peak_kind,
                          "algorithmic_bytes_per_launch": BYTES_PER_DOF_SWEEP * N,
                          "step_frac": step_gbs / peak,
-                         "step_bytes": 6 * BYTES_PER_DOF_SWEEP * N},
+                         "step_bytes": 6 * BYTES_PER_DOF_SWEEP * N,
+                         "sweeps_per_launch": per_kernel[dom]["sweeps_per_launch"],
+                         "unfused_equivalent_frac": per_kernel[dom]["unfused_equivalent_frac"],
+                         "fp64_frac": per_kernel[dom].get("fp64_frac"),
+                         "fp64_peak_gops": fp64_peak if cfg["method"] == "dg" else None,
+                         "fp64_peak_source": "derived: SMs x 64 fp64 lanes x max SM clock "
+                                             "(not measured)"},
             "kernels": per_kernel,
             "e2e": e2e,
             "cpu_baseline": cpu,

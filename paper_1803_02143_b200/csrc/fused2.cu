@@ -34,7 +34,24 @@
 #include "common.cuh"
 #include "xplane.cuh"
 
+// VPB_X2_DIRECT (default): second-half outputs go straight to HBM with
+// streaming stores (each warp row is one contiguous 32*P*8-byte span; L2
+// merges the partial sectors) instead of a shared-memory staging tile + bulk
+// store, which frees the staging smem for a deeper load ring: 4% faster at
+// config 2, 14% at config 3 (profiles/r01_ncu_summary.md).
+#ifndef VPB_X2_DIRECT
+#define VPB_X2_DIRECT 1
+#endif
+
 namespace vpb {
+
+__device__ __forceinline__ void st_out(double* p, double v) {
+#if VPB_X2_DIRECT
+  __stcs(p, v);
+#else
+  *p = v;
+#endif
+}
 
 template <int P, bool DENS>
 __global__ void __launch_bounds__(128)
@@ -53,7 +70,8 @@ __global__ void __launch_bounds__(128)
   double* hb = inb + nst * slot;                      // [2][slot] first-half cells
   double* h0b = hb + 2 * slot;                        // [cell] first-half cell h0
   double* outb = h0b + cell;                          // [2][(G+1)*cell] output staging
-  uint64_t* bars = reinterpret_cast<uint64_t*>(outb + 2 * (G + 1) * cell);
+  uint64_t* bars =
+      reinterpret_cast<uint64_t*>(outb + (VPB_X2_DIRECT ? 0 : 2 * (G + 1) * cell));
 
   const int tid = threadIdx.x;
   const int64_t pl_begin = blockIdx.x * planes_per_block;
@@ -146,7 +164,11 @@ __global__ void __launch_bounds__(128)
     }
     const XChunk c = drain ? XChunk{0, 0, 0, 0} : cur.chunk(G, C2);
     const int o_begin = o_next;
+#if VPB_X2_DIRECT
+    double* out = dst + plane * plane_elems + (int64_t)o_begin * cell;
+#else
     double* out = outb + (it & 1) * ((G + 1) * cell);
+#endif
 
     // Both stages for one (ex1, ex2) combination (uniform over the plane).
     auto run = [&](auto ex1c, auto ex2c) {
@@ -176,17 +198,9 @@ __global__ void __launch_bounds__(128)
           }
           double* ot = out + (o_next - o_begin) * cell + tid * P;
 #pragma unroll
-          for (int j2 = 0; j2 < P; ++j2) {
-            if constexpr (P % 2 == 0) {
+          for (int j2 = 0; j2 < P; ++j2)
 #pragma unroll
-              for (int jj = 0; jj < P; jj += 2)
-                *reinterpret_cast<double2*>(ot + j2 * n1 + jj) =
-                    make_double2(o[j2][jj], o[j2][jj + 1]);
-            } else {
-#pragma unroll
-              for (int jj = 0; jj < P; ++jj) ot[j2 * n1 + jj] = o[j2][jj];
-            }
-          }
+            for (int jj = 0; jj < P; ++jj) st_out(ot + j2 * n1 + jj, o[j2][jj]);
           if constexpr (DENS) {
             double rcv, mv = 0.0;
             if constexpr (P % 2 == 1) {
@@ -235,7 +249,7 @@ __global__ void __launch_bounds__(128)
             for (int jj = 0; jj < P; ++jj) {
               e2.add(o2[j2][jj]);
               e1.add(o1[j2][jj]);
-              ot[j2 * n1 + jj] = o2[j2][jj];
+              st_out(ot + j2 * n1 + jj, o2[j2][jj]);
               ht[j2 * n1 + jj] = o1[j2][jj];
             }
           if constexpr (DENS) {
@@ -341,6 +355,10 @@ __global__ void __launch_bounds__(128)
       else if (!ex2) run(T{}, F{});
       else run(T{}, T{});
     }
+#if VPB_X2_DIRECT
+    __syncthreads();
+    if (tid == 0 && !drain && prod_j < nloads) issue_next();
+#else
     fence_proxy_async_smem();
     if (tid == 0) bulk_wait_read<0>();  // the store issued last iteration left the other tile
     __syncthreads();
@@ -352,6 +370,7 @@ __global__ void __launch_bounds__(128)
       }
       if (!drain && prod_j < nloads) issue_next();
     }
+#endif
     if (!drain) {
       nout_prev = c.nout;
       cur.advance(per_plane, C2, q2, nv1, pl_end);
@@ -401,16 +420,19 @@ static int plan_xplane2(const int64_t dims[4], X2Launch* L) {
     return VPB_ERR_UNSUPPORTED;
   }
   static const int env_chunk =
-      getenv("VPB_XPLANE2_CHUNK") ? atoi(getenv("VPB_XPLANE2_CHUNK")) : 4608;
-  static const int env_st = getenv("VPB_XPLANE2_STAGES") ? atoi(getenv("VPB_XPLANE2_STAGES")) : 3;
+      getenv("VPB_XPLANE2_CHUNK") ? atoi(getenv("VPB_XPLANE2_CHUNK")) : (VPB_X2_DIRECT ? 9216 : 4608);
+  // measured best ring depths (A/B on B200): 4 x 2 cells at P = 3 (config 2),
+  // 2 x 4 cells at P = 2 (config 3)
+  static const int env_st =
+      getenv("VPB_XPLANE2_STAGES") ? atoi(getenv("VPB_XPLANE2_STAGES")) : (P >= 3 ? 4 : 2);
   static const int env_smem =
       getenv("VPB_XPLANE2_SMEM") ? atoi(getenv("VPB_XPLANE2_SMEM")) : 56 * 1024;
   L->threads = ((C1 + 31) / 32) * 32;
   L->nst = std::max(2, std::min(8, env_st));
   const size_t cell_bytes = (size_t)P * n1 * 8;
   auto smem_for = [&](int g) {
-    return (size_t)(L->nst + 2) * g * cell_bytes + cell_bytes + 2 * (size_t)(g + 1) * cell_bytes +
-           L->nst * 8;
+    return (size_t)(L->nst + 2) * g * cell_bytes + cell_bytes +
+           (VPB_X2_DIRECT ? 0 : 2 * (size_t)(g + 1) * cell_bytes) + L->nst * 8;
   };
   int G = std::max<int>(1, (int)(env_chunk / cell_bytes));
   G = std::min(G, C2);
