@@ -249,20 +249,33 @@ __global__ void __launch_bounds__(128)
 
 // rc[c2][c1] = sum over CTAs (in order) of the partial slabs; stats[0] =
 // weighted density mean / volume.
-__global__ void xdens_reduce_kernel(const double* __restrict__ part,
-                                    const double* __restrict__ mean_part, int64_t nblocks,
-                                    int64_t cc, double volume, double* __restrict__ rc,
-                                    double* __restrict__ stats) {
-  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e < cc) {
-    double s = 0.0;
-    for (int64_t b = 0; b < nblocks; ++b) s += part[b * cc + e];
-    rc[e] = s;
+// Block = 16 warps over 32 consecutive cells (lane = cell): warp w sums the
+// slabs b = w, w+16, ... in order, then the 16 warp partials are added in warp
+// order -- a fixed order, independent of timing.
+constexpr int kRedWarps = 16;
+
+__global__ void __launch_bounds__(32 * kRedWarps)
+    xdens_reduce_kernel(const double* __restrict__ part, const double* __restrict__ mean_part,
+                        int64_t nblocks, int64_t cc, double volume, double* __restrict__ rc,
+                        double* __restrict__ stats) {
+  __shared__ double ws[kRedWarps][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t e = (int64_t)blockIdx.x * 32 + lane;
+  double s = 0.0;
+  if (e < cc)
+    for (int64_t b = w; b < nblocks; b += kRedWarps) s += part[b * cc + e];
+  ws[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && e < cc) {
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < kRedWarps; ++k) t += ws[k][lane];
+    rc[e] = t;
   }
-  if (e == 0 && stats != nullptr) {
-    double s = 0.0;
-    for (int64_t b = 0; b < nblocks; ++b) s += mean_part[b];
-    stats[0] = s / volume;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && stats != nullptr) {
+    double m = 0.0;
+    for (int64_t b = 0; b < nblocks; ++b) m += mean_part[b];
+    stats[0] = m / volume;
   }
 }
 
@@ -386,8 +399,8 @@ int xdensity_setup(XDensity* dn, int order, const double* wv1, const double* wv2
 
 int launch_xdens_reduce(const double* work, int64_t nblk, int64_t cc, double volume,
                         double* rc_out, double* stats, cudaStream_t st) {
-  xdens_reduce_kernel<<<(unsigned)((cc + 255) / 256), 256, 0, st>>>(work, work + nblk * cc, nblk,
-                                                                    cc, volume, rc_out, stats);
+  xdens_reduce_kernel<<<(unsigned)((cc + 31) / 32), 32 * kRedWarps, 0, st>>>(
+      work, work + nblk * cc, nblk, cc, volume, rc_out, stats);
   return launched("xdens_reduce_kernel");
 }
 
