@@ -141,6 +141,22 @@ int vpb_dg_sweep_xplane_density(const double* src, double* dst, const int64_t di
                                 double volume, double* work, double* rc_out, double* stats,
                                 void* stream);
 
+/* vpb_dg_sweep_xplane_density plus the diagnostics moments of the OUTPUT
+ * (driver.py:279-316: mass, l1, l2^2, kinetic -> diag_out[0..3]); v1sq /
+ * v2sq: DEVICE squared velocity nodes.  With the field solve of rc_out and
+ * vpb_electric_energy this is a whole DiagnosticsRecord of the post-step
+ * state without re-reading f.  Same work buffer as the density variant. */
+int vpb_dg_sweep_xplane_moments(const double* src, double* dst, const int64_t dims[4],
+                                int32_t order, const double* a1, const double* b1,
+                                const int64_t* q1, const double* alpha1, const double* a2,
+                                const double* b2, const int64_t* q2, const double* alpha2,
+                                int32_t* flag1, int32_t* flag2, const double* wv1,
+                                const double* wv2, const double* mid_host,
+                                const double* wcell1_host, const double* wcell2_host,
+                                const double* v1sq, const double* v2sq, double volume,
+                                double* work, double* rc_out, double* stats, double* diag_out,
+                                void* stream);
+
 /* Two consecutive x half steps in one HBM pass: the closing x1(τ/2) x2(τ/2)
  * of a Strang step followed by the opening x1(τ/2) x2(τ/2) of the next one
  * (driver.py:245-265 applied twice; run loop driver.py:371-377), with the

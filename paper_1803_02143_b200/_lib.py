@@ -78,6 +78,8 @@ SIGNATURES = {
                                             c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                             c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                             c_double, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "vpb_dg_sweep_xplane_moments": (c_int, [c_void_p, c_void_p, POINTER(c_int64), c_int32]
+                                    + [c_void_p] * 17 + [c_double] + [c_void_p] * 5),
     "vpb_dg_sweep_xplane2": (c_int, [c_void_p, c_void_p, POINTER(c_int64), c_int32]
                              + [c_void_p] * 13),
     "vpb_dg_xplane2_density_work_len": (c_int64, [POINTER(c_int64), c_int32]),
@@ -124,7 +126,10 @@ def load(path: Path | None = None):
             "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)"
         )
     lib = ctypes.CDLL(str(p))
+    override = not path and bool(os.environ.get("VPB_LIB"))
     for name, (res, args) in SIGNATURES.items():
+        if override and not hasattr(lib, name):
+            continue  # an older build under A/B timing: entry points it lacks stay unbound
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

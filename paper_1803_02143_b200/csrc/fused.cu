@@ -37,7 +37,9 @@ namespace vpb {
 
 constexpr int kXStages = 6;
 
-template <int P, bool DENS>
+// DM: 0 = sweeps only, 1 = + density epilogue, 2 = + diagnostics moments
+// (mass, l1, l2^2, kinetic of the output, driver.py:279-316) as well.
+template <int P, int DM>
 __global__ void __launch_bounds__(128)
     dg_xplane_kernel(const double* __restrict__ src, double* __restrict__ dst, int n1, int C2,
                      int G, int64_t nv1, int64_t nplanes, int64_t planes_per_block,
@@ -46,7 +48,7 @@ __global__ void __launch_bounds__(128)
                      const double* __restrict__ a2, const double* __restrict__ b2,
                      const int64_t* __restrict__ q2, const double* __restrict__ al2,
                      int32_t* __restrict__ flag1, int32_t* __restrict__ flag2,
-                     const XDensity dn) {
+                     const XDensity dn, const XMoments mo) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int cell = P * n1;          // one x2 cell: P rows of n1 dofs
   const int slot = G * cell;        // ring slot
@@ -104,8 +106,10 @@ __global__ void __launch_bounds__(128)
   int st = 0;
   uint32_t phase = 0;
   // density epilogue state
+  constexpr bool DENS = DM >= 1;
   constexpr bool dens = DENS;
   double wplane = 0.0, meanacc = 0.0;
+  double kplane = 0.0, l1acc = 0.0, l2acc = 0.0, kinacc = 0.0;  // DM == 2
   double* mypart = dens ? dn.rc_part + (int64_t)blockIdx.x * C2 * C1 : nullptr;
   if (dens && active)
     for (int c2 = 0; c2 < C2; ++c2) mypart[c2 * C1 + tid] = 0.0;
@@ -116,6 +120,7 @@ __global__ void __launch_bounds__(128)
     if (active && cur.i == 0) {
       const int64_t iv2 = plane / nv1, iv1 = plane - iv2 * nv1;
       if (dens) wplane = dn.wv1[iv1] * dn.wv2[iv2];
+      if (DM == 2) kplane = 0.5 * (mo.vsq1[iv1] + mo.vsq2[iv2]);
       ex1 = (al1[iv1] == 0.0);
       ex2 = (al2[iv2] == 0.0);
 #pragma unroll
@@ -191,10 +196,26 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
                 for (int jj = 0; jj < P; ++jj) rcv = fma(dn.mm[j2 * P + jj], o[j2][jj], rcv);
             }
+            if constexpr (DM == 2) {
+              double l1 = 0.0, l2 = 0.0;
 #pragma unroll
-            for (int j2 = 0; j2 < P; ++j2)
+              for (int j2 = 0; j2 < P; ++j2)
 #pragma unroll
-              for (int jj = 0; jj < P; ++jj) mv = fma(dn.ww[j2 * P + jj], o[j2][jj], mv);
+                for (int jj = 0; jj < P; ++jj) {
+                  const double t = dn.ww[j2 * P + jj] * o[j2][jj];
+                  mv += t;
+                  l1 += fabs(t);
+                  l2 = fma(t, o[j2][jj], l2);
+                }
+              l1acc = fma(wplane, l1, l1acc);
+              l2acc = fma(wplane, l2, l2acc);
+              kinacc = fma(wplane * kplane, mv, kinacc);
+            } else {
+#pragma unroll
+              for (int j2 = 0; j2 < P; ++j2)
+#pragma unroll
+                for (int jj = 0; jj < P; ++jj) mv = fma(dn.ww[j2 * P + jj], o[j2][jj], mv);
+            }
             atomicAdd(mypart + (c.first + sc) * C1 + tid, dmul(wplane, rcv));
             meanacc = fma(wplane, mv, meanacc);
           }
@@ -233,16 +254,24 @@ __global__ void __launch_bounds__(128)
   if (tid == 0) bulk_wait<0>();
   report_flag(bad1, flag1);
   report_flag(bad2, flag2);
-  if (dens) {  // fixed-order block sum of the neutrality-mean partials
-    __shared__ double red[4];
+  if (dens) {  // fixed-order block sums of the mean (and moment) partials
+    __shared__ double red[4][4];
+    double v[4] = {meanacc, l1acc, l2acc, kinacc};
+    constexpr int nv = DM == 2 ? 4 : 1;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) meanacc += __shfl_down_sync(0xffffffffu, meanacc, o);
-    if ((tid & 31) == 0) red[tid >> 5] = meanacc;
+    for (int k = 0; k < nv; ++k) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_down_sync(0xffffffffu, v[k], o);
+      if ((tid & 31) == 0) red[k][tid >> 5] = v[k];
+    }
     __syncthreads();
-    if (tid == 0) {
+    if (tid < nv) {
       double s = 0.0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
-      dn.mean_part[blockIdx.x] = s;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[tid][w];
+      if (tid == 0)
+        dn.mean_part[blockIdx.x] = s;
+      else
+        mo.mom_part[blockIdx.x * 3 + tid - 1] = s;
     }
   }
 }
@@ -257,7 +286,8 @@ constexpr int kRedWarps = 16;
 __global__ void __launch_bounds__(32 * kRedWarps)
     xdens_reduce_kernel(const double* __restrict__ part, const double* __restrict__ mean_part,
                         int64_t nblocks, int64_t cc, double volume, double* __restrict__ rc,
-                        double* __restrict__ stats) {
+                        double* __restrict__ stats, const double* __restrict__ mom_part,
+                        double* __restrict__ diag_out) {
   __shared__ double ws[kRedWarps][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t e = (int64_t)blockIdx.x * 32 + lane;
@@ -272,10 +302,18 @@ __global__ void __launch_bounds__(32 * kRedWarps)
     for (int k = 0; k < kRedWarps; ++k) t += ws[k][lane];
     rc[e] = t;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0 && stats != nullptr) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     double m = 0.0;
     for (int64_t b = 0; b < nblocks; ++b) m += mean_part[b];
-    stats[0] = m / volume;
+    if (stats != nullptr) stats[0] = m / volume;
+    if (diag_out != nullptr) diag_out[0] = m;  // mass
+  }
+  if (blockIdx.x == 0 && threadIdx.x >= 32 && threadIdx.x < 35 && diag_out != nullptr &&
+      mom_part != nullptr) {
+    const int k = threadIdx.x - 32;  // l1, l2^2, kinetic
+    double m = 0.0;
+    for (int64_t b = 0; b < nblocks; ++b) m += mom_part[b * 3 + k];
+    diag_out[1 + k] = m;
   }
 }
 
@@ -296,7 +334,7 @@ struct XLaunch {
   int64_t ppb, blocks;
 };
 
-template <int P, bool DENS>
+template <int P, int DM>
 static int plan_xplane(const int64_t dims[4], XLaunch* L) {
   const int n1 = (int)dims[0];
   const int C1 = n1 / P;
@@ -326,12 +364,12 @@ static int plan_xplane(const int64_t dims[4], XLaunch* L) {
   }
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(dg_xplane_kernel<P, DENS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(dg_xplane_kernel<P, DM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          220 * 1024);
     attr = true;
   }
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dg_xplane_kernel<P, DENS>, L->threads,
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dg_xplane_kernel<P, DM>, L->threads,
                                                 L->smem);
   if (occ < 1) occ = 1;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(nplanes, (int64_t)occ * xplane_sm_count()));
@@ -340,7 +378,7 @@ static int plan_xplane(const int64_t dims[4], XLaunch* L) {
   return VPB_OK;
 }
 
-template <int P, bool DENS>
+template <int P, int DM>
 static int launch_xplane(const double* src, double* dst, const int64_t dims[4], const double* a1,
                          const double* b1, const int64_t* q1, const double* al1,
                          const double* a2, const double* b2, const int64_t* q2,
@@ -349,23 +387,56 @@ static int launch_xplane(const double* src, double* dst, const int64_t dims[4], 
   const int64_t nplanes = dims[2] * dims[3];
   if (nplanes == 0) return VPB_OK;
   XLaunch L;
-  int rc = plan_xplane<P, DENS>(dims, &L);
+  int rc = plan_xplane<P, DM>(dims, &L);
   if (rc) return rc;
-  dg_xplane_kernel<P, DENS><<<(unsigned)L.blocks, L.threads, L.smem, st>>>(
+  dg_xplane_kernel<P, DM><<<(unsigned)L.blocks, L.threads, L.smem, st>>>(
       src, dst, (int)dims[0], (int)(dims[1] / P), L.G, dims[2], nplanes, L.ppb, a1, b1, q1, al1,
-      a2, b2, q2, al2, f1, f2, dn);
+      a2, b2, q2, al2, f1, f2, dn, XMoments{nullptr, nullptr, nullptr});
   if (nblocks_out) *nblocks_out = L.blocks;
   return launched("dg_xplane_kernel");
 }
 
+// Work of the density / moments epilogues: [blocks][cc] slabs, [blocks] mean
+// partials, [blocks][3] moment partials; sized for the larger of the two plans.
 template <int P>
 static int xplane_density_len(const int64_t dims[4], int64_t* len) {
-  XLaunch L;
-  int rc = plan_xplane<P, true>(dims, &L);
+  XLaunch L1, L2;
+  int rc = plan_xplane<P, 1>(dims, &L1);
+  if (rc == VPB_OK) rc = plan_xplane<P, 2>(dims, &L2);
   if (rc) return rc;
   const int64_t cc = (dims[0] / P) * (dims[1] / P);
-  *len = L.blocks * (cc + 1);
+  *len = std::max(L1.blocks, L2.blocks) * (cc + 4);
   return VPB_OK;
+}
+
+// Density (DM 1) or density + diagnostics moments (DM 2) pass, then the
+// fixed-order reduction of the CTA partials.
+template <int P, int DM>
+static int xplane_epilogue_pass(const double* src, double* dst, const int64_t dims[4],
+                                const double* a1, const double* b1, const int64_t* q1,
+                                const double* al1, const double* a2, const double* b2,
+                                const int64_t* q2, const double* al2, int32_t* f1, int32_t* f2,
+                                const double* wv1, const double* wv2, const double* mid_host,
+                                const double* wc1, const double* wc2, const double* vsq1,
+                                const double* vsq2, double volume, double* work, double* rc_out,
+                                double* stats, double* diag_out, cudaStream_t st) {
+  const int64_t nplanes = dims[2] * dims[3];
+  if (nplanes == 0) return VPB_OK;
+  XLaunch L;
+  int rc = plan_xplane<P, DM>(dims, &L);
+  if (rc) return rc;
+  const int64_t cc = (dims[0] / P) * (dims[1] / P);
+  XDensity dn;
+  rc = xdensity_setup(&dn, P, wv1, wv2, mid_host, wc1, wc2, work, L.blocks, cc);
+  if (rc) return rc;
+  const XMoments mo{dn.mean_part + L.blocks, vsq1, vsq2};
+  dg_xplane_kernel<P, DM><<<(unsigned)L.blocks, L.threads, L.smem, st>>>(
+      src, dst, (int)dims[0], (int)(dims[1] / P), L.G, dims[2], nplanes, L.ppb, a1, b1, q1, al1,
+      a2, b2, q2, al2, f1, f2, dn, mo);
+  rc = launched("dg_xplane_kernel");
+  if (rc) return rc;
+  return launch_xdens_reduce(work, L.blocks, cc, volume, rc_out, stats, st,
+                             DM == 2 ? mo.mom_part : nullptr, DM == 2 ? diag_out : nullptr);
 }
 
 int xplane_args_ok(const double* src, const double* dst, const int64_t dims[4], int32_t order) {
@@ -398,9 +469,10 @@ int xdensity_setup(XDensity* dn, int order, const double* wv1, const double* wv2
 }
 
 int launch_xdens_reduce(const double* work, int64_t nblk, int64_t cc, double volume,
-                        double* rc_out, double* stats, cudaStream_t st) {
+                        double* rc_out, double* stats, cudaStream_t st, const double* mom_part,
+                        double* diag_out) {
   xdens_reduce_kernel<<<(unsigned)((cc + 31) / 32), 32 * kRedWarps, 0, st>>>(
-      work, work + nblk * cc, nblk, cc, volume, rc_out, stats);
+      work, work + nblk * cc, nblk, cc, volume, rc_out, stats, mom_part, diag_out);
   return launched("xdens_reduce_kernel");
 }
 
@@ -417,7 +489,7 @@ extern "C" int vpb_dg_sweep_xplane(const double* src, double* dst, const int64_t
   int rc = xplane_args_ok(src, dst, dims, order);
   if (rc) return rc;
   const XDensity none{nullptr, nullptr, nullptr, nullptr, {}, {}};
-  VPB_XPLANE_SWITCH(order, rc = launch_xplane<PP, false>(src, dst, dims, a1, b1, q1, alpha1, a2,
+  VPB_XPLANE_SWITCH(order, rc = launch_xplane<PP, 0>(src, dst, dims, a1, b1, q1, alpha1, a2,
                                                   b2, q2, alpha2, flag1, flag2, none,
                                                   (cudaStream_t)stream, nullptr));
   return rc;
@@ -440,23 +512,32 @@ extern "C" int vpb_dg_sweep_xplane_density(
     void* stream) {
   int rc = xplane_args_ok(src, dst, dims, order);
   if (rc) return rc;
-  VPB_REQUIRE(wv1 && wv2 && mid_host && wcell1_host && wcell2_host && work && rc_out,
-              "null pointer");
-  const int64_t cc = (dims[0] / order) * (dims[1] / order);
-  int64_t len = vpb_dg_xplane_density_work_len(dims, order);
-  VPB_REQUIRE(len > 0, "cannot plan the x-plane launch");
-  const int64_t nblk = len / (cc + 1);
-  XDensity dn;
-  rc = xdensity_setup(&dn, order, wv1, wv2, mid_host, wcell1_host, wcell2_host, work, nblk, cc);
-  if (rc) return rc;
-  int64_t used = 0;
+  VPB_REQUIRE(rc_out != nullptr, "null pointer");
   cudaStream_t st = (cudaStream_t)stream;
-  VPB_XPLANE_SWITCH(order, rc = launch_xplane<PP, true>(src, dst, dims, a1, b1, q1, alpha1, a2,
-                                                  b2, q2, alpha2, flag1, flag2, dn, st, &used));
+  VPB_XPLANE_SWITCH(order, rc = xplane_epilogue_pass<PP, 1>(
+                               src, dst, dims, a1, b1, q1, alpha1, a2, b2, q2, alpha2, flag1,
+                               flag2, wv1, wv2, mid_host, wcell1_host, wcell2_host, nullptr,
+                               nullptr, volume, work, rc_out, stats, nullptr, st));
+  return rc;
+}
+
+extern "C" int vpb_dg_sweep_xplane_moments(
+    const double* src, double* dst, const int64_t dims[4], int32_t order, const double* a1,
+    const double* b1, const int64_t* q1, const double* alpha1, const double* a2,
+    const double* b2, const int64_t* q2, const double* alpha2, int32_t* flag1, int32_t* flag2,
+    const double* wv1, const double* wv2, const double* mid_host, const double* wcell1_host,
+    const double* wcell2_host, const double* v1sq, const double* v2sq, double volume,
+    double* work, double* rc_out, double* stats, double* diag_out, void* stream) {
+  int rc = xplane_args_ok(src, dst, dims, order);
   if (rc) return rc;
-  VPB_REQUIRE(used == nblk, "x-plane launch plan changed (%lld vs %lld CTAs)", (long long)used,
-              (long long)nblk);
-  return launch_xdens_reduce(work, nblk, cc, volume, rc_out, stats, st);
+  VPB_REQUIRE(rc_out != nullptr && v1sq != nullptr && v2sq != nullptr && diag_out != nullptr,
+              "null pointer");
+  cudaStream_t st = (cudaStream_t)stream;
+  VPB_XPLANE_SWITCH(order, rc = xplane_epilogue_pass<PP, 2>(
+                               src, dst, dims, a1, b1, q1, alpha1, a2, b2, q2, alpha2, flag1,
+                               flag2, wv1, wv2, mid_host, wcell1_host, wcell2_host, v1sq, v2sq,
+                               volume, work, rc_out, stats, diag_out, st));
+  return rc;
 }
 
 namespace vpb {

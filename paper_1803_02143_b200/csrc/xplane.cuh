@@ -148,14 +148,23 @@ struct XDensity {
   double ww[kMaxOrder * kMaxOrder];  // cell space weights wcell2[j2] * wcell1[jj]
 };
 
+// Diagnostics-moment partials of the single x pass (fused.cu, DM == 2).
+struct XMoments {
+  double* mom_part;    // [grid][3] = l1, l2^2, kinetic
+  const double* vsq1;  // [nv1] v1^2
+  const double* vsq2;  // [nv2] v2^2
+};
+
 int xplane_sm_count();
 int xplane_args_ok(const double* src, const double* dst, const int64_t dims[4], int32_t order);
 int xdensity_setup(XDensity* dn, int order, const double* wv1, const double* wv2,
                    const double* mid_host, const double* wcell1_host, const double* wcell2_host,
                    double* work, int64_t nblk, int64_t cc);
 // rc[c2][c1] = fixed-order sum of the CTA slabs; stats[0] = mean / volume
+// With mom_part / diag_out: diag_out[0..3] = mass, l1, l2^2, kinetic as well.
 int launch_xdens_reduce(const double* work, int64_t nblk, int64_t cc, double volume,
-                        double* rc_out, double* stats, cudaStream_t st);
+                        double* rc_out, double* stats, cudaStream_t st,
+                        const double* mom_part = nullptr, double* diag_out = nullptr);
 
 }  // namespace vpb
 

@@ -353,7 +353,7 @@ def enqueue_step(field: DistributionField, tau: float, state: StepState | None =
 
 def enqueue_steps(field: DistributionField, tau: float, nsteps: int, st: StepState,
                   flags: torch.Tensor, stats: torch.Tensor, timer=None,
-                  merge: bool = True) -> None:
+                  merge: bool = True, moments: torch.Tensor | None = None) -> None:
     """Queue ``nsteps`` Strang steps (driver.py:245-265 each).
 
     ``flags[m]`` / ``stats[m]`` receive step m's flag words (slots as
@@ -362,6 +362,11 @@ def enqueue_steps(field: DistributionField, tau: float, nsteps: int, st: StepSta
     one HBM pass (``vpb_dg_sweep_xplane2``: four sweeps chained in registers
     and shared memory, bitwise equal to running them separately); the state
     between the two steps is then never written to HBM.
+
+    ``moments`` (8 doubles, needs ``st.fused_rho``): the closing pass of the
+    last step also produces the diagnostics of the final state
+    (driver.py:279-316; fresh ρ -> E of that state): moments[0..4] = mass,
+    l1, l2^2, kinetic, electric energy and moments[5] = its density mean.
     """
     grid = field.grid
     mark = timer or (lambda label: None)
@@ -439,11 +444,31 @@ def enqueue_steps(field: DistributionField, tau: float, nsteps: int, st: StepSta
                 tab = st.v_tables(d, tau)
                 sweep(nx + d, tab, tau, f"sweep_{vn[d]}", fl[v_k + d:v_k + d + 1])
 
+    def x_close_with_moments(fl) -> None:
+        out = st.buf
+        t1, t2 = st.x_tables(0, tau), st.x_tables(1, tau)
+        mark("sweep_x12_diag")
+        xplane_moments_dg(grid, field._phys.view(-1), out, t1, t2, fl[close_k:close_k + 1],
+                          fl[close_k + 1:close_k + 2], st, moments)
+        swap(out)
+        mark("diag_field")
+        solve_into(st.rc, grid, st.e, None, None, centred=True)
+        lib = _lib.load()
+        _lib.check(lib.vpb_electric_energy(st.e.data_ptr(), st.geom.ncomp, st.nx,
+                                           st.geom.tensors["wx"].data_ptr(),
+                                           moments[4:5].data_ptr(), _device.stream()),
+                   "vpb_electric_energy")
+
+    if moments is not None and not (st.fused_x and st.fused_rho):
+        raise ValueError("fused diagnostics need the fused x pass with the density epilogue")
     x_half(flags[0], 0, st.fused_rho, stats[0])  # "open" of step 0
     for m in range(nsteps):
         field_and_velocity(m)
         if m + 1 == nsteps:
-            x_half(flags[m], close_k, False, None)  # "close" of the last step
+            if moments is not None:
+                x_close_with_moments(flags[m])
+            else:
+                x_half(flags[m], close_k, False, None)  # "close" of the last step
         elif merge and st.fused_x:
             x_double(flags[m], flags[m + 1], st.fused_rho, stats[m + 1])
         else:
@@ -467,6 +492,24 @@ def xplane_density_dg(grid, src, dst, t1, t2, flag1, flag2, st: StepState, stats
             g.volume, st.rho_work.data_ptr(), st.rc.data_ptr(),
             stats.data_ptr(), _device.stream()),
         "vpb_dg_sweep_xplane_density",
+    )
+
+
+def xplane_moments_dg(grid, src, dst, t1, t2, flag1, flag2, st: StepState, moments) -> None:
+    """Fused x pass with the density epilogue (-> st.rc) and the diagnostics
+    moments of its output (-> moments[0..3], its mean -> moments[5])."""
+    lib = _lib.load()
+    g = st.geom
+    _lib.check(
+        lib.vpb_dg_sweep_xplane_moments(
+            src.data_ptr(), dst.data_ptr(), _lib.dims(grid.dims4), t1.order, t1.a.data_ptr(),
+            t1.b.data_ptr(), t1.q.data_ptr(), t1.alpha.data_ptr(), t2.a.data_ptr(),
+            t2.b.data_ptr(), t2.q.data_ptr(), t2.alpha.data_ptr(), flag1.data_ptr(),
+            flag2.data_ptr(), st.wv1.data_ptr(), st.wv2.data_ptr(),
+            st.dens_mid.ctypes.data, st.dens_w1.ctypes.data, st.dens_w2.ctypes.data,
+            st.v1sq.data_ptr(), st.v2sq.data_ptr(), g.volume, st.rho_work.data_ptr(),
+            st.rc.data_ptr(), moments[5:6].data_ptr(), moments.data_ptr(), _device.stream()),
+        "vpb_dg_sweep_xplane_moments",
     )
 
 
@@ -562,7 +605,7 @@ def strang_step(field: DistributionField, tau: float, workers: int = 1, consume:
 
 
 def advance(field: DistributionField, tau: float, nsteps: int, consume: bool = False,
-            first_step: int | None = None) -> DistributionField:
+            first_step: int | None = None, record_time: float | None = None):
     """``nsteps`` Strang steps; the result is bitwise that of ``nsteps``
     :func:`strang_step` calls, with the same errors and warnings.
 
@@ -572,6 +615,11 @@ def advance(field: DistributionField, tau: float, nsteps: int, consume: bool = F
     needed.  Non-finite checks and neutrality warnings are evaluated after
     the last step, in step order; with ``first_step`` the errors carry the
     time label ``(first_step + m) * tau`` of step m (as run() labels them).
+
+    With ``record_time`` the result is ``(field, DiagnosticsRecord)``: the
+    diagnostics of the final state (== ``diagnostics(field, record_time)``
+    up to summation order), computed by the closing x pass itself when the
+    fused path is available (no extra read of f).
     """
     if nsteps < 0:
         raise ValueError("nsteps must be non-negative")
@@ -582,9 +630,20 @@ def advance(field: DistributionField, tau: float, nsteps: int, consume: bool = F
     dev = _device.device()
     flags = torch.zeros((nsteps, st.flags.numel()), dtype=torch.int32, device=dev)
     stats = torch.zeros((nsteps, st.stats.numel()), dtype=torch.float64, device=dev)
-    enqueue_steps(work, tau, nsteps, st, flags, stats)
+    fused_record = record_time is not None and st.fused_x and st.fused_rho
+    moments = torch.zeros(8, dtype=torch.float64, device=dev) if fused_record else None
+    enqueue_steps(work, tau, nsteps, st, flags, stats, moments=moments)
     check_steps(st, flags, stats, first_step, tau)
-    return work
+    if record_time is None:
+        return work
+    if not fused_record:
+        return work, diagnostics(work, record_time)
+    v = moments.cpu().numpy()
+    _warn_if_not_neutral(float(v[5]))
+    mass, l1, l2sq, kin, ee = (float(x) for x in v[:5])
+    return work, DiagnosticsRecord(
+        time=float(record_time), electric_energy=ee, mass=mass, l1_norm=l1,
+        l2_norm=float(math.sqrt(max(l2sq, 0.0))), kinetic_energy=kin, total_energy=kin + ee)
 
 
 def check_steps(st: StepState, flags: torch.Tensor, stats: torch.Tensor,
@@ -711,11 +770,14 @@ def run(config: RunConfig):
                    | {m for m in snap_at if m > 0} | ({nsteps} if nsteps else set()))
     done = 0
     for m in stops:
-        field = advance(field, config.tau, m - done, consume=True, first_step=done + 1)
-        done = m
         t = m * config.tau
         if m % config.diag_every == 0:
-            records.append(diagnostics(field, time=t))
+            field, rec = advance(field, config.tau, m - done, consume=True, first_step=done + 1,
+                                 record_time=t)
+            records.append(rec)
+        else:
+            field = advance(field, config.tau, m - done, consume=True, first_step=done + 1)
+        done = m
         if m in snap_at:
             capture(snap_at[m])
     return records, snapshots

@@ -484,3 +484,17 @@ def test_run_with_sparse_diagnostics_matches_every_step_records():
         for k in KEYS[1:]:
             assert getattr(r, k) == pytest.approx(getattr(r1, k), rel=1e-12, abs=1e-300), k
     assert snaps[0][0] == pytest.approx(0.5)
+
+
+@pytest.mark.parametrize("order,dofs", [(3, (24, 18, 12, 15)), (2, (128, 22, 4, 6)),
+                                        (3, (192, 24, 6, 6))])
+def test_advance_record_matches_diagnostics_of_the_final_state(order, dofs):
+    """The closing pass's diagnostics epilogue == diagnostics() of the state."""
+    prob = vpb.problem_spec("landau4d")
+    grid = vpb.make_grid(prob, "dg", dofs, dg_order=order)
+    f, rec = vpb.advance(vpb.initialize(prob, grid), 0.37, 3, record_time=1.11)
+    assert driver.step_state(grid).fused_rho
+    ref = vpb.diagnostics(f, 1.11)
+    assert rec.time == ref.time
+    for k in KEYS[1:]:
+        assert getattr(rec, k) == pytest.approx(getattr(ref, k), rel=1e-12, abs=1e-300), k
