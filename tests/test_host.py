@@ -186,3 +186,25 @@ def test_substep_error_message():
     err = vpb.SubstepError("x1 half (open)", 0.1)
     assert str(err) == "non-finite values after sub-step 'x1 half (open)' at t=0.1"
     assert str(vpb.SubstepError("field solve")) == "non-finite values after sub-step 'field solve'"
+
+
+def test_diagnostics_csv_and_meta_match_the_reference_cli_format(tmp_path):
+    from paper_1803_02143_b200 import records
+    from paper_1803_02143_b200.driver import DiagnosticsRecord
+
+    recs = [DiagnosticsRecord(0.0, 1.0 / 3.0, 2.0, 2.5, 0.1, 1e-300, 1.0 / 3.0 + 1e-300),
+            DiagnosticsRecord(0.05, 2.5e-7, 39.47841760435743, 39.4784176043574, 3.0, 1.5, 1.5)]
+    out = tmp_path / "sub" / "run.csv"
+    records.write_diagnostics_csv(out, recs)
+    lines = out.read_text().split("\n")
+    assert lines[0] == "time,electric_energy,mass,l1_norm,l2_norm,kinetic_energy,total_energy"
+    for rec, line in zip(recs, lines[1:3]):
+        assert line == ",".join(format(float(v), ".17g") for v in (
+            rec.time, rec.electric_energy, rec.mass, rec.l1_norm, rec.l2_norm,
+            rec.kinetic_energy, rec.total_energy))
+    assert lines[2].startswith("0.050000000000000003,2.4999999999999999e-07,39.478417604357432,")
+    assert lines[-1] == "" and len(lines) == 4
+    records.write_meta(out, "run cfg.toml", {"tau": "0.05", "grid": "dg"}, ["synthetic"])
+    meta = out.with_suffix(".meta").read_text().split("\n")
+    assert meta[:3] == [f"version = {vpb.__version__}", "command = run cfg.toml", "backend = cuda"]
+    assert meta[3:6] == ["grid = dg", "tau = 0.05", "note = synthetic"]
