@@ -498,3 +498,20 @@ def test_advance_record_matches_diagnostics_of_the_final_state(order, dofs):
     assert rec.time == ref.time
     for k in KEYS[1:]:
         assert getattr(rec, k) == pytest.approx(getattr(ref, k), rel=1e-12, abs=1e-300), k
+
+
+@pytest.mark.parametrize("prob,method,dofs,order", [
+    ("landau4d", "spline", 16, 0), ("landau2d", "dg", 32, 4), ("landau2d", "spline", 32, 0)])
+def test_advance_without_fused_x_pass_equals_strang_steps(prob, method, dofs, order):
+    """Grids without the fused x pass (spline, 1x1v) run advance() as plain
+    steps: bitwise the strang_step loop, records via diagnostics()."""
+    problem = vpb.problem_spec(prob)
+    grid = vpb.make_grid(problem, method, dofs, dg_order=order)
+    f1 = vpb.initialize(problem, grid)
+    for _ in range(3):
+        f1 = vpb.strang_step(f1, 0.1, consume=True)
+    f2, rec = vpb.advance(vpb.initialize(problem, grid), 0.1, 3, record_time=0.3)
+    assert np.array_equal(f1.numpy(), f2.numpy())
+    ref = vpb.diagnostics(f1, 0.3)
+    for k in KEYS:
+        assert getattr(rec, k) == getattr(ref, k), k
