@@ -49,6 +49,7 @@ __global__ void __launch_bounds__(128)
                      const int64_t* __restrict__ q2, const double* __restrict__ al2,
                      int32_t* __restrict__ flag1, int32_t* __restrict__ flag2,
                      const XDensity dn, const XMoments mo) {
+  constexpr bool DENS = DM >= 1;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int cell = P * n1;          // one x2 cell: P rows of n1 dofs
   const int slot = G * cell;        // ring slot
@@ -64,6 +65,9 @@ __global__ void __launch_bounds__(128)
   const int64_t nchunks = (pl_end - pl_begin) * per_plane;
   const int64_t plane_elems = (int64_t)C2 * cell;
 
+  // L2 policies: f streams through (evict first); the density slabs stay
+  const uint64_t pol_stream = l2_evict_first();
+  const uint64_t pol_keep = l2_evict_last();
   // producer cursor (thread 0 only)
   XCursor prod;
   prod.start(pl_begin, C2, q2, nv1);
@@ -75,11 +79,19 @@ __global__ void __launch_bounds__(128)
     double* dstp = inb + prod_st * slot;
     mbar_arrive_expect_tx(bars + prod_st, (uint32_t)c.nsrc * cell * 8u);
     const int run1 = min(c.nsrc, C2 - c.s_begin);
-    bulk_g2s(dstp, base + (int64_t)c.s_begin * cell, (uint32_t)run1 * cell * 8u,
-             bars + prod_st);
+    // with a density epilogue, keep its slabs in L2: f streams evict-first
+    if (DENS)
+      bulk_g2s_hint(dstp, base + (int64_t)c.s_begin * cell, (uint32_t)run1 * cell * 8u,
+                    bars + prod_st, pol_stream);
+    else
+      bulk_g2s(dstp, base + (int64_t)c.s_begin * cell, (uint32_t)run1 * cell * 8u, bars + prod_st);
     if (run1 < c.nsrc)  // wrapped: the rest starts at source cell 0
-      bulk_g2s(dstp + run1 * cell, base, (uint32_t)(c.nsrc - run1) * cell * 8u,
-               bars + prod_st);
+      if (DENS)
+        bulk_g2s_hint(dstp + run1 * cell, base, (uint32_t)(c.nsrc - run1) * cell * 8u,
+                      bars + prod_st, pol_stream);
+      else
+        bulk_g2s(dstp + run1 * cell, base, (uint32_t)(c.nsrc - run1) * cell * 8u,
+                 bars + prod_st);
     ++prod_j;
     if (++prod_st == kXStages) prod_st = 0;
     prod.advance(per_plane, C2, q2, nv1, pl_end);
@@ -106,7 +118,6 @@ __global__ void __launch_bounds__(128)
   int st = 0;
   uint32_t phase = 0;
   // density epilogue state
-  constexpr bool DENS = DM >= 1;
   constexpr bool dens = DENS;
   double wplane = 0.0, meanacc = 0.0;
   double kplane = 0.0, l1acc = 0.0, l2acc = 0.0, kinacc = 0.0;  // DM == 2
@@ -216,7 +227,7 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
                 for (int jj = 0; jj < P; ++jj) mv = fma(dn.ww[j2 * P + jj], o[j2][jj], mv);
             }
-            atomicAdd(mypart + (c.first + sc) * C1 + tid, dmul(wplane, rcv));
+            red_add_hint(mypart + (c.first + sc) * C1 + tid, dmul(wplane, rcv), pol_keep);
             meanacc = fma(wplane, mv, meanacc);
           }
         }
@@ -239,8 +250,12 @@ __global__ void __launch_bounds__(128)
     __syncthreads();
     if (tid == 0) {
       if (c.nout > 0) {
-        bulk_s2g(dst + plane * plane_elems + (int64_t)c.first * cell, out,
-                 (uint32_t)c.nout * cell * 8u);
+        if (DENS)
+          bulk_s2g_hint(dst + plane * plane_elems + (int64_t)c.first * cell, out,
+                        (uint32_t)c.nout * cell * 8u, pol_stream);
+        else
+          bulk_s2g(dst + plane * plane_elems + (int64_t)c.first * cell, out,
+                   (uint32_t)c.nout * cell * 8u);
         bulk_commit();
       }
       if (prod_j < nchunks) issue_next();
