@@ -745,6 +745,8 @@ __global__ void __launch_bounds__(32 * kVCells)
   __syncthreads();
   const int qmax = s_qmax;
   const bool use_tma = (qmax - s_qmin) <= kVSpan - 1;
+  // source v1 cells the block needs: kVCells + 1 + (q1 spread) <= W
+  const int wcells = min(W, kVCells + 1 + (qmax - s_qmin));
   int wstart = c1a - qmax - 1;  // first window cell (mod C1)
   wstart %= C1;
   if (wstart < 0) wstart += C1;
@@ -776,9 +778,9 @@ __global__ void __launch_bounds__(32 * kVCells)
     const int s = k == C2 ? 0 : k;
     const int sl = k % kVStages;
     double* dstp = ring + sl * stage;
-    mbar_arrive_expect_tx(bars + sl, (uint32_t)stage * 8u);
+    mbar_arrive_expect_tx(bars + sl, (uint32_t)(wcells * P * P * 32) * 8u);
     int cell = wstart;
-    for (int w = 0; w < W; ++w) {  // one {32 x, P dofs, P rows} box per window cell
+    for (int w = 0; w < wcells; ++w) {  // one {32 x, P dofs, P rows} box per needed cell
       tma_load_3d(dstp + w * (P * P * 32), &tmap, (int)x0, cell * P, s * P, bars + sl);
       if (++cell == C1) cell = 0;
     }
