@@ -244,6 +244,16 @@ class CudaOps:
         L.check(self.lib.vpb_slab_copy(src.data_ptr(), src_stride, dst.data_ptr(), dst_stride,
                                        outer, run, self._device.stream()), "vpb_slab_copy")
 
+    def vplane(self, src, dst, dims, order, t1, t2, f1, f2):
+        """Both v sweeps of a shard in one pass (they are local in x)."""
+        L = self._lib
+        L.check(self.lib.vpb_dg_sweep_vplane(src.data_ptr(), dst.data_ptr(), L.dims(dims), order,
+                                             t1.a.data_ptr(), t1.b.data_ptr(), t1.q.data_ptr(),
+                                             t1.alpha.data_ptr(), t2.a.data_ptr(), t2.b.data_ptr(),
+                                             t2.q.data_ptr(), t2.alpha.data_ptr(), f1.data_ptr(),
+                                             f2.data_ptr(), self._device.stream()),
+                "vpb_dg_sweep_vplane")
+
     def pack(self, axis, f, dims, order, cell0, width, buf):
         L = self._lib
         L.check(self.lib.vpb_halo_pack(axis, f.data_ptr(), L.dims(dims), order, cell0, width,
@@ -490,12 +500,16 @@ class ShardedSolver:
         self._advect_space(tau, 0)  # x half (open); the x tables carry the tau/2
         self._gather_rho()
         self.ops.field_solve(self.grid, self.rho, self.e, self.stats, self.solve_flag)
-        for d in range(2):
-            axis = 2 + d
-            h = self.grid.axes[axis].h
-            for sh in self.shards.values():
-                tab = self.ops.tables(self._local_e(sh, d), tau, h, self.grid.dg_degree)
-                self.ops.sweep(axis, sh.f, sh.buf, sh.dims, self.order, tab,
+        for sh in self.shards.values():
+            tabs = [self.ops.tables(self._local_e(sh, d), tau, self.grid.axes[2 + d].h,
+                                    self.grid.dg_degree) for d in range(2)]
+            if hasattr(self.ops, "vplane"):  # v1 + v2 in one pass (local in x)
+                self.ops.vplane(sh.f, sh.buf, sh.dims, self.order, tabs[0], tabs[1],
+                                sh.flags[3:4], sh.flags[4:5])
+                sh.swap()
+                continue
+            for d in range(2):
+                self.ops.sweep(2 + d, sh.f, sh.buf, sh.dims, self.order, tabs[d],
                                sh.flags[3 + d:4 + d])
                 sh.swap()
         self._advect_space(tau, 5)
