@@ -21,6 +21,21 @@ __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a,
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 
+// acc + a*b in the fused step passes: two roundings, in the reference's
+// order (bitwise reproduction of its compiled kernels) unless the library is
+// built with -DVPB_STEP_FMA=1 (one rounding; an A/B experiment, not the
+// shipped configuration -- see DESIGN.md).
+#ifndef VPB_STEP_FMA
+#define VPB_STEP_FMA 0
+#endif
+__device__ __forceinline__ double step_madd(double acc, double a, double b) {
+#if VPB_STEP_FMA
+  return __fma_rn(a, b, acc);
+#else
+  return dadd(acc, dmul(a, b));
+#endif
+}
+
 // Python-style modulo into [0, n).
 __host__ __device__ __forceinline__ int64_t wrap_mod(int64_t v, int64_t n) {
   int64_t r = v % n;

@@ -628,10 +628,10 @@ __global__ void __launch_bounds__(32 * kVCells)
         } else {
           double acc_a = dmul(A1[j][0], ul[m2][0]);
 #pragma unroll
-          for (int m = 1; m < P; ++m) acc_a = dadd(acc_a, dmul(A1[j][m], ul[m2][m]));
+          for (int m = 1; m < P; ++m) acc_a = step_madd(acc_a, A1[j][m], ul[m2][m]);
           double acc_b = dmul(B1[j][0], uu[m2][0]);
 #pragma unroll
-          for (int m = 1; m < P; ++m) acc_b = dadd(acc_b, dmul(B1[j][m], uu[m2][m]));
+          for (int m = 1; m < P; ++m) acc_b = step_madd(acc_b, B1[j][m], uu[m2][m]);
           v = dadd(acc_a, acc_b);
         }
         g[m2][j] = v;
@@ -660,10 +660,10 @@ __global__ void __launch_bounds__(32 * kVCells)
         } else {
           double acc_a = dmul(A2[j2][0], gp[0][j]);
 #pragma unroll
-          for (int m = 1; m < P; ++m) acc_a = dadd(acc_a, dmul(A2[j2][m], gp[m][j]));
+          for (int m = 1; m < P; ++m) acc_a = step_madd(acc_a, A2[j2][m], gp[m][j]);
           double acc_b = dmul(B2[j2][0], g[0][j]);
 #pragma unroll
-          for (int m = 1; m < P; ++m) acc_b = dadd(acc_b, dmul(B2[j2][m], g[m][j]));
+          for (int m = 1; m < P; ++m) acc_b = step_madd(acc_b, B2[j2][m], g[m][j]);
           o = dadd(acc_a, acc_b);
         }
         e2.add(o);
@@ -831,10 +831,10 @@ __global__ void __launch_bounds__(32 * kVCells)
         } else {
           double acc_a = dmul(A1[j][0], ul[m2][0]);
 #pragma unroll
-          for (int m = 1; m < P; ++m) acc_a = dadd(acc_a, dmul(A1[j][m], ul[m2][m]));
+          for (int m = 1; m < P; ++m) acc_a = step_madd(acc_a, A1[j][m], ul[m2][m]);
           double acc_b = dmul(B1[j][0], uu[m2][0]);
 #pragma unroll
-          for (int m = 1; m < P; ++m) acc_b = dadd(acc_b, dmul(B1[j][m], uu[m2][m]));
+          for (int m = 1; m < P; ++m) acc_b = step_madd(acc_b, B1[j][m], uu[m2][m]);
           v = dadd(acc_a, acc_b);
         }
         g[m2][j] = v;
@@ -865,10 +865,10 @@ __global__ void __launch_bounds__(32 * kVCells)
         } else {
           double acc_a = dmul(A2[j2][0], gp[0][j]);
 #pragma unroll
-          for (int m = 1; m < P; ++m) acc_a = dadd(acc_a, dmul(A2[j2][m], gp[m][j]));
+          for (int m = 1; m < P; ++m) acc_a = step_madd(acc_a, A2[j2][m], gp[m][j]);
           double acc_b = dmul(B2[j2][0], g[0][j]);
 #pragma unroll
-          for (int m = 1; m < P; ++m) acc_b = dadd(acc_b, dmul(B2[j2][m], g[m][j]));
+          for (int m = 1; m < P; ++m) acc_b = step_madd(acc_b, B2[j2][m], g[m][j]);
           o = dadd(acc_a, acc_b);
         }
         eo.add(o);

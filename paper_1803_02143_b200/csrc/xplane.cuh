@@ -95,10 +95,10 @@ __device__ __forceinline__ void xplane_x1_cell(const double* rows, int n1, int l
       for (int jj = 0; jj < P; ++jj) {
         double acc_a = dmul(A1[jj][0], ul[0]);
 #pragma unroll
-        for (int m = 1; m < P; ++m) acc_a = dadd(acc_a, dmul(A1[jj][m], ul[m]));
+        for (int m = 1; m < P; ++m) acc_a = step_madd(acc_a, A1[jj][m], ul[m]);
         double acc_b = dmul(B1[jj][0], uu[0]);
 #pragma unroll
-        for (int m = 1; m < P; ++m) acc_b = dadd(acc_b, dmul(B1[jj][m], uu[m]));
+        for (int m = 1; m < P; ++m) acc_b = step_madd(acc_b, B1[jj][m], uu[m]);
         g[m2][jj] = dadd(acc_a, acc_b);
       }
     }
@@ -120,10 +120,10 @@ __device__ __forceinline__ void xplane_x2_cell(const double (&A2)[P][P], const d
       } else {
         double acc_a = dmul(A2[j2][0], gp[0][jj]);
 #pragma unroll
-        for (int m = 1; m < P; ++m) acc_a = dadd(acc_a, dmul(A2[j2][m], gp[m][jj]));
+        for (int m = 1; m < P; ++m) acc_a = step_madd(acc_a, A2[j2][m], gp[m][jj]);
         double acc_b = dmul(B2[j2][0], g[0][jj]);
 #pragma unroll
-        for (int m = 1; m < P; ++m) acc_b = dadd(acc_b, dmul(B2[j2][m], g[m][jj]));
+        for (int m = 1; m < P; ++m) acc_b = step_madd(acc_b, B2[j2][m], g[m][jj]);
         o[j2][jj] = dadd(acc_a, acc_b);
       }
     }
