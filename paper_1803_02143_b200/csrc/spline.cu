@@ -77,7 +77,8 @@ static int get_factors(int64_t n, const double** out) {
     *out = it->second;
     return VPB_OK;
   }
-  const int64_t len = 4 * n + 8 + kPcrLevels;
+  // [mult | denom | rden | z | 8 scalars | PCR k_l, 6/b_L | z1^k, k = 0..n]
+  const int64_t len = 5 * n + 9 + kPcrLevels;
   double* h = new double[len];
   double sden;
   host_factors(n, h, h + n, h + 3 * n, &sden);
@@ -116,6 +117,14 @@ static int get_factors(int64_t n, const double** out) {
     }
     const bool wraps = ((1LL << kPcrLevels) % n) == 0;
     h[4 * n + 7 + kPcrLevels] = 6.0 / (wraps ? pb + 2.0 * pa : pb);
+  }
+  {  // powers of the recursive-filter pole z1 = sqrt(3) - 2 (spline_rows_kernel)
+    const double z1 = std::sqrt(3.0) - 2.0;
+    double pz = 1.0;
+    for (int64_t k = 0; k <= n; ++k) {
+      h[4 * n + 8 + kPcrLevels + k] = pz;
+      pz *= z1;
+    }
   }
   double* d = nullptr;
   if (cudaMalloc(&d, len * sizeof(double)) != cudaSuccess ||
@@ -486,6 +495,164 @@ __global__ void __launch_bounds__(kSplineT)
   report_flag(bad, a.flag);
 }
 
+// Contiguous-axis spline sweep with the line spread over a warp: lane L
+// holds points NPT*L .. NPT*L+NPT-1 in registers (one coalesced load per
+// line).  The periodic system w_{i-1} + 4 w_i + w_{i+1} = 6 u_i is solved with
+// the cubic-B-spline recursive filters (pole z1 = sqrt(3) - 2):
+//   causal      y+_k = u_k + z1 y+_{k-1},   anticausal  y_k = y+_k + z1 y_{k+1},
+//   w = -6 z1 y  (6/(z + 4 + 1/z) = -6 z1 / ((1 - z1/z)(1 - z1 z))),
+// each as a local recurrence over the lane's points plus a 5-step
+// Kogge-Stone scan of the lane carries (multiplier z1^NPT) and the periodic
+// wrap term z1^(k+1) y+_{n-1} (exact to z1^n <= 5e-19, below rounding).
+// The evaluation (_kernels.pyx:62-93) reads w from a per-warp shared row
+// with lanes along consecutive outputs, so loads and stores are coalesced.
+// Same system as the Thomas + Sherman-Morrison solve (_kernels.pyx:37-59) to
+// round-off; replaces the shared-memory tile (one line per lane), whose
+// five PCR passes were shared-memory bound at 6 warps per SM.
+constexpr int kRowWarps = 8;
+
+// Evaluation weights of one line (_kernels.pyx:62-87), the gain g folded in.
+__device__ __forceinline__ void spline_eval_weights(const SplineTileArgs& a, int64_t L, int n,
+                                                    double g, double (&w)[4], int& j0) {
+  const int64_t trow = a.idx ? a.idx[L] : (L / a.tdiv) % a.tmod;
+  const double shift = __dmul_rn(a.values[trow], a.scale);
+  const double sh = __ddiv_rn(shift, a.h);
+  double off = floor(-sh);
+  double th = __dsub_rn(-sh, off);
+  if (th >= 1.0) {
+    off = __dadd_rn(off, 1.0);
+    th = 0.0;
+  }
+  const double omt = __dsub_rn(1.0, th);
+  w[0] = g * __ddiv_rn(__dmul_rn(__dmul_rn(omt, omt), omt), 6.0);
+  w[1] = g * __ddiv_rn(__dadd_rn(__dsub_rn(4.0, __dmul_rn(__dmul_rn(6.0, th), th)),
+                                 __dmul_rn(__dmul_rn(__dmul_rn(3.0, th), th), th)),
+                       6.0);
+  w[2] = g * __ddiv_rn(__dadd_rn(__dsub_rn(4.0, __dmul_rn(__dmul_rn(6.0, omt), omt)),
+                                 __dmul_rn(__dmul_rn(__dmul_rn(3.0, omt), omt), omt)),
+                       6.0);
+  w[3] = g * __ddiv_rn(__dmul_rn(__dmul_rn(th, th), th), 6.0);
+  j0 = (int)wrap_mod((int64_t)off - 1, n);
+}
+
+template <int NPT>
+__global__ void __launch_bounds__(32 * kRowWarps)
+    spline_rows_kernel(SplineTileArgs a) {
+  constexpr int n = 32 * NPT;
+  __shared__ double wrow[kRowWarps][n + 4];  // + wrap copies of points 0..3
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* zp = a.fac + 4 * n + 8 + kPcrLevels;  // z1^k
+  const double z1 = zp[1];
+  const double g = -6.0 * z1;
+  double mj[5];  // z1^(NPT 2^j)
+#pragma unroll
+  for (int j = 0; j < 5; ++j) mj[j] = zp[NPT << j];
+  double zr[NPT + 1];
+#pragma unroll
+  for (int r = 0; r <= NPT; ++r) zr[r] = zp[r];
+  const double zin = zp[NPT * lane];             // z1^(NPT L): wrap into lane L's carry-in
+  const double zout = zp[n - NPT * (lane + 1)];  // z1^(n - NPT(L+1))
+  ExpMax em;
+  const int64_t L0 = (int64_t)blockIdx.x * kRowWarps + warp;
+  const int64_t Lstep = (int64_t)gridDim.x * kRowWarps;
+  auto load_line = [&](int64_t L, double (&v)[NPT]) {
+    if (L >= a.nlines) return;
+    const double* src = a.src + L * n + NPT * lane;
+    if constexpr (NPT % 2 == 0) {
+#pragma unroll
+      for (int r = 0; r < NPT; r += 2) {
+        const double2 t = __ldcs(reinterpret_cast<const double2*>(src + r));
+        v[r] = t.x;
+        v[r + 1] = t.y;
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < NPT; ++r) v[r] = __ldcs(src + r);
+    }
+  };
+  // the weights of the warp's next 32 lines: lane t holds line (k + t)'s
+  double wl[4] = {0.0, 0.0, 0.0, 0.0};
+  int jl = 0;
+  double nxt[NPT];
+  load_line(L0, nxt);
+  int k = 0;
+  for (int64_t L = L0; L < a.nlines; L += Lstep, ++k) {
+    if ((k & 31) == 0) {
+      const int64_t Lw = L + lane * Lstep;
+      if (Lw < a.nlines) spline_eval_weights(a, Lw, n, g, wl, jl);
+    }
+    double x[NPT];
+#pragma unroll
+    for (int r = 0; r < NPT; ++r) x[r] = nxt[r];
+    load_line(L + Lstep, nxt);  // next line's loads fly while this one is solved
+    // ---- causal filter
+#pragma unroll
+    for (int r = 1; r < NPT; ++r) x[r] = fma(z1, x[r - 1], x[r]);
+    double X = x[NPT - 1];
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const double t = __shfl_up_sync(0xffffffffu, X, 1 << j);
+      if (lane >= (1 << j)) X = fma(mj[j], t, X);
+    }
+    const double W = __shfl_sync(0xffffffffu, X, 31);  // y+_{n-1} (periodic)
+    double E = __shfl_up_sync(0xffffffffu, X, 1);
+    E = lane == 0 ? W : fma(zin, W, E);
+#pragma unroll
+    for (int r = 0; r < NPT; ++r) x[r] = fma(zr[r + 1], E, x[r]);
+    // ---- anticausal filter
+#pragma unroll
+    for (int r = NPT - 2; r >= 0; --r) x[r] = fma(z1, x[r + 1], x[r]);
+    double Y = x[0];
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const double t = __shfl_down_sync(0xffffffffu, Y, 1 << j);
+      if (lane + (1 << j) < 32) Y = fma(mj[j], t, Y);
+    }
+    const double V = __shfl_sync(0xffffffffu, Y, 0);  // y_0 (periodic)
+    double F = __shfl_down_sync(0xffffffffu, Y, 1);
+    F = lane == 31 ? V : fma(zout, V, F);
+#pragma unroll
+    for (int r = 0; r < NPT; ++r) x[r] = fma(zr[NPT - r], F, x[r]);
+    // ---- w (the -6 z1 gain is folded into the evaluation weights)
+    double* row = wrow[warp];
+    if constexpr (NPT % 2 == 0) {
+#pragma unroll
+      for (int r = 0; r < NPT; r += 2)
+        *reinterpret_cast<double2*>(row + NPT * lane + r) = make_double2(x[r], x[r + 1]);
+    } else {
+#pragma unroll
+      for (int r = 0; r < NPT; ++r) row[NPT * lane + r] = x[r];
+    }
+    if (lane < (4 + NPT - 1) / NPT)  // wrap copies row[n + i] = row[i], i < 4
+#pragma unroll
+      for (int r = 0; r < NPT; ++r)
+        if (NPT * lane + r < 4) row[n + NPT * lane + r] = x[r];
+    __syncwarp();
+    // ---- evaluation: out_i = w0 w[j0+i] + w1 w[j0+i+1] + w2 w[j0+i+2] + w3 w[j0+i+3]
+    const int src_lane = k & 31;
+    const double w0 = __shfl_sync(0xffffffffu, wl[0], src_lane);
+    const double w1 = __shfl_sync(0xffffffffu, wl[1], src_lane);
+    const double w2 = __shfl_sync(0xffffffffu, wl[2], src_lane);
+    const double w3 = __shfl_sync(0xffffffffu, wl[3], src_lane);
+    const int j0 = __shfl_sync(0xffffffffu, jl, src_lane);
+    double* dst = a.dst + L * n;
+#pragma unroll
+    for (int r = 0; r < NPT; ++r) {
+      const int i = lane + 32 * r;
+      int q = j0 + i;
+      if (q >= n) q -= n;
+      double o = __dmul_rn(w0, row[q]);
+      o = __dadd_rn(o, __dmul_rn(w1, row[q + 1]));
+      o = __dadd_rn(o, __dmul_rn(w2, row[q + 2]));
+      o = __dadd_rn(o, __dmul_rn(w3, row[q + 3]));
+      em.add(o);
+      __stcs(dst + i, o);
+    }
+    __syncwarp();  // the row is rewritten by the next line
+  }
+  report_flag(em.bad(), a.flag);
+}
+
 static size_t spline_smem(int n, bool contig) {
   const size_t tile = contig ? (size_t)kSplineT * contig_rs(n) : (size_t)n * kSplineT;
   return ((tile + 4 * kSplineT) * 8 + kSplineT * 4 + 7) / 8 * 8 + kSplineBars * 8;
@@ -529,6 +696,21 @@ static int launch_spline(SplineTileArgs a, bool contig, bool exact, cudaStream_t
                                (uint32_t)std::min(a.n, 256), 1)
                     ? 1
                     : 0;
+  }
+  static const bool no_rows = getenv("VPB_SPLINE_TILES") != nullptr;
+  const int npt = a.n / 32;
+  if (contig && pcr && !no_rows && a.n % 32 == 0 && (npt == 1 || npt == 2 || npt == 4 ||
+                                                      npt == 8) &&
+      (reinterpret_cast<uintptr_t>(a.src) & 15) == 0) {
+    const int64_t want = (a.nlines + kRowWarps - 1) / kRowWarps;
+    const unsigned rblocks = (unsigned)std::min<int64_t>(want, 148 * 8);
+    switch (npt) {
+      case 1: spline_rows_kernel<1><<<rblocks, 32 * kRowWarps, 0, st>>>(a); break;
+      case 2: spline_rows_kernel<2><<<rblocks, 32 * kRowWarps, 0, st>>>(a); break;
+      case 4: spline_rows_kernel<4><<<rblocks, 32 * kRowWarps, 0, st>>>(a); break;
+      default: spline_rows_kernel<8><<<rblocks, 32 * kRowWarps, 0, st>>>(a); break;
+    }
+    return launched("spline_rows_kernel");
   }
   if (contig) {
     if (pcr)

@@ -292,8 +292,9 @@ def test_poisson_dg_coupling_single_mode_1d():
     assert np.abs(e.components[0].cpu().numpy() - np.sin(0.5 * x)).max() <= 1e-11
 
 
-@pytest.mark.parametrize("axis", [0, 1, 2, 3])
-@pytest.mark.parametrize("dofs", [(32, 64, 48, 128), (128, 32, 64, 48)])
+@pytest.mark.parametrize("axis,dofs", [
+    (a, d) for a in (0, 1, 2, 3) for d in ((32, 64, 48, 128), (128, 32, 64, 48))]
+    + [(0, (64, 16, 8, 8)), (0, (256, 8, 8, 4)), (0, (96, 16, 8, 4))])
 def test_spline_pcr_axis_sweep_matches_reference_solver(axis, dofs):
     """Product spline sweeps use parallel cyclic reduction when the line length
     allows (n % 16 == 0, n >= 32); they agree with the reference's Thomas +
