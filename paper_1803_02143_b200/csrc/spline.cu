@@ -161,6 +161,7 @@ struct SplineTileArgs {
   const double* fac;
   int32_t* flag;
   int use_tma;  // strided tiles: one TMA tensor copy per tile (tmap valid)
+  int iir;      // fast path: recursive filters (n % 8 == 0, n >= 32) instead of PCR
 };
 
 constexpr int kSplineBars = 8;  // row groups with their own mbarrier (strided tiles)
@@ -211,6 +212,56 @@ __device__ __forceinline__ void pcr_level(double* y, const int YS, const int n, 
     for (int r = 0; r < S; ++r) ring[r] = c[B - S + r];
 #pragma unroll
     for (int r = 0; r < B; ++r) y[(i0 + r) * YS] = o[r];
+  }
+}
+
+// The same periodic solve as spline_rows_kernel, one line per lane, serial
+// along the line in shared memory: causal then anticausal recursive filter
+// (pole z1), each started from its periodic value summed over the 32 points
+// that wrap into it (z1^32 ~ 5e-19).  Five shared-memory accesses per point
+// instead of the eleven of five PCR levels.  Requires n >= 32.  Leaves
+// y = w / g with g = -6 z1.
+__device__ __forceinline__ void iir_solve(double* y, const int YS, const int n, const double z1) {
+  constexpr int U = 8;
+  double p = 0.0;
+  for (int k = n - 32; k < n; k += U) {  // y+_{n-1}, periodic
+    double u[U];
+#pragma unroll
+    for (int r = 0; r < U; ++r) u[r] = y[(k + r) * YS];
+#pragma unroll
+    for (int r = 0; r < U; ++r) p = fma(z1, p, u[r]);
+  }
+  for (int k = 0; k < n; k += U) {  // causal: y+_k = u_k + z1 y+_{k-1}
+    double u[U];
+#pragma unroll
+    for (int r = 0; r < U; ++r) u[r] = y[(k + r) * YS];
+#pragma unroll
+    for (int r = 0; r < U; ++r) {
+      p = fma(z1, p, u[r]);
+      u[r] = p;
+    }
+#pragma unroll
+    for (int r = 0; r < U; ++r) y[(k + r) * YS] = u[r];
+  }
+  double q = 0.0;
+  for (int k = 32 - U; k >= 0; k -= U) {  // y_0, periodic
+    double u[U];
+#pragma unroll
+    for (int r = 0; r < U; ++r) u[r] = y[(k + r) * YS];
+#pragma unroll
+    for (int r = U - 1; r >= 0; --r) q = fma(z1, q, u[r]);
+  }
+  for (int k = n - U; k >= 0; k -= U) {  // anticausal: y_k = y+_k + z1 y_{k+1}
+    double u[U];
+#pragma unroll
+    for (int r = 0; r < U; ++r) u[r] = y[(k + r) * YS];
+#pragma unroll
+    for (int r = U - 1; r >= 0; --r) {
+      q = fma(z1, q, u[r]);
+      u[r] = q;
+    }
+#pragma unroll
+    for (int r = 0; r < U; ++r) y[(k + r) * YS] = u[r];
   }
 }
 
@@ -311,12 +362,18 @@ __global__ void __launch_bounds__(kSplineT)
       if (bulk)
         for (int bb = 0; bb < nbars; ++bb) mbar_wait(bars + bb, 0);
       const double* pk = a.fac + 4 * n + 7;
-      pcr_level<1>(y, YS, n, pk[0]);
-      pcr_level<2>(y, YS, n, pk[1]);
-      pcr_level<4>(y, YS, n, pk[2]);
-      pcr_level<8>(y, YS, n, pk[3]);
-      pcr_level<16>(y, YS, n, pk[4]);
-      wscale = pk[kPcrLevels];  // 6 / b_L: folded into the evaluation weights
+      if (a.iir) {
+        const double z1 = pk[kPcrLevels + 2];  // z1^1 of the power table
+        iir_solve(y, YS, n, z1);
+        wscale = -6.0 * z1;
+      } else {
+        pcr_level<1>(y, YS, n, pk[0]);
+        pcr_level<2>(y, YS, n, pk[1]);
+        pcr_level<4>(y, YS, n, pk[2]);
+        pcr_level<8>(y, YS, n, pk[3]);
+        pcr_level<16>(y, YS, n, pk[4]);
+        wscale = pk[kPcrLevels];  // 6 / b_L: folded into the evaluation weights
+      }
     } else {
     // Forward elimination y_i = 6u_i - mult_i*y_{i-1}, in blocks of U points:
     // the U loads are issued before the dependent chain so only the two
@@ -683,7 +740,9 @@ static int launch_spline(SplineTileArgs a, bool contig, bool exact, cudaStream_t
     attr = true;
   }
   static const bool force_exact = getenv("VPB_SPLINE_EXACT") != nullptr;
+  static const bool force_pcr = getenv("VPB_SPLINE_PCR") != nullptr;
   const bool pcr = !exact && !force_exact && a.n % 16 == 0 && a.n >= 32;
+  a.iir = pcr && !force_pcr ? 1 : 0;
   int64_t blocks = (a.nlines + kSplineT - 1) / kSplineT;
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
