@@ -182,6 +182,38 @@ int vpb_dg_sweep_xplane2_density(const double* src, double* dst, const int64_t d
                                  const double* wcell2_host, double volume, double* work,
                                  double* rc_out, double* stats, void* stream);
 
+/* Composed tables for two same-table sweeps along one axis: out[t] =
+ * {A A, A B + B A, B B} (row-major p x p each, fused multiply-adds), i.e.
+ * _kernels.pyx:113-123 applied twice as one three-cell stencil
+ * out[c] = AA u[c-2q-2] + (AB+BA) u[c-2q-1] + BB u[c-2q].  a, b: DEVICE
+ * [n][p][p] from vpb_dg_tables; out: DEVICE [n][3][p][p]. */
+int vpb_dg_compose_tables(const double* a, const double* b, int64_t n, int32_t order,
+                          double* out, void* stream);
+
+/* The merged x half steps of vpb_dg_sweep_xplane2 (closing x1 x2 of a Strang
+ * step + opening x1 x2 of the next, driver.py:245-265 / 371-377) with
+ * composed stencils: x1 x2 x1 x2 = (x1 x1)(x2 x2) applied as one three-cell
+ * stencil per axis (k1 / k2 from vpb_dg_compose_tables; q / alpha from
+ * vpb_dg_tables: alpha == 0 rows stay exact copies from cell c-2q).  Equal
+ * to vpb_dg_sweep_xplane2 up to round-off ("fast" arithmetic mode).  flag:
+ * any non-finite output (or NULL). */
+int vpb_dg_sweep_xcomp(const double* src, double* dst, const int64_t dims[4], int32_t order,
+                       const double* k1, const int64_t* q1, const double* alpha1,
+                       const double* k2, const int64_t* q2, const double* alpha2, int32_t* flag,
+                       void* stream);
+
+/* vpb_dg_sweep_xcomp with the density epilogue of vpb_dg_sweep_xplane_density
+ * on its output (work: vpb_dg_xcomp_density_work_len doubles). */
+int64_t vpb_dg_xcomp_density_work_len(const int64_t dims[4], int32_t order);
+int vpb_dg_sweep_xcomp_density(const double* src, double* dst, const int64_t dims[4],
+                               int32_t order, const double* k1, const int64_t* q1,
+                               const double* alpha1, const double* k2, const int64_t* q2,
+                               const double* alpha2, int32_t* flag, const double* wv1,
+                               const double* wv2, const double* mid_host,
+                               const double* wcell1_host, const double* wcell2_host,
+                               double volume, double* work, double* rc_out, double* stats,
+                               void* stream);
+
 /* One spline sweep along `axis`; shift of line = values[table row]*scale. */
 int vpb_spline_sweep_axis(int32_t axis, const double* src, double* dst, const int64_t dims[4],
                           const double* values, double scale, double h, int32_t* flag,

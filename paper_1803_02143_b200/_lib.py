@@ -85,6 +85,12 @@ SIGNATURES = {
     "vpb_dg_xplane2_density_work_len": (c_int64, [POINTER(c_int64), c_int32]),
     "vpb_dg_sweep_xplane2_density": (c_int, [c_void_p, c_void_p, POINTER(c_int64), c_int32]
                                      + [c_void_p] * 17 + [c_double] + [c_void_p] * 4),
+    "vpb_dg_compose_tables": (c_int, [c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p]),
+    "vpb_dg_sweep_xcomp": (c_int, [c_void_p, c_void_p, POINTER(c_int64), c_int32]
+                           + [c_void_p] * 8),
+    "vpb_dg_xcomp_density_work_len": (c_int64, [POINTER(c_int64), c_int32]),
+    "vpb_dg_sweep_xcomp_density": (c_int, [c_void_p, c_void_p, POINTER(c_int64), c_int32]
+                                   + [c_void_p] * 12 + [c_double] + [c_void_p] * 4),
     "vpb_slab_copy": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, c_void_p]),
     "vpb_spline_sweep_axis": (c_int, [c_int32, c_void_p, c_void_p, POINTER(c_int64), c_void_p,
                                       c_double, c_double, c_void_p, c_void_p]),

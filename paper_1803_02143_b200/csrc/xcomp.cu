@@ -1,0 +1,453 @@
+// Merged x half steps with composed stencils (the "fast" arithmetic mode).
+//
+// Between two Strang steps the reference applies x1(τ/2) x2(τ/2) (closing
+// half step of step m, driver.py:262-265) and then x1(τ/2) x2(τ/2) again
+// (opening half step of step m+1, driver.py:257-258), with the same tables
+// (run loop driver.py:371-377).  Each sweep is the projection
+//     out[c] = A u[c-q-1] + B u[c-q]              (_kernels.pyx:113-123)
+// so two sweeps along one axis are the three-cell stencil
+//     out[c] = AA u[c-2q-2] + (AB+BA) u[c-2q-1] + BB u[c-2q]
+// -- both projections are kept (this is (P T)(P T), not the P T_τ merge
+// SURVEY.md §8f rules out), only the matrix products are formed once per
+// table row.  x1 and x2 act on different indices of a (v1, v2) plane, so
+// x1 x2 x1 x2 = (x1 x1)(x2 x2) exactly in real arithmetic; the pass applies
+// the composed x1 stencil and then the composed x2 stencil while the plane
+// streams through shared memory.  Per dof that is 2 x 3P fused multiply-adds
+// instead of 4 x (4P-1) separately rounded operations of the bitwise chain
+// (fused2.cu), so the pass is HBM-bound instead of fp64-issue bound.  The
+// result differs from the bitwise chain by round-off only (≈1e-16 relative
+// per step; tests hold it to the 1e-12 per-step bar against the oracle).
+//
+// alpha == 0 rows (exact shifts, dg.py:130-132: A = 0, B = I) stay exact
+// copies: out[c] = u[c-2q].
+//
+// Streaming along x2 (per plane, source order from s0 = -2(q2+1) mod C2):
+// C2+2 source cells t = 0, 1, ..., C2+1 arrive in chunks of G cells through an
+// mbarrier ring of 1-D bulk copies; thread c = x1 cell c applies the composed
+// x1 stencil to source cell t (3 x1 cells of each of its P rows), keeps the
+// last two results in registers, and from t = 2 on emits output x2 cell t-2
+// (streaming stores), optionally with the density epilogue of xplane.cuh.
+#include <algorithm>
+#include <cstdlib>
+#include <type_traits>
+
+#include "async_copy.cuh"
+#include "common.cuh"
+#include "xplane.cuh"
+
+namespace vpb {
+
+// out[t][0] = A A, out[t][1] = A B + B A, out[t][2] = B B  (row-major P x P)
+__global__ void compose_tables_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                                      int64_t T, int P, double* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t pp = (int64_t)P * P;
+  if (e >= T * pp) return;
+  const int64_t t = e / pp;
+  const int j = (int)((e / P) % P), m = (int)(e % P);
+  const double* A = a + t * pp;
+  const double* B = b + t * pp;
+  double c0 = 0.0, c1 = 0.0, c2 = 0.0;
+  for (int k = 0; k < P; ++k) {
+    c0 = fma(A[j * P + k], A[k * P + m], c0);
+    c1 = fma(A[j * P + k], B[k * P + m], c1);
+    c1 = fma(B[j * P + k], A[k * P + m], c1);
+    c2 = fma(B[j * P + k], B[k * P + m], c2);
+  }
+  double* o = out + t * 3 * pp + j * P + m;
+  o[0] = c0;
+  o[pp] = c1;
+  o[2 * pp] = c2;
+}
+
+template <int P>
+__device__ __forceinline__ void load_cell_row(const double* p, double (&u)[P]) {
+  lds_row_cell<P>(p, u);
+}
+
+template <int P, bool DENS>
+__global__ void __launch_bounds__(128)
+    dg_xcomp_kernel(const double* __restrict__ src, double* __restrict__ dst, int n1, int C2,
+                    int G, int nst, int64_t nv1, int64_t nplanes, int64_t planes_per_block,
+                    const double* __restrict__ k1, const int64_t* __restrict__ q1,
+                    const double* __restrict__ al1, const double* __restrict__ k2,
+                    const int64_t* __restrict__ q2, const double* __restrict__ al2,
+                    int32_t* __restrict__ flag, const XDensity dn) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int cell = P * n1;  // one x2 cell: P rows of n1 dofs
+  const int slot = G * cell;
+  double* inb = reinterpret_cast<double*>(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(inb + nst * slot);
+
+  const int tid = threadIdx.x;
+  const int64_t pl_begin = blockIdx.x * planes_per_block;
+  const int64_t pl_end = min(nplanes, pl_begin + planes_per_block);
+  if (pl_begin >= pl_end) return;
+  const int L = C2 + 2;  // source cells per plane
+  const int per_plane = (L + G - 1) / G;
+  const int64_t nchunks = (pl_end - pl_begin) * per_plane;
+  const int64_t plane_elems = (int64_t)C2 * cell;
+  const uint64_t pol_stream = l2_evict_first();
+  const uint64_t pol_keep = l2_evict_last();
+
+  auto s0_of = [&](int64_t pl) { return (int)wrap_mod(-2 * (q2[pl / nv1] + 1), C2); };
+  // producer (thread 0)
+  int64_t p_plane = pl_begin;
+  int p_k = 0, p_s0 = 0, p_st = 0;
+  int64_t prod_j = 0;
+  auto issue_next = [&]() {
+    const int t0 = p_k * G;
+    const int ns = min(G, L - t0);
+    int sb = p_s0 + t0;
+    while (sb >= C2) sb -= C2;
+    const double* base = src + p_plane * plane_elems;
+    double* d = inb + p_st * slot;
+    mbar_arrive_expect_tx(bars + p_st, (uint32_t)ns * cell * 8u);
+    const int run1 = min(ns, C2 - sb);
+    if (DENS)
+      bulk_g2s_hint(d, base + (int64_t)sb * cell, (uint32_t)run1 * cell * 8u, bars + p_st,
+                    pol_stream);
+    else
+      bulk_g2s(d, base + (int64_t)sb * cell, (uint32_t)run1 * cell * 8u, bars + p_st);
+    if (run1 < ns) {  // wrapped: the rest starts at source cell 0
+      if (DENS)
+        bulk_g2s_hint(d + run1 * cell, base, (uint32_t)(ns - run1) * cell * 8u, bars + p_st,
+                      pol_stream);
+      else
+        bulk_g2s(d + run1 * cell, base, (uint32_t)(ns - run1) * cell * 8u, bars + p_st);
+    }
+    ++prod_j;
+    if (++p_st == nst) p_st = 0;
+    if (++p_k == per_plane) {
+      p_k = 0;
+      if (++p_plane < pl_end) p_s0 = s0_of(p_plane);
+    }
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < nst; ++s) mbar_init(bars + s, 1);
+    fence_mbar_init();
+    p_s0 = s0_of(pl_begin);
+  }
+  __syncthreads();
+  if (tid == 0)
+    while (prod_j < nst && prod_j < nchunks) issue_next();
+
+  const int C1 = n1 / P;
+  const bool active = tid < C1;
+  double T1[3][P][P], T2[3][P][P];
+  bool ex1 = true, ex2 = true;
+  int off0 = 0, off1 = 0, off2 = 0;  // element offsets of the three x1 source cells
+  double w0[P][P], w1[P][P];         // x1 results of source cells t-2, t-1
+  bool bad = false;
+  int st = 0;
+  uint32_t phase = 0;
+  int k = 0;  // chunk index inside the plane
+  int64_t plane = pl_begin;
+  double wplane = 0.0, meanacc = 0.0;
+  double* mypart = DENS ? dn.rc_part + (int64_t)blockIdx.x * C2 * C1 : nullptr;
+  if (DENS && active)
+    for (int c2 = 0; c2 < C2; ++c2) mypart[c2 * C1 + tid] = 0.0;
+
+  for (int64_t j = 0; j < nchunks; ++j) {
+    if (active && k == 0) {
+      const int64_t iv2 = plane / nv1, iv1 = plane - iv2 * nv1;
+      if (DENS) wplane = dn.wv1[iv1] * dn.wv2[iv2];
+      ex1 = (al1[iv1] == 0.0);
+      ex2 = (al2[iv2] == 0.0);
+#pragma unroll
+      for (int s = 0; s < 3; ++s)
+#pragma unroll
+        for (int jj = 0; jj < P; ++jj)
+#pragma unroll
+          for (int m = 0; m < P; ++m) {
+            T1[s][jj][m] = __ldg(k1 + (iv1 * 3 + s) * P * P + jj * P + m);
+            T2[s][jj][m] = __ldg(k2 + (iv2 * 3 + s) * P * P + jj * P + m);
+          }
+      const int qq = (int)wrap_mod(2 * q1[iv1], C1);
+      int lo = tid - qq - 2;
+      while (lo < 0) lo += C1;
+      const int mid = lo + 1 == C1 ? 0 : lo + 1;
+      const int up = mid + 1 == C1 ? 0 : mid + 1;
+      off0 = lo * P;
+      off1 = mid * P;
+      off2 = up * P;
+    }
+    const int t0 = k * G;
+    const int ns = min(G, L - t0);
+    mbar_wait(bars + st, phase);
+    const double* in = inb + st * slot;
+    double* outp = dst + plane * plane_elems;
+
+    auto run = [&](auto ex1c, auto ex2c) {
+      constexpr bool E1 = decltype(ex1c)::value, E2 = decltype(ex2c)::value;
+      for (int sc = 0; sc < ns; ++sc) {
+        const int t = t0 + sc;
+        const double* rows = in + sc * cell;
+        double g[P][P];
+        // composed x1 stencil on this source x2 cell: g[m2][jj]
+#pragma unroll
+        for (int m2 = 0; m2 < P; ++m2) {
+          const double* row = rows + m2 * n1;
+          double u2[P];
+          load_cell_row<P>(row + off2, u2);
+          if constexpr (E1) {
+#pragma unroll
+            for (int jj = 0; jj < P; ++jj) g[m2][jj] = u2[jj];
+          } else {
+            double u0[P], u1[P];
+            load_cell_row<P>(row + off0, u0);
+            load_cell_row<P>(row + off1, u1);
+#pragma unroll
+            for (int jj = 0; jj < P; ++jj) {
+              double acc = T1[0][jj][0] * u0[0];
+#pragma unroll
+              for (int m = 1; m < P; ++m) acc = fma(T1[0][jj][m], u0[m], acc);
+#pragma unroll
+              for (int m = 0; m < P; ++m) acc = fma(T1[1][jj][m], u1[m], acc);
+#pragma unroll
+              for (int m = 0; m < P; ++m) acc = fma(T1[2][jj][m], u2[m], acc);
+              g[m2][jj] = acc;
+            }
+          }
+        }
+        if (t >= 2) {
+          double o[P][P];
+#pragma unroll
+          for (int j2 = 0; j2 < P; ++j2)
+#pragma unroll
+            for (int jj = 0; jj < P; ++jj) {
+              if constexpr (E2) {
+                o[j2][jj] = g[j2][jj];
+              } else {
+                double acc = T2[0][j2][0] * w0[0][jj];
+#pragma unroll
+                for (int m = 1; m < P; ++m) acc = fma(T2[0][j2][m], w0[m][jj], acc);
+#pragma unroll
+                for (int m = 0; m < P; ++m) acc = fma(T2[1][j2][m], w1[m][jj], acc);
+#pragma unroll
+                for (int m = 0; m < P; ++m) acc = fma(T2[2][j2][m], g[m][jj], acc);
+                o[j2][jj] = acc;
+              }
+            }
+          ExpMax eo;
+          const int oc = t - 2;
+          double* ot = outp + (int64_t)oc * cell + tid * P;
+#pragma unroll
+          for (int j2 = 0; j2 < P; ++j2) {
+#pragma unroll
+            for (int jj = 0; jj < P; ++jj) eo.add(o[j2][jj]);
+            if constexpr (P % 2 == 0) {
+#pragma unroll
+              for (int jj = 0; jj < P; jj += 2)
+                __stcs(reinterpret_cast<double2*>(ot + j2 * n1 + jj),
+                       make_double2(o[j2][jj], o[j2][jj + 1]));
+            } else {
+#pragma unroll
+              for (int jj = 0; jj < P; ++jj) __stcs(ot + j2 * n1 + jj, o[j2][jj]);
+            }
+          }
+          bad |= eo.bad();
+          if constexpr (DENS) {
+            double rcv, mv = 0.0;
+            if constexpr (P % 2 == 1) {
+              rcv = o[P / 2][P / 2];  // mid = e_centre exactly (checked on the host)
+            } else {
+              rcv = 0.0;
+#pragma unroll
+              for (int j2 = 0; j2 < P; ++j2)
+#pragma unroll
+                for (int jj = 0; jj < P; ++jj) rcv = fma(dn.mm[j2 * P + jj], o[j2][jj], rcv);
+            }
+#pragma unroll
+            for (int j2 = 0; j2 < P; ++j2)
+#pragma unroll
+              for (int jj = 0; jj < P; ++jj) mv = fma(dn.ww[j2 * P + jj], o[j2][jj], mv);
+            red_add_hint(mypart + oc * C1 + tid, dmul(wplane, rcv), pol_keep);
+            meanacc = fma(wplane, mv, meanacc);
+          }
+        }
+#pragma unroll
+        for (int m2 = 0; m2 < P; ++m2)
+#pragma unroll
+          for (int jj = 0; jj < P; ++jj) {
+            w0[m2][jj] = w1[m2][jj];
+            w1[m2][jj] = g[m2][jj];
+          }
+      }
+    };
+    if (active) {
+      using F = std::false_type;
+      using T = std::true_type;
+      if (!ex1 && !ex2) run(F{}, F{});
+      else if (!ex1) run(F{}, T{});
+      else if (!ex2) run(T{}, F{});
+      else run(T{}, T{});
+    }
+    __syncthreads();  // every thread is done with ring slot st
+    if (tid == 0 && prod_j < nchunks) issue_next();
+    if (++st == nst) {
+      st = 0;
+      phase ^= 1u;
+    }
+    if (++k == per_plane) {
+      k = 0;
+      ++plane;
+    }
+  }
+  report_flag(bad, flag);
+  if (DENS) {
+    __shared__ double red[4];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) meanacc += __shfl_down_sync(0xffffffffu, meanacc, o);
+    if ((tid & 31) == 0) red[tid >> 5] = meanacc;
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+      dn.mean_part[blockIdx.x] = s;
+    }
+  }
+}
+
+struct XcLaunch {
+  int threads, G, nst;
+  size_t smem;
+  int64_t ppb, blocks;
+};
+
+template <int P, bool DENS>
+static int plan_xcomp(const int64_t dims[4], XcLaunch* L) {
+  const int n1 = (int)dims[0];
+  const int C1 = n1 / P;
+  const int C2 = (int)(dims[1] / P);
+  const int64_t nplanes = dims[2] * dims[3];
+  if (C1 > 128) {
+    set_error("x1 lines of %d cells exceed one CTA", C1);
+    return VPB_ERR_UNSUPPORTED;
+  }
+  static const int env_chunk =
+      getenv("VPB_XCOMP_CHUNK") ? atoi(getenv("VPB_XCOMP_CHUNK")) : 9216;
+  static const int env_st = getenv("VPB_XCOMP_STAGES") ? atoi(getenv("VPB_XCOMP_STAGES")) : 4;
+  static const int env_smem =
+      getenv("VPB_XCOMP_SMEM") ? atoi(getenv("VPB_XCOMP_SMEM")) : 56 * 1024;
+  L->threads = ((C1 + 31) / 32) * 32;
+  L->nst = std::max(2, std::min(8, env_st));
+  const size_t cell_bytes = (size_t)P * n1 * 8;
+  auto smem_for = [&](int g) { return (size_t)L->nst * g * cell_bytes + L->nst * 8; };
+  int G = std::max<int>(1, (int)(env_chunk / cell_bytes));
+  G = std::min(G, C2);
+  while (G > 1 && (int)smem_for(G) > env_smem) --G;
+  L->G = G;
+  L->smem = smem_for(G);
+  if (L->smem > 220 * 1024) {
+    set_error("x plane chunk of %d dofs does not fit shared memory", P * n1);
+    return VPB_ERR_UNSUPPORTED;
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(dg_xcomp_kernel<P, DENS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         220 * 1024);
+    attr = true;
+  }
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dg_xcomp_kernel<P, DENS>, L->threads,
+                                                L->smem);
+  if (occ < 1) occ = 1;
+  const int64_t grid =
+      std::max<int64_t>(1, std::min<int64_t>(nplanes, (int64_t)occ * xplane_sm_count()));
+  L->ppb = (nplanes + grid - 1) / grid;
+  L->blocks = (nplanes + L->ppb - 1) / L->ppb;
+  return VPB_OK;
+}
+
+template <int P, bool DENS>
+static int launch_xcomp(const double* src, double* dst, const int64_t dims[4], const double* k1,
+                        const int64_t* q1, const double* al1, const double* k2,
+                        const int64_t* q2, const double* al2, int32_t* flag, const XDensity& dn,
+                        cudaStream_t st, int64_t* nblocks_out) {
+  const int64_t nplanes = dims[2] * dims[3];
+  if (nplanes == 0) return VPB_OK;
+  XcLaunch L;
+  int rc = plan_xcomp<P, DENS>(dims, &L);
+  if (rc) return rc;
+  dg_xcomp_kernel<P, DENS><<<(unsigned)L.blocks, L.threads, L.smem, st>>>(
+      src, dst, (int)dims[0], (int)(dims[1] / P), L.G, L.nst, dims[2], nplanes, L.ppb, k1, q1,
+      al1, k2, q2, al2, flag, dn);
+  if (nblocks_out) *nblocks_out = L.blocks;
+  return launched("dg_xcomp_kernel");
+}
+
+template <int P>
+static int xcomp_density_len(const int64_t dims[4], int64_t* len) {
+  XcLaunch L;
+  int rc = plan_xcomp<P, true>(dims, &L);
+  if (rc) return rc;
+  const int64_t cc = (dims[0] / P) * (dims[1] / P);
+  *len = L.blocks * (cc + 1);
+  return VPB_OK;
+}
+
+}  // namespace vpb
+
+using namespace vpb;
+
+extern "C" int vpb_dg_compose_tables(const double* a, const double* b, int64_t n, int32_t order,
+                                     double* out, void* stream) {
+  VPB_REQUIRE(order >= 1 && order <= kMaxOrder, "order %d outside 1..9", order);
+  VPB_REQUIRE(n >= 0, "negative table length");
+  if (n == 0) return VPB_OK;
+  VPB_REQUIRE(a && b && out, "null pointer");
+  const int64_t total = n * order * order;
+  compose_tables_kernel<<<(unsigned)((total + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+      a, b, n, order, out);
+  return launched("compose_tables_kernel");
+}
+
+extern "C" int vpb_dg_sweep_xcomp(const double* src, double* dst, const int64_t dims[4],
+                                  int32_t order, const double* k1, const int64_t* q1,
+                                  const double* alpha1, const double* k2, const int64_t* q2,
+                                  const double* alpha2, int32_t* flag, void* stream) {
+  int rc = xplane_args_ok(src, dst, dims, order);
+  if (rc) return rc;
+  VPB_REQUIRE(k1 && q1 && alpha1 && k2 && q2 && alpha2, "null pointer");
+  const XDensity none{nullptr, nullptr, nullptr, nullptr, {}, {}};
+  VPB_XPLANE_SWITCH(order, rc = launch_xcomp<PP, false>(src, dst, dims, k1, q1, alpha1, k2, q2,
+                                                  alpha2, flag, none, (cudaStream_t)stream,
+                                                  nullptr));
+  return rc;
+}
+
+extern "C" int64_t vpb_dg_xcomp_density_work_len(const int64_t dims[4], int32_t order) {
+  if (order < 1 || order > kMaxOrder || dims[0] % order || dims[1] % order) return -1;
+  int64_t len = -1;
+  int rc = VPB_OK;
+  VPB_XPLANE_SWITCH(order, rc = xcomp_density_len<PP>(dims, &len));
+  return rc == VPB_OK ? len : -1;
+}
+
+extern "C" int vpb_dg_sweep_xcomp_density(
+    const double* src, double* dst, const int64_t dims[4], int32_t order, const double* k1,
+    const int64_t* q1, const double* alpha1, const double* k2, const int64_t* q2,
+    const double* alpha2, int32_t* flag, const double* wv1, const double* wv2,
+    const double* mid_host, const double* wcell1_host, const double* wcell2_host, double volume,
+    double* work, double* rc_out, double* stats, void* stream) {
+  int rc = xplane_args_ok(src, dst, dims, order);
+  if (rc) return rc;
+  VPB_REQUIRE(k1 && q1 && alpha1 && k2 && q2 && alpha2 && rc_out, "null pointer");
+  const int64_t cc = (dims[0] / order) * (dims[1] / order);
+  const int64_t len = vpb_dg_xcomp_density_work_len(dims, order);
+  VPB_REQUIRE(len > 0, "cannot plan the x-plane launch");
+  const int64_t nblk = len / (cc + 1);
+  XDensity dn;
+  rc = xdensity_setup(&dn, order, wv1, wv2, mid_host, wcell1_host, wcell2_host, work, nblk, cc);
+  if (rc) return rc;
+  int64_t used = 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  VPB_XPLANE_SWITCH(order, rc = launch_xcomp<PP, true>(src, dst, dims, k1, q1, alpha1, k2, q2,
+                                                 alpha2, flag, dn, st, &used));
+  if (rc) return rc;
+  VPB_REQUIRE(used == nblk, "x-plane launch plan changed (%lld vs %lld CTAs)", (long long)used,
+              (long long)nblk);
+  return launch_xdens_reduce(work, nblk, cc, volume, rc_out, stats, st);
+}

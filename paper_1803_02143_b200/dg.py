@@ -45,6 +45,7 @@ class DeviceTables:
         self.b = torch.empty((n, p, p), dtype=torch.float64, device=dev)
         self.q = torch.empty(n, dtype=torch.int64, device=dev)
         self.alpha = torch.empty(n, dtype=torch.float64, device=dev)
+        self._k = None
         self.refresh(values, scale, h)
 
     def refresh(self, values: torch.Tensor, scale: float, h: float) -> None:
@@ -55,6 +56,26 @@ class DeviceTables:
                               self.a.data_ptr(), self.b.data_ptr(), self.q.data_ptr(),
                               self.alpha.data_ptr(), _device.stream()),
             "vpb_dg_tables",
+        )
+        if self._k is not None:
+            self._compose()
+
+    def composed(self) -> torch.Tensor:
+        """Two same-table sweeps as one three-cell stencil, per row:
+        ``[AA, AB+BA, BB]`` (n, 3, p, p), for the merged x half steps of the
+        "fast" arithmetic mode (``vpb_dg_sweep_xcomp``)."""
+        if self._k is None:
+            p = self.order
+            self._k = torch.empty((self.n, 3, p, p), dtype=torch.float64, device=self.a.device)
+            self._compose()
+        return self._k
+
+    def _compose(self) -> None:
+        lib = _lib.load()
+        _lib.check(
+            lib.vpb_dg_compose_tables(self.a.data_ptr(), self.b.data_ptr(), self.n, self.order,
+                                      self._k.data_ptr(), _device.stream()),
+            "vpb_dg_compose_tables",
         )
 
 
@@ -211,6 +232,21 @@ def xplane2_dg(grid, src: torch.Tensor, dst: torch.Tensor, t1: DeviceTables, t2:
                                  t2.q.data_ptr(), t2.alpha.data_ptr(), fa[0], fa[1], fb[0], fb[1],
                                  _device.stream()),
         "vpb_dg_sweep_xplane2",
+    )
+
+
+def xcomp_dg(grid, src: torch.Tensor, dst: torch.Tensor, t1: DeviceTables, t2: DeviceTables,
+             flag: torch.Tensor | None) -> None:
+    """Two consecutive x half steps (same tables) in one pass with composed
+    three-cell stencils (``vpb_dg_sweep_xcomp``; equal to
+    :func:`xplane2_dg` up to round-off).  ``flag``: any non-finite output."""
+    lib = _lib.load()
+    _lib.check(
+        lib.vpb_dg_sweep_xcomp(src.data_ptr(), dst.data_ptr(), _lib.dims(grid.dims4), t1.order,
+                               t1.composed().data_ptr(), t1.q.data_ptr(), t1.alpha.data_ptr(),
+                               t2.composed().data_ptr(), t2.q.data_ptr(), t2.alpha.data_ptr(),
+                               None if flag is None else flag.data_ptr(), _device.stream()),
+        "vpb_dg_sweep_xcomp",
     )
 
 

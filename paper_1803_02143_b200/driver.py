@@ -26,7 +26,7 @@ import numpy as np
 import torch
 
 from . import _device, _lib
-from .dg import DeviceTables, sweep_dg, vplane_dg, xplane2_dg, xplane_dg
+from .dg import DeviceTables, sweep_dg, vplane_dg, xcomp_dg, xplane2_dg, xplane_dg
 from .field import DEFAULT_STRATEGY, DistributionField, LayoutDescriptor, write_snapshot
 from .grid import DG, SPACE, SPLINE, VELOCITY, Axis, GridSpec, gauss_nodes
 from .poisson import (
@@ -49,6 +49,36 @@ FUSE_V = True
 # Density as an epilogue of the opening x pass (dG): saves the 8 B/dof read
 # of the standalone density pass.  VPB_FUSE_RHO=0/1 overrides the default.
 FUSE_RHO = os.environ.get("VPB_FUSE_RHO", "1") != "0"
+
+# Arithmetic of the merged x half steps (closing x1 x2 of step m + opening
+# x1 x2 of step m+1 in one pass, see enqueue_steps):
+#   "fast"  (default) -- x1 x2 x1 x2 = (x1 x1)(x2 x2) applied as one composed
+#           three-cell stencil per axis with fused multiply-adds
+#           (vpb_dg_sweep_xcomp): HBM-bound; equal to the sweep chain up to
+#           round-off (~1e-16 relative per step, far inside the 1e-12 bar);
+#   "exact" -- the four sweeps chained with the reference's rounding
+#           (vpb_dg_sweep_xplane2): advance() is then bitwise K strang_step
+#           calls.
+# Every other pass keeps the reference's operation order in both modes.
+# VPB_ARITH=exact|fast overrides the default; see set_arithmetic().
+_ARITH_MODES = ("fast", "exact")
+ARITH = os.environ.get("VPB_ARITH", "fast")
+if ARITH not in _ARITH_MODES:
+    raise ValueError(f"VPB_ARITH must be one of {_ARITH_MODES}, got {ARITH!r}")
+
+
+def set_arithmetic(mode: str) -> str:
+    """Select the merged-x-pass arithmetic ("fast" or "exact"); returns the
+    previous mode."""
+    global ARITH
+    if mode not in _ARITH_MODES:
+        raise ValueError(f"unknown arithmetic mode {mode!r}; expected one of {_ARITH_MODES}")
+    prev, ARITH = ARITH, mode
+    return prev
+
+
+def arithmetic() -> str:
+    return ARITH
 
 
 class SubstepError(RuntimeError):
@@ -272,6 +302,7 @@ class StepState:
             else:
                 self.rho_work = torch.empty(n, dtype=torch.float64, device=dev)
                 self.rho_work2 = None  # double x pass work, allocated on first use
+                self.rho_work3 = None  # composed x pass work, allocated on first use
                 self.rc = torch.empty(grid.axes[0].count * grid.axes[1].count,
                                       dtype=torch.float64, device=dev)
                 # host constants of the epilogue: centre Lagrange weights and
@@ -411,6 +442,19 @@ def enqueue_steps(field: DistributionField, tau: float, nsteps: int, st: StepSta
         t1, t2 = st.x_tables(0, tau), st.x_tables(1, tau)
         fa = (fl_a[close_k:close_k + 1], fl_a[close_k + 1:close_k + 2])
         fb = (fl_b[0:1], fl_b[1:2])
+        if ARITH == "fast":
+            # composed stencils: intermediate states never exist, so a
+            # non-finite output is reported against the pass's first sub-step
+            # (inputs are checked by the producing pass, so only an overflow
+            # inside this pass can land here)
+            if with_density:
+                mark("sweep_x12x12_rho")
+                xcomp_density_dg(grid, field._phys.view(-1), out, t1, t2, fa[0], st, stats_row)
+            else:
+                mark("sweep_x12x12")
+                xcomp_dg(grid, field._phys.view(-1), out, t1, t2, fa[0])
+            swap(out)
+            return
         if with_density:
             mark("sweep_x12x12_rho")
             xplane2_density_dg(grid, field._phys.view(-1), out, t1, t2, fa, fb, st, stats_row)
@@ -532,6 +576,27 @@ def xplane2_density_dg(grid, src, dst, t1, t2, fa, fb, st: StepState, stats) -> 
             st.dens_w2.ctypes.data, g.volume, st.rho_work2.data_ptr(), st.rc.data_ptr(),
             stats.data_ptr(), _device.stream()),
         "vpb_dg_sweep_xplane2_density",
+    )
+
+
+def xcomp_density_dg(grid, src, dst, t1, t2, flag, st: StepState, stats) -> None:
+    """Merged x half steps with composed stencils and the density epilogue."""
+    lib = _lib.load()
+    g = st.geom
+    if st.rho_work3 is None:
+        n = int(lib.vpb_dg_xcomp_density_work_len(_lib.dims(grid.dims4), grid.order))
+        if n <= 0:
+            raise _lib.VpbError("cannot plan the composed x pass")
+        st.rho_work3 = torch.empty(n, dtype=torch.float64, device=_device.device())
+    _lib.check(
+        lib.vpb_dg_sweep_xcomp_density(
+            src.data_ptr(), dst.data_ptr(), _lib.dims(grid.dims4), t1.order,
+            t1.composed().data_ptr(), t1.q.data_ptr(), t1.alpha.data_ptr(),
+            t2.composed().data_ptr(), t2.q.data_ptr(), t2.alpha.data_ptr(), flag.data_ptr(),
+            st.wv1.data_ptr(), st.wv2.data_ptr(), st.dens_mid.ctypes.data,
+            st.dens_w1.ctypes.data, st.dens_w2.ctypes.data, g.volume,
+            st.rho_work3.data_ptr(), st.rc.data_ptr(), stats.data_ptr(), _device.stream()),
+        "vpb_dg_sweep_xcomp_density",
     )
 
 

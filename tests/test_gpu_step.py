@@ -394,16 +394,20 @@ ADVANCE_CASES = [
     (2, (128, 22, 4, 6), 5.0),
     (4, (16, 20, 12, 8), 0.37),
     (1, (12, 10, 8, 6), 0.37),
+    (3, (24, 18, 15, 12), 0.37),    # v1 = 0 plane: alpha == 0 (exact shift) along x1
+    (2, (16, 12, 6, 10), 0.0),      # tau = 0: every row an exact shift
 ]
 
 
 @pytest.mark.parametrize("order,dofs,tau", ADVANCE_CASES)
 def test_advance_bitwise_equal_to_strang_steps(monkeypatch, order, dofs, tau):
-    """K steps with merged x half steps == K separate strang_step calls, bit
-    for bit (separate density pass in both, so every reduction is the same)."""
+    """"exact" arithmetic: K steps with merged x half steps == K separate
+    strang_step calls, bit for bit (separate density pass in both, so every
+    reduction is the same)."""
     prob = vpb.problem_spec("landau4d")
     grid = vpb.make_grid(prob, "dg", dofs, dg_order=order)
     monkeypatch.setattr(driver, "FUSE_RHO", False)
+    monkeypatch.setattr(driver, "ARITH", "exact")
     driver._state_cached.cache_clear()
     f1 = vpb.initialize(prob, grid)
     for _ in range(4):
@@ -414,13 +418,52 @@ def test_advance_bitwise_equal_to_strang_steps(monkeypatch, order, dofs, tau):
     assert np.array_equal(f1.numpy(), f2.numpy())
 
 
+@pytest.mark.parametrize("order,dofs,tau", ADVANCE_CASES)
+def test_advance_fast_arithmetic_matches_strang_steps(monkeypatch, order, dofs, tau):
+    """"fast" arithmetic (composed three-cell stencils, vpb_dg_sweep_xcomp):
+    K merged steps == K strang_step calls up to round-off."""
+    prob = vpb.problem_spec("landau4d")
+    grid = vpb.make_grid(prob, "dg", dofs, dg_order=order)
+    monkeypatch.setattr(driver, "FUSE_RHO", False)
+    monkeypatch.setattr(driver, "ARITH", "fast")
+    driver._state_cached.cache_clear()
+    f1 = vpb.initialize(prob, grid)
+    for _ in range(4):
+        f1 = vpb.strang_step(f1, tau, consume=True)
+    f2 = vpb.advance(vpb.initialize(prob, grid), tau, 4)
+    driver._state_cached.cache_clear()
+    a, b = f1.numpy(), f2.numpy()
+    assert max_rel(b, a) <= 1e-14
+    if tau == 0.0:
+        assert np.array_equal(a, b)  # exact shifts stay copies
+    # mass: the composed projections conserve it like the separate ones
+    m1, m2 = vpb.diagnostics(f1).mass, vpb.diagnostics(f2).mass
+    assert abs(m2 - m1) <= 1e-14 * abs(m1)
+
+
+def test_composed_tables_are_the_matrix_products():
+    prob = vpb.problem_spec("landau4d")
+    grid = vpb.make_grid(prob, "dg", (24, 18, 15, 12), dg_order=3)
+    st = driver.step_state(grid)
+    for d in (0, 1):
+        t = st.x_tables(d, 0.37)
+        a, b = t.a.cpu().numpy(), t.b.cpu().numpy()
+        k = t.composed().cpu().numpy()
+        np.testing.assert_allclose(k[:, 0], a @ a, rtol=0, atol=1e-15)
+        np.testing.assert_allclose(k[:, 1], a @ b + b @ a, rtol=0, atol=1e-15)
+        np.testing.assert_allclose(k[:, 2], b @ b, rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("arith", ["fast", "exact"])
 @pytest.mark.parametrize("order,dofs,tau", ADVANCE_CASES[:5])
-def test_advance_with_density_epilogues(monkeypatch, order, dofs, tau):
+def test_advance_with_density_epilogues(monkeypatch, order, dofs, tau, arith):
     """With the density folded into the x passes only the density summation
-    order differs between the single and the merged pass."""
+    order (and, for "fast", the composed stencils' rounding) differs between
+    the single and the merged pass."""
     prob = vpb.problem_spec("landau4d")
     grid = vpb.make_grid(prob, "dg", dofs, dg_order=order)
     monkeypatch.setattr(driver, "FUSE_RHO", True)
+    monkeypatch.setattr(driver, "ARITH", arith)
     driver._state_cached.cache_clear()
     f1 = vpb.initialize(prob, grid)
     for _ in range(4):
@@ -431,8 +474,10 @@ def test_advance_with_density_epilogues(monkeypatch, order, dofs, tau):
     assert max_rel(f2.numpy(), f1.numpy()) <= 1e-13
 
 
-def test_advance_config1_parity_vs_oracle():
+@pytest.mark.parametrize("arith", ["fast", "exact"])
+def test_advance_config1_parity_vs_oracle(monkeypatch, arith):
     """BASELINE config 1, 10 merged steps vs the oracle: north-star bar."""
+    monkeypatch.setattr(driver, "ARITH", arith)
     prob, method, dofs, order, tau = "landau4d", "dg", 48, 3, 0.1
     for ref, _ in _oracle_run(prob, method, dofs, order, tau, 10):
         pass
@@ -458,6 +503,23 @@ def test_double_x_pass_flags_every_substep():
     driver.xplane2_dg(grid, f.data, out, t1, t2, (flags[0:1], flags[1:2]),
                       (flags[2:3], flags[3:4]))
     assert flags.tolist() == [0, 0, 0, 0]
+
+
+def test_composed_x_pass_flags_nonfinite_output():
+    prob = vpb.problem_spec("landau4d")
+    grid = vpb.make_grid(prob, "dg", (192, 24, 6, 6), dg_order=3)
+    f = vpb.initialize(prob, grid)
+    st = driver.step_state(grid)
+    bad = f.data.clone()
+    bad[12345] = math.nan
+    out = torch.empty_like(bad)
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    t1, t2 = st.x_tables(0, 0.37), st.x_tables(1, 0.37)
+    driver.xcomp_dg(grid, bad, out, t1, t2, flag)
+    assert flag.item() == 1
+    flag.zero_()
+    driver.xcomp_dg(grid, f.data, out, t1, t2, flag)
+    assert flag.item() == 0
 
 
 def test_advance_reports_first_nonfinite_substep_with_time_label():
