@@ -108,6 +108,19 @@ def l2_note(copy_bytes: int) -> str:
             "launch-bound configuration, not a headline number")
 
 
+def load_traffic(cfg_name: str, label: str):
+    """ncu DRAM bytes (read + write) per launch of the kernel behind ``label``
+    on this workload, from the committed capture summary profiles/traffic.json
+    (null when that kernel has not been captured)."""
+    p = ROOT / "profiles" / "traffic.json"
+    if not p.exists():
+        return None
+    ent = json.loads(p.read_text()).get(cfg_name, {}).get(label)
+    if not ent or ent.get("arithmetic") not in (None, os.environ.get("VPB_ARITH", "fast")):
+        return None
+    return float(ent["dram_bytes_per_launch"])
+
+
 def load_peaks() -> tuple[float, str]:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -576,7 +589,10 @@ def run_vpb(args, cfg_name: str, cfg: dict) -> None:
                        "bytes_per_copy": 8 * N, "l2": l2_note(8 * N),
                        "parallelism": "replicas" if world > 1 else "single-gpu"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": args.traffic, "kernel": dom,
+                         "frac": achieved / peak,
+                         "traffic": (args.traffic if args.traffic is not None
+                                     else load_traffic(cfg_name, dom)),
+                         "kernel": dom,
                          "peak_source": peak_kind,
                          "algorithmic_bytes_per_launch": BYTES_PER_DOF_SWEEP * N,
                          "step_frac": step_gbs / peak,

@@ -46,9 +46,12 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     objdir.mkdir(parents=True, exist_ok=True)
     objs = []
     procs = []
+    headers = list(CSRC.glob("*.cuh")) + [ROOT / "include" / "vpb200.h", Path(__file__)]
     for s in SOURCES:
         obj = objdir / (Path(s).stem + ".o")
         objs.append(obj)
+        if not force and not _stale(obj, [CSRC / s, *headers]):
+            continue  # object newer than its source and every header
         cmd = [
             nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17",
             "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",

@@ -328,14 +328,18 @@ static int plan_xcomp(const int64_t dims[4], XcLaunch* L) {
   }
   static const int env_chunk =
       getenv("VPB_XCOMP_CHUNK") ? atoi(getenv("VPB_XCOMP_CHUNK")) : 9216;
-  static const int env_st = getenv("VPB_XCOMP_STAGES") ? atoi(getenv("VPB_XCOMP_STAGES")) : 4;
+  // measured on B200 (scripts/tune_xcomp.py): 3 stages x 2 cells at P = 3
+  // (config 2: 91 %, config 5: 80 % of HBM), 6 stages x 4 cells at P = 2
+  // (config 3: 91 %); G = 1 costs config 5 12 %
+  static const int env_st =
+      getenv("VPB_XCOMP_STAGES") ? atoi(getenv("VPB_XCOMP_STAGES")) : (P >= 3 ? 3 : 6);
   static const int env_smem =
       getenv("VPB_XCOMP_SMEM") ? atoi(getenv("VPB_XCOMP_SMEM")) : 56 * 1024;
   L->threads = ((C1 + 31) / 32) * 32;
   L->nst = std::max(2, std::min(8, env_st));
   const size_t cell_bytes = (size_t)P * n1 * 8;
   auto smem_for = [&](int g) { return (size_t)L->nst * g * cell_bytes + L->nst * 8; };
-  int G = std::max<int>(1, (int)(env_chunk / cell_bytes));
+  int G = std::max<int>(2, (int)(env_chunk / cell_bytes));
   G = std::min(G, C2);
   while (G > 1 && (int)smem_for(G) > env_smem) --G;
   L->G = G;
