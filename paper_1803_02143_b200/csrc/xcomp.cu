@@ -29,10 +29,12 @@
 // (streaming stores), optionally with the density epilogue of xplane.cuh.
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 #include "async_copy.cuh"
 #include "common.cuh"
+#include "tensormap.cuh"
 #include "xplane.cuh"
 
 namespace vpb {
@@ -65,14 +67,27 @@ __device__ __forceinline__ void load_cell_row(const double* p, double (&u)[P]) {
   lds_row_cell<P>(p, u);
 }
 
+// Which planes a launch covers: source plane l (contiguous in src) is the
+// global (iv2, iv1) = (iv2_0 + l / nv1, iv1_0 + l % nv1) and lands at dst
+// plane iv2 * nv1_glob + iv1.  The whole field is the identity map (nv1 =
+// nv1_glob, offsets 0).  Each plane may be split into nseg x2 segments of SL
+// output cells (work items = planes x segments) when a launch covers few
+// planes.  (A blocked v -> x variant that fed blocks of planes through an
+// L2-resident scratch buffer used this; it measured slower.)
+struct XcMap {
+  int64_t nv1, iv1_0, iv2_0, nv1_glob;
+  int nseg, SL;
+};
+
+// 224 registers at P >= 3 keep 3 CTAs of 96 threads (config 5) per SM
 template <int P, bool DENS>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? 224 : 168)
     dg_xcomp_kernel(const double* __restrict__ src, double* __restrict__ dst, int n1, int C2,
-                    int G, int nst, int64_t nv1, int64_t nplanes, int64_t planes_per_block,
+                    int G, int nst, int64_t nitems, int64_t items_per_block, const XcMap mp,
                     const double* __restrict__ k1, const int64_t* __restrict__ q1,
                     const double* __restrict__ al1, const double* __restrict__ k2,
                     const int64_t* __restrict__ q2, const double* __restrict__ al2,
-                    int32_t* __restrict__ flag, const XDensity dn) {
+                    int32_t* __restrict__ flag, const XDensity dn, int dacc) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int cell = P * n1;  // one x2 cell: P rows of n1 dofs
   const int slot = G * cell;
@@ -80,27 +95,41 @@ __global__ void __launch_bounds__(128)
   uint64_t* bars = reinterpret_cast<uint64_t*>(inb + nst * slot);
 
   const int tid = threadIdx.x;
-  const int64_t pl_begin = blockIdx.x * planes_per_block;
-  const int64_t pl_end = min(nplanes, pl_begin + planes_per_block);
-  if (pl_begin >= pl_end) return;
-  const int L = C2 + 2;  // source cells per plane
-  const int per_plane = (L + G - 1) / G;
-  const int64_t nchunks = (pl_end - pl_begin) * per_plane;
+  const int it_begin = (int)(blockIdx.x * items_per_block);
+  const int it_end = (int)min(nitems, (int64_t)it_begin + items_per_block);
+  if (it_begin >= it_end) return;
   const int64_t plane_elems = (int64_t)C2 * cell;
   const uint64_t pol_stream = l2_evict_first();
   const uint64_t pol_keep = l2_evict_last();
 
-  auto s0_of = [&](int64_t pl) { return (int)wrap_mod(-2 * (q2[pl / nv1] + 1), C2); };
+  // item -> (source plane, first output cell, source cells to stream, chunks)
+  struct Item {
+    int l, oa, L, nch;
+  };
+  auto item_of = [&](int it) {
+    Item r;
+    r.l = it / mp.nseg;
+    r.oa = (int)(it - r.l * mp.nseg) * mp.SL;
+    r.L = min(mp.SL, C2 - r.oa) + 2;
+    r.nch = (r.L + G - 1) / G;
+    return r;
+  };
+  const int nv1l = (int)mp.nv1;
+  auto iv2_of = [&](int l) { return (int)mp.iv2_0 + l / nv1l; };
+  // first source cell of an item: -2(q2+1) + oa (mod C2)
+  auto s0_of = [&](const Item& r) {
+    return (int)wrap_mod(-2 * (q2[iv2_of(r.l)] + 1) + r.oa, C2);
+  };
   // producer (thread 0)
-  int64_t p_plane = pl_begin;
+  int p_it = it_begin;
+  Item p_r{};
   int p_k = 0, p_s0 = 0, p_st = 0;
-  int64_t prod_j = 0;
   auto issue_next = [&]() {
     const int t0 = p_k * G;
-    const int ns = min(G, L - t0);
+    const int ns = min(G, p_r.L - t0);
     int sb = p_s0 + t0;
     while (sb >= C2) sb -= C2;
-    const double* base = src + p_plane * plane_elems;
+    const double* base = src + (int64_t)p_r.l * plane_elems;
     double* d = inb + p_st * slot;
     mbar_arrive_expect_tx(bars + p_st, (uint32_t)ns * cell * 8u);
     const int run1 = min(ns, C2 - sb);
@@ -116,22 +145,25 @@ __global__ void __launch_bounds__(128)
       else
         bulk_g2s(d + run1 * cell, base, (uint32_t)(ns - run1) * cell * 8u, bars + p_st);
     }
-    ++prod_j;
     if (++p_st == nst) p_st = 0;
-    if (++p_k == per_plane) {
+    if (++p_k == p_r.nch) {
       p_k = 0;
-      if (++p_plane < pl_end) p_s0 = s0_of(p_plane);
+      if (++p_it < it_end) {
+        p_r = item_of(p_it);
+        p_s0 = s0_of(p_r);
+      }
     }
   };
 
   if (tid == 0) {
     for (int s = 0; s < nst; ++s) mbar_init(bars + s, 1);
     fence_mbar_init();
-    p_s0 = s0_of(pl_begin);
+    p_r = item_of(it_begin);
+    p_s0 = s0_of(p_r);
   }
   __syncthreads();
   if (tid == 0)
-    while (prod_j < nst && prod_j < nchunks) issue_next();
+    for (int s = 0; s < nst && p_it < it_end; ++s) issue_next();
 
   const int C1 = n1 / P;
   const bool active = tid < C1;
@@ -142,16 +174,16 @@ __global__ void __launch_bounds__(128)
   bool bad = false;
   int st = 0;
   uint32_t phase = 0;
-  int k = 0;  // chunk index inside the plane
-  int64_t plane = pl_begin;
   double wplane = 0.0, meanacc = 0.0;
   double* mypart = DENS ? dn.rc_part + (int64_t)blockIdx.x * C2 * C1 : nullptr;
-  if (DENS && active)
+  if (DENS && active && !dacc)
     for (int c2 = 0; c2 < C2; ++c2) mypart[c2 * C1 + tid] = 0.0;
 
-  for (int64_t j = 0; j < nchunks; ++j) {
-    if (active && k == 0) {
-      const int64_t iv2 = plane / nv1, iv1 = plane - iv2 * nv1;
+  for (int it = it_begin; it < it_end; ++it) {
+    const Item r = item_of(it);
+    const int l2 = r.l / nv1l;
+    const int iv2 = (int)mp.iv2_0 + l2, iv1 = (int)mp.iv1_0 + (r.l - l2 * nv1l);
+    if (active) {
       if (DENS) wplane = dn.wv1[iv1] * dn.wv2[iv2];
       ex1 = (al1[iv1] == 0.0);
       ex2 = (al2[iv2] == 0.0);
@@ -173,126 +205,124 @@ __global__ void __launch_bounds__(128)
       off1 = mid * P;
       off2 = up * P;
     }
-    const int t0 = k * G;
-    const int ns = min(G, L - t0);
-    mbar_wait(bars + st, phase);
-    const double* in = inb + st * slot;
-    double* outp = dst + plane * plane_elems;
+    double* outp = dst + ((int64_t)iv2 * mp.nv1_glob + iv1) * plane_elems;
+    for (int k = 0; k < r.nch; ++k) {
+      const int t0 = k * G;
+      const int ns = min(G, r.L - t0);
+      mbar_wait(bars + st, phase);
+      const double* in = inb + st * slot;
 
-    auto run = [&](auto ex1c, auto ex2c) {
-      constexpr bool E1 = decltype(ex1c)::value, E2 = decltype(ex2c)::value;
-      for (int sc = 0; sc < ns; ++sc) {
-        const int t = t0 + sc;
-        const double* rows = in + sc * cell;
-        double g[P][P];
-        // composed x1 stencil on this source x2 cell: g[m2][jj]
+      auto run = [&](auto ex1c, auto ex2c) {
+        constexpr bool E1 = decltype(ex1c)::value, E2 = decltype(ex2c)::value;
+        for (int sc = 0; sc < ns; ++sc) {
+          const int t = t0 + sc;
+          const double* rows = in + sc * cell;
+          double g[P][P];
+          // composed x1 stencil on this source x2 cell: g[m2][jj]
 #pragma unroll
-        for (int m2 = 0; m2 < P; ++m2) {
-          const double* row = rows + m2 * n1;
-          double u2[P];
-          load_cell_row<P>(row + off2, u2);
-          if constexpr (E1) {
+          for (int m2 = 0; m2 < P; ++m2) {
+            const double* row = rows + m2 * n1;
+            double u2[P];
+            load_cell_row<P>(row + off2, u2);
+            if constexpr (E1) {
 #pragma unroll
-            for (int jj = 0; jj < P; ++jj) g[m2][jj] = u2[jj];
-          } else {
-            double u0[P], u1[P];
-            load_cell_row<P>(row + off0, u0);
-            load_cell_row<P>(row + off1, u1);
+              for (int jj = 0; jj < P; ++jj) g[m2][jj] = u2[jj];
+            } else {
+              double u0[P], u1[P];
+              load_cell_row<P>(row + off0, u0);
+              load_cell_row<P>(row + off1, u1);
 #pragma unroll
-            for (int jj = 0; jj < P; ++jj) {
-              double acc = T1[0][jj][0] * u0[0];
+              for (int jj = 0; jj < P; ++jj) {
+                double acc = T1[0][jj][0] * u0[0];
 #pragma unroll
-              for (int m = 1; m < P; ++m) acc = fma(T1[0][jj][m], u0[m], acc);
+                for (int m = 1; m < P; ++m) acc = fma(T1[0][jj][m], u0[m], acc);
 #pragma unroll
-              for (int m = 0; m < P; ++m) acc = fma(T1[1][jj][m], u1[m], acc);
+                for (int m = 0; m < P; ++m) acc = fma(T1[1][jj][m], u1[m], acc);
 #pragma unroll
-              for (int m = 0; m < P; ++m) acc = fma(T1[2][jj][m], u2[m], acc);
-              g[m2][jj] = acc;
-            }
-          }
-        }
-        if (t >= 2) {
-          double o[P][P];
-#pragma unroll
-          for (int j2 = 0; j2 < P; ++j2)
-#pragma unroll
-            for (int jj = 0; jj < P; ++jj) {
-              if constexpr (E2) {
-                o[j2][jj] = g[j2][jj];
-              } else {
-                double acc = T2[0][j2][0] * w0[0][jj];
-#pragma unroll
-                for (int m = 1; m < P; ++m) acc = fma(T2[0][j2][m], w0[m][jj], acc);
-#pragma unroll
-                for (int m = 0; m < P; ++m) acc = fma(T2[1][j2][m], w1[m][jj], acc);
-#pragma unroll
-                for (int m = 0; m < P; ++m) acc = fma(T2[2][j2][m], g[m][jj], acc);
-                o[j2][jj] = acc;
+                for (int m = 0; m < P; ++m) acc = fma(T1[2][jj][m], u2[m], acc);
+                g[m2][jj] = acc;
               }
             }
-          ExpMax eo;
-          const int oc = t - 2;
-          double* ot = outp + (int64_t)oc * cell + tid * P;
-#pragma unroll
-          for (int j2 = 0; j2 < P; ++j2) {
-#pragma unroll
-            for (int jj = 0; jj < P; ++jj) eo.add(o[j2][jj]);
-            if constexpr (P % 2 == 0) {
-#pragma unroll
-              for (int jj = 0; jj < P; jj += 2)
-                __stcs(reinterpret_cast<double2*>(ot + j2 * n1 + jj),
-                       make_double2(o[j2][jj], o[j2][jj + 1]));
-            } else {
-#pragma unroll
-              for (int jj = 0; jj < P; ++jj) __stcs(ot + j2 * n1 + jj, o[j2][jj]);
-            }
           }
-          bad |= eo.bad();
-          if constexpr (DENS) {
-            double rcv, mv = 0.0;
-            if constexpr (P % 2 == 1) {
-              rcv = o[P / 2][P / 2];  // mid = e_centre exactly (checked on the host)
-            } else {
-              rcv = 0.0;
-#pragma unroll
-              for (int j2 = 0; j2 < P; ++j2)
-#pragma unroll
-                for (int jj = 0; jj < P; ++jj) rcv = fma(dn.mm[j2 * P + jj], o[j2][jj], rcv);
-            }
+          if (t >= 2) {
+            double o[P][P];
 #pragma unroll
             for (int j2 = 0; j2 < P; ++j2)
 #pragma unroll
-              for (int jj = 0; jj < P; ++jj) mv = fma(dn.ww[j2 * P + jj], o[j2][jj], mv);
-            red_add_hint(mypart + oc * C1 + tid, dmul(wplane, rcv), pol_keep);
-            meanacc = fma(wplane, mv, meanacc);
+              for (int jj = 0; jj < P; ++jj) {
+                if constexpr (E2) {
+                  o[j2][jj] = g[j2][jj];
+                } else {
+                  double acc = T2[0][j2][0] * w0[0][jj];
+#pragma unroll
+                  for (int m = 1; m < P; ++m) acc = fma(T2[0][j2][m], w0[m][jj], acc);
+#pragma unroll
+                  for (int m = 0; m < P; ++m) acc = fma(T2[1][j2][m], w1[m][jj], acc);
+#pragma unroll
+                  for (int m = 0; m < P; ++m) acc = fma(T2[2][j2][m], g[m][jj], acc);
+                  o[j2][jj] = acc;
+                }
+              }
+            ExpMax eo;
+            const int oc = r.oa + t - 2;
+            double* ot = outp + (int64_t)oc * cell + tid * P;
+#pragma unroll
+            for (int j2 = 0; j2 < P; ++j2) {
+#pragma unroll
+              for (int jj = 0; jj < P; ++jj) eo.add(o[j2][jj]);
+              if constexpr (P % 2 == 0) {
+#pragma unroll
+                for (int jj = 0; jj < P; jj += 2)
+                  __stcs(reinterpret_cast<double2*>(ot + j2 * n1 + jj),
+                         make_double2(o[j2][jj], o[j2][jj + 1]));
+              } else {
+#pragma unroll
+                for (int jj = 0; jj < P; ++jj) __stcs(ot + j2 * n1 + jj, o[j2][jj]);
+              }
+            }
+            bad |= eo.bad();
+            if constexpr (DENS) {
+              double rcv, mv = 0.0;
+              if constexpr (P % 2 == 1) {
+                rcv = o[P / 2][P / 2];  // mid = e_centre exactly (checked on the host)
+              } else {
+                rcv = 0.0;
+#pragma unroll
+                for (int j2 = 0; j2 < P; ++j2)
+#pragma unroll
+                  for (int jj = 0; jj < P; ++jj) rcv = fma(dn.mm[j2 * P + jj], o[j2][jj], rcv);
+              }
+#pragma unroll
+              for (int j2 = 0; j2 < P; ++j2)
+#pragma unroll
+                for (int jj = 0; jj < P; ++jj) mv = fma(dn.ww[j2 * P + jj], o[j2][jj], mv);
+              red_add_hint(mypart + oc * C1 + tid, dmul(wplane, rcv), pol_keep);
+              meanacc = fma(wplane, mv, meanacc);
+            }
           }
+#pragma unroll
+          for (int m2 = 0; m2 < P; ++m2)
+#pragma unroll
+            for (int jj = 0; jj < P; ++jj) {
+              w0[m2][jj] = w1[m2][jj];
+              w1[m2][jj] = g[m2][jj];
+            }
         }
-#pragma unroll
-        for (int m2 = 0; m2 < P; ++m2)
-#pragma unroll
-          for (int jj = 0; jj < P; ++jj) {
-            w0[m2][jj] = w1[m2][jj];
-            w1[m2][jj] = g[m2][jj];
-          }
+      };
+      if (active) {
+        using F = std::false_type;
+        using T = std::true_type;
+        if (!ex1 && !ex2) run(F{}, F{});
+        else if (!ex1) run(F{}, T{});
+        else if (!ex2) run(T{}, F{});
+        else run(T{}, T{});
       }
-    };
-    if (active) {
-      using F = std::false_type;
-      using T = std::true_type;
-      if (!ex1 && !ex2) run(F{}, F{});
-      else if (!ex1) run(F{}, T{});
-      else if (!ex2) run(T{}, F{});
-      else run(T{}, T{});
-    }
-    __syncthreads();  // every thread is done with ring slot st
-    if (tid == 0 && prod_j < nchunks) issue_next();
-    if (++st == nst) {
-      st = 0;
-      phase ^= 1u;
-    }
-    if (++k == per_plane) {
-      k = 0;
-      ++plane;
+      __syncthreads();  // every thread is done with ring slot st
+      if (tid == 0 && p_it < it_end) issue_next();
+      if (++st == nst) {
+        st = 0;
+        phase ^= 1u;
+      }
     }
   }
   report_flag(bad, flag);
@@ -305,7 +335,10 @@ __global__ void __launch_bounds__(128)
     if (tid == 0) {
       double s = 0.0;
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
-      dn.mean_part[blockIdx.x] = s;
+      if (dacc)
+        dn.mean_part[blockIdx.x] += s;
+      else
+        dn.mean_part[blockIdx.x] = s;
     }
   }
 }
@@ -313,15 +346,14 @@ __global__ void __launch_bounds__(128)
 struct XcLaunch {
   int threads, G, nst;
   size_t smem;
-  int64_t ppb, blocks;
+  int64_t ppb, blocks, max_blocks;
 };
 
 template <int P, bool DENS>
-static int plan_xcomp(const int64_t dims[4], XcLaunch* L) {
+static int plan_xcomp(const int64_t dims[4], int64_t nitems, XcLaunch* L) {
   const int n1 = (int)dims[0];
   const int C1 = n1 / P;
   const int C2 = (int)(dims[1] / P);
-  const int64_t nplanes = dims[2] * dims[3];
   if (C1 > 128) {
     set_error("x1 lines of %d cells exceed one CTA", C1);
     return VPB_ERR_UNSUPPORTED;
@@ -358,34 +390,38 @@ static int plan_xcomp(const int64_t dims[4], XcLaunch* L) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dg_xcomp_kernel<P, DENS>, L->threads,
                                                 L->smem);
   if (occ < 1) occ = 1;
-  const int64_t grid =
-      std::max<int64_t>(1, std::min<int64_t>(nplanes, (int64_t)occ * xplane_sm_count()));
-  L->ppb = (nplanes + grid - 1) / grid;
-  L->blocks = (nplanes + L->ppb - 1) / L->ppb;
+  L->max_blocks = (int64_t)occ * xplane_sm_count();
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(nitems, L->max_blocks));
+  L->ppb = (nitems + grid - 1) / grid;
+  L->blocks = (nitems + L->ppb - 1) / L->ppb;
   return VPB_OK;
 }
 
 template <int P, bool DENS>
-static int launch_xcomp(const double* src, double* dst, const int64_t dims[4], const double* k1,
-                        const int64_t* q1, const double* al1, const double* k2,
-                        const int64_t* q2, const double* al2, int32_t* flag, const XDensity& dn,
-                        cudaStream_t st, int64_t* nblocks_out) {
-  const int64_t nplanes = dims[2] * dims[3];
-  if (nplanes == 0) return VPB_OK;
+static int launch_xcomp(const double* src, double* dst, const int64_t dims[4], int64_t nitems,
+                        const XcMap& mp, const double* k1, const int64_t* q1, const double* al1,
+                        const double* k2, const int64_t* q2, const double* al2, int32_t* flag,
+                        const XDensity& dn, int dacc, cudaStream_t st, int64_t* nblocks_out) {
+  if (nitems == 0) return VPB_OK;
   XcLaunch L;
-  int rc = plan_xcomp<P, DENS>(dims, &L);
+  int rc = plan_xcomp<P, DENS>(dims, nitems, &L);
   if (rc) return rc;
   dg_xcomp_kernel<P, DENS><<<(unsigned)L.blocks, L.threads, L.smem, st>>>(
-      src, dst, (int)dims[0], (int)(dims[1] / P), L.G, L.nst, dims[2], nplanes, L.ppb, k1, q1,
-      al1, k2, q2, al2, flag, dn);
+      src, dst, (int)dims[0], (int)(dims[1] / P), L.G, L.nst, nitems, L.ppb, mp, k1, q1, al1, k2,
+      q2, al2, flag, dn, dacc);
   if (nblocks_out) *nblocks_out = L.blocks;
   return launched("dg_xcomp_kernel");
+}
+
+inline XcMap xcomp_whole_field(const int64_t dims[4], int P) {
+  const int C2 = (int)(dims[1] / P);
+  return XcMap{dims[2], 0, 0, dims[2], 1, C2};
 }
 
 template <int P>
 static int xcomp_density_len(const int64_t dims[4], int64_t* len) {
   XcLaunch L;
-  int rc = plan_xcomp<P, true>(dims, &L);
+  int rc = plan_xcomp<P, true>(dims, dims[2] * dims[3], &L);
   if (rc) return rc;
   const int64_t cc = (dims[0] / P) * (dims[1] / P);
   *len = L.blocks * (cc + 1);
@@ -416,9 +452,10 @@ extern "C" int vpb_dg_sweep_xcomp(const double* src, double* dst, const int64_t 
   if (rc) return rc;
   VPB_REQUIRE(k1 && q1 && alpha1 && k2 && q2 && alpha2, "null pointer");
   const XDensity none{nullptr, nullptr, nullptr, nullptr, {}, {}};
-  VPB_XPLANE_SWITCH(order, rc = launch_xcomp<PP, false>(src, dst, dims, k1, q1, alpha1, k2, q2,
-                                                  alpha2, flag, none, (cudaStream_t)stream,
-                                                  nullptr));
+  VPB_XPLANE_SWITCH(order, rc = launch_xcomp<PP, false>(
+                               src, dst, dims, dims[2] * dims[3], xcomp_whole_field(dims, PP), k1,
+                               q1, alpha1, k2, q2, alpha2, flag, none, 0, (cudaStream_t)stream,
+                               nullptr));
   return rc;
 }
 
@@ -448,8 +485,9 @@ extern "C" int vpb_dg_sweep_xcomp_density(
   if (rc) return rc;
   int64_t used = 0;
   cudaStream_t st = (cudaStream_t)stream;
-  VPB_XPLANE_SWITCH(order, rc = launch_xcomp<PP, true>(src, dst, dims, k1, q1, alpha1, k2, q2,
-                                                 alpha2, flag, dn, st, &used));
+  VPB_XPLANE_SWITCH(order, rc = launch_xcomp<PP, true>(
+                               src, dst, dims, dims[2] * dims[3], xcomp_whole_field(dims, PP), k1,
+                               q1, alpha1, k2, q2, alpha2, flag, dn, 0, st, &used));
   if (rc) return rc;
   VPB_REQUIRE(used == nblk, "x-plane launch plan changed (%lld vs %lld CTAs)", (long long)used,
               (long long)nblk);

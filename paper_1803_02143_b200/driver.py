@@ -463,7 +463,7 @@ def enqueue_steps(field: DistributionField, tau: float, nsteps: int, st: StepSta
             xplane2_dg(grid, field._phys.view(-1), out, t1, t2, fa, fb)
         swap(out)
 
-    def field_and_velocity(m: int) -> None:
+    def field_solve_of(m: int) -> None:
         fl = flags[m]
         if st.fused_rho:
             mark("field_solve")
@@ -473,6 +473,10 @@ def enqueue_steps(field: DistributionField, tau: float, nsteps: int, st: StepSta
             density_into(field.data, grid, st.rho)  # compute_density  poisson.py:85-95
             mark("field_solve")
             solve_into(st.rho, grid, st.e, stats[m], fl[field_k:field_k + 1])  # solve_poisson
+
+    def field_and_velocity(m: int) -> None:
+        field_solve_of(m)
+        fl = flags[m]
         if st.fused_v:  # _advect_velocity(tau) in one pass  driver.py:231-242
             mark("tables_v12")
             t1 = st.v_tables(0, tau)
