@@ -82,7 +82,7 @@ L2_BYTES = 126 * 2**20
 def sweeps_per_launch(label: str) -> int:
     """1-D sweeps one launch of a kernel group performs (labels of driver.enqueue_steps)."""
     name = label[len("sweep_"):].replace("_rho", "")
-    return {"x12": 2, "v12": 2, "x12x12": 4}.get(name, 1)
+    return {"x12": 2, "v12": 2, "x12x12": 4, "x1x2": 2, "x2x2": 2, "xx2": 2}.get(name, 1)
 
 
 def fp64_peak_gops() -> float:

@@ -219,6 +219,18 @@ int vpb_spline_sweep_axis(int32_t axis, const double* src, double* dst, const in
                           const double* values, double scale, double h, int32_t* flag,
                           void* stream);
 
+/* Two consecutive spline sweeps along `axis` with the same shifts in one
+ * pass (the closing and opening x half steps of consecutive Strang steps,
+ * driver.py:245-265 / 371-377): E^2 (6 T^-1)^2 u -- the circulant solve and
+ * evaluation of _kernels.pyx:37-93 commute, so the recursive-filter solve
+ * runs twice and the evaluation is the 7-tap self-convolution of the weights
+ * at offset 2 j0.  Equal to two vpb_spline_sweep_axis calls up to round-off.
+ * Needs n % 16 == 0, n >= 32 (and n / 32 in {1, 2, 4, 8} for axis 0);
+ * VPB_ERR_UNSUPPORTED otherwise. */
+int vpb_spline_sweep_axis2(int32_t axis, const double* src, double* dst, const int64_t dims[4],
+                           const double* values, double scale, double h, int32_t* flag,
+                           void* stream);
+
 /* rho[ix2*n1+ix1] = sum_v f * wv1[iv1] * wv2[iv2].  work: vpb_density_work_len doubles. */
 int64_t vpb_density_work_len(const int64_t dims[4]);
 int vpb_density(const double* f, const int64_t dims[4], const double* wv1, const double* wv2,

@@ -162,7 +162,25 @@ struct SplineTileArgs {
   int32_t* flag;
   int use_tma;  // strided tiles: one TMA tensor copy per tile (tmap valid)
   int iir;      // fast path: recursive filters (n % 8 == 0, n >= 32) instead of PCR
+  int dbl;      // two consecutive sweeps with the same shift in one pass (see below)
 };
+
+// Two sweeps by the same shift (the closing and opening x half steps of
+// consecutive Strang steps, driver.py:245-265 / 371-377) in one pass.  One
+// sweep is out = E w with w = 6 T^-1 u (_kernels.pyx:37-93): T the periodic
+// (1, 4, 1) matrix, E the periodic 4-tap evaluation at offset j0.  Both are
+// circulant, so they commute and two sweeps are E^2 (6 T^-1)^2 u: the
+// recursive-filter solve runs twice and the evaluation is the 7-tap
+// self-convolution of the weights at offset 2 j0.  Equal to two separate
+// sweeps up to round-off.
+__device__ __forceinline__ void spline_weights2(const double (&w)[4], double (&c)[7]) {
+#pragma unroll
+  for (int m = 0; m < 7; ++m) c[m] = 0.0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) c[k + kk] = fma(w[k], w[kk], c[k + kk]);
+}
 
 constexpr int kSplineBars = 8;  // row groups with their own mbarrier (strided tiles)
 
@@ -265,7 +283,7 @@ __device__ __forceinline__ void iir_solve(double* y, const int YS, const int n, 
   }
 }
 
-template <bool CONTIG, bool PCR>
+template <bool CONTIG, bool PCR, bool DBL = false>
 __global__ void __launch_bounds__(kSplineT)
     spline_tile_kernel(SplineTileArgs a, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -365,6 +383,7 @@ __global__ void __launch_bounds__(kSplineT)
       if (a.iir) {
         const double z1 = pk[kPcrLevels + 2];  // z1^1 of the power table
         iir_solve(y, YS, n, z1);
+        if constexpr (DBL) iir_solve(y, YS, n, z1);
         wscale = -6.0 * z1;
       } else {
         pcr_level<1>(y, YS, n, pk[0]);
@@ -473,6 +492,58 @@ __global__ void __launch_bounds__(kSplineT)
     }
     const int j0 = (int)wrap_mod((int64_t)off - 1, n);
     j0s[t] = j0;
+    if constexpr (DBL && !CONTIG) {
+      // out_i = sum_m c_m w2[2 j0 + i + m], m = 0..6: a 7-value sliding window
+      const double wv[4] = {w0, w1, w2, w3};
+      double c[7];
+      spline_weights2(wv, c);
+      int jn = (2 * j0) % n;
+      auto nxt = [&]() {
+        const double v = y[jn * YS];
+        if (++jn == n) jn = 0;
+        return v;
+      };
+      double sv[6], win[6];
+#pragma unroll
+      for (int r = 0; r < 6; ++r) win[r] = sv[r] = nxt();
+      const int64_t outer = L / a.S, inner = L - outer * a.S;
+      const int64_t obase = outer * a.S * n + inner;
+      auto emit = [&](double v6) {
+        double o = c[0] * win[0];
+#pragma unroll
+        for (int m = 1; m < 6; ++m) o = fma(c[m], win[m], o);
+        o = fma(c[6], v6, o);
+#pragma unroll
+        for (int m = 0; m < 5; ++m) win[m] = win[m + 1];
+        win[5] = v6;
+        bad |= not_finite(o);
+        return o;
+      };
+      constexpr int E = 16;
+      int k = 0;
+      for (; k + E <= n - 6; k += E) {
+        double v[E], o[E];
+#pragma unroll
+        for (int r = 0; r < E; ++r) v[r] = nxt();
+#pragma unroll
+        for (int r = 0; r < E; ++r) o[r] = emit(v[r]);
+#pragma unroll
+        for (int r = 0; r < E; ++r) __stcs(a.dst + obase + (int64_t)(k + r) * a.S, o[r]);
+      }
+      for (; k < n; ++k) {
+        const int back = k - (n - 6);
+        double v6;
+        if (back < 0) {
+          v6 = nxt();
+        } else {
+          v6 = sv[0];
+#pragma unroll
+          for (int r = 1; r < 6; ++r)
+            if (back == r) v6 = sv[r];
+        }
+        __stcs(a.dst + obase + (int64_t)k * a.S, emit(v6));
+      }
+    } else {
 
     // out_i = w0 om[j0+i] + w1 om[j0+i+1] + w2 om[j0+i+2] + w3 om[j0+i+3]
     // with a 4-value sliding window (one smem load per output).  On the
@@ -534,6 +605,7 @@ __global__ void __launch_bounds__(kSplineT)
         __stcs(a.dst + obase + (int64_t)k * a.S, o);
       }
     }
+    }  // single sweep
   }
   __syncwarp();
   if (CONTIG) {
@@ -594,14 +666,16 @@ __device__ __forceinline__ void spline_eval_weights(const SplineTileArgs& a, int
 
 // H = 32 / LPW lanes per line, LPW lines per warp at a time (independent
 // scans interleave; shallower scans), NPT = n / H points per lane.
-template <int NPT, int LPW>
+template <int NPT, int LPW, bool DBL = false>
 __global__ void __launch_bounds__(32 * kRowWarps)
     spline_rows_kernel(SplineTileArgs a) {
   constexpr int H = 32 / LPW;
   constexpr int LOGH = H == 32 ? 5 : H == 16 ? 4 : 3;
   constexpr int n = H * NPT;
   constexpr int IT = 32 / LPW;  // iterations covered by one batch of weights
-  __shared__ double wrow[kRowWarps][LPW][n + 4];  // + wrap copies of points 0..3
+  constexpr int NTAP = DBL ? 7 : 4;  // evaluation taps (DBL: two sweeps, spline_weights2)
+  // + wrap copies of points 0..NTAP-1 (row length kept even: 16-B stores)
+  __shared__ double wrow[kRowWarps][LPW][n + (NTAP + 1) / 2 * 2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int sub = lane / H, hl = lane % H;
   const double* zp = a.fac + 4 * n + 8 + kPcrLevels;  // z1^k
@@ -635,7 +709,9 @@ __global__ void __launch_bounds__(32 * kRowWarps)
   };
   // weights of the next IT iterations: lane t holds those of iteration
   // (t / LPW) for sub-line (t % LPW)
-  double wl[4] = {0.0, 0.0, 0.0, 0.0};
+  double wl[NTAP];
+#pragma unroll
+  for (int m = 0; m < NTAP; ++m) wl[m] = 0.0;
   int jl = 0;
   double nxt[NPT];
   load_line(P0 * LPW + sub, nxt);
@@ -644,12 +720,23 @@ __global__ void __launch_bounds__(32 * kRowWarps)
     const int64_t L = P * LPW + sub;
     if (k % IT == 0) {
       const int64_t Lw = (P + (lane / LPW) * Pstep) * LPW + lane % LPW;
-      if (Lw < a.nlines) spline_eval_weights(a, Lw, n, g, wl, jl);
+      if (Lw < a.nlines) {
+        if constexpr (DBL) {
+          double w4[4];
+          spline_eval_weights(a, Lw, n, g, w4, jl);
+          spline_weights2(w4, wl);
+          jl = (2 * jl) % n;
+        } else {
+          spline_eval_weights(a, Lw, n, g, wl, jl);
+        }
+      }
     }
     double x[NPT];
 #pragma unroll
     for (int r = 0; r < NPT; ++r) x[r] = nxt[r];
     load_line(L + Pstep * LPW, nxt);  // next lines' loads fly while these are solved
+#pragma unroll
+    for (int pass = 0; pass < (DBL ? 2 : 1); ++pass) {
     // ---- causal filter
 #pragma unroll
     for (int r = 1; r < NPT; ++r) x[r] = fma(z1, x[r - 1], x[r]);
@@ -678,6 +765,7 @@ __global__ void __launch_bounds__(32 * kRowWarps)
     F = hl == H - 1 ? V : fma(zout, V, F);
 #pragma unroll
     for (int r = 0; r < NPT; ++r) x[r] = fma(zr[NPT - r], F, x[r]);
+    }  // pass
     // ---- w (the -6 z1 gain is folded into the evaluation weights)
     double* row = wrow[warp][sub];
     if constexpr (NPT % 2 == 0) {
@@ -688,18 +776,39 @@ __global__ void __launch_bounds__(32 * kRowWarps)
 #pragma unroll
       for (int r = 0; r < NPT; ++r) row[NPT * hl + r] = x[r];
     }
-    if (hl < (4 + NPT - 1) / NPT)  // wrap copies row[n + i] = row[i], i < 4
+    if (hl < (NTAP + NPT - 1) / NPT)  // wrap copies row[n + i] = row[i], i < NTAP
 #pragma unroll
       for (int r = 0; r < NPT; ++r)
-        if (NPT * hl + r < 4) row[n + NPT * hl + r] = x[r];
+        if (NPT * hl + r < NTAP) row[n + NPT * hl + r] = x[r];
     __syncwarp();
     // ---- evaluation: out_i = w0 w[j0+i] + w1 w[j0+i+1] + w2 w[j0+i+2] + w3 w[j0+i+3]
     const int src_lane = (k % IT) * LPW + sub;
+    const int j0 = __shfl_sync(0xffffffffu, jl, src_lane);
+    if constexpr (DBL) {
+      double c[7];
+#pragma unroll
+      for (int m = 0; m < 7; ++m) c[m] = __shfl_sync(0xffffffffu, wl[m], src_lane);
+      if (L < a.nlines) {
+        double* dst = a.dst + L * n;
+#pragma unroll
+        for (int r = 0; r < NPT; ++r) {
+          const int i = hl + H * r;
+          int q = j0 + i;
+          if (q >= n) q -= n;
+          double o = c[0] * row[q];
+#pragma unroll
+          for (int m = 1; m < 7; ++m) o = fma(c[m], row[q + m], o);
+          em.add(o);
+          __stcs(dst + i, o);
+        }
+      }
+      __syncwarp();
+      continue;
+    }
     const double w0 = __shfl_sync(0xffffffffu, wl[0], src_lane);
     const double w1 = __shfl_sync(0xffffffffu, wl[1], src_lane);
     const double w2 = __shfl_sync(0xffffffffu, wl[2], src_lane);
     const double w3 = __shfl_sync(0xffffffffu, wl[3], src_lane);
-    const int j0 = __shfl_sync(0xffffffffu, jl, src_lane);
     if (L < a.nlines) {
       double* dst = a.dst + L * n;
 #pragma unroll
@@ -747,12 +856,18 @@ static int launch_spline(SplineTileArgs a, bool contig, bool exact, cudaStream_t
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(spline_tile_kernel<false, true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(spline_tile_kernel<false, true, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr = true;
   }
   static const bool force_exact = getenv("VPB_SPLINE_EXACT") != nullptr;
   static const bool force_pcr = getenv("VPB_SPLINE_PCR") != nullptr;
   const bool pcr = !exact && !force_exact && a.n % 16 == 0 && a.n >= 32;
   a.iir = pcr && !force_pcr ? 1 : 0;
+  if (a.dbl && !a.iir) {
+    set_error("double spline sweep needs the recursive-filter solve (n %% 16 == 0, n >= 32)");
+    return VPB_ERR_UNSUPPORTED;
+  }
   int64_t blocks = (a.nlines + kSplineT - 1) / kSplineT;
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
@@ -777,6 +892,15 @@ static int launch_spline(SplineTileArgs a, bool contig, bool exact, cudaStream_t
     const int64_t want = (a.nlines + kRowWarps - 1) / kRowWarps;
     const unsigned rblocks = (unsigned)std::min<int64_t>(want, 148 * 8);
     const dim3 thr(32 * kRowWarps);
+    if (a.dbl) {
+      switch (npt) {
+        case 1: spline_rows_kernel<1, 1, true><<<rblocks, thr, 0, st>>>(a); break;
+        case 2: spline_rows_kernel<2, 1, true><<<rblocks, thr, 0, st>>>(a); break;
+        case 4: spline_rows_kernel<4, 1, true><<<rblocks, thr, 0, st>>>(a); break;
+        default: spline_rows_kernel<8, 1, true><<<rblocks, thr, 0, st>>>(a); break;
+      }
+      return launched("spline_rows_kernel");
+    }
     switch (npt) {
       case 1: spline_rows_kernel<1, 1><<<rblocks, thr, 0, st>>>(a); break;
       case 2: spline_rows_kernel<2, 1><<<rblocks, thr, 0, st>>>(a); break;
@@ -784,6 +908,14 @@ static int launch_spline(SplineTileArgs a, bool contig, bool exact, cudaStream_t
       default: spline_rows_kernel<8, 1><<<rblocks, thr, 0, st>>>(a); break;
     }
     return launched("spline_rows_kernel");
+  }
+  if (a.dbl) {
+    if (contig) {
+      set_error("double spline sweep along the contiguous axis needs n / 32 in {1, 2, 4, 8}");
+      return VPB_ERR_UNSUPPORTED;
+    }
+    spline_tile_kernel<false, true, true><<<(unsigned)blocks, kSplineT, smem, st>>>(a, tmap);
+    return launched("spline_tile_kernel");
   }
   if (contig) {
     if (pcr)
@@ -861,9 +993,25 @@ extern "C" int vpb_spline_sweep_strided(double* view, const int64_t shape[4],
   return rc;
 }
 
+static int spline_axis(int32_t axis, const double* src, double* dst, const int64_t dims[4],
+                       const double* values, double scale, double h, int32_t* flag, int dbl,
+                       void* stream);
+
 extern "C" int vpb_spline_sweep_axis(int32_t axis, const double* src, double* dst,
                                      const int64_t dims[4], const double* values, double scale,
                                      double h, int32_t* flag, void* stream) {
+  return spline_axis(axis, src, dst, dims, values, scale, h, flag, 0, stream);
+}
+
+extern "C" int vpb_spline_sweep_axis2(int32_t axis, const double* src, double* dst,
+                                      const int64_t dims[4], const double* values, double scale,
+                                      double h, int32_t* flag, void* stream) {
+  return spline_axis(axis, src, dst, dims, values, scale, h, flag, 1, stream);
+}
+
+static int spline_axis(int32_t axis, const double* src, double* dst, const int64_t dims[4],
+                       const double* values, double scale, double h, int32_t* flag, int dbl,
+                       void* stream) {
   VPB_REQUIRE(axis >= 0 && axis < 4, "axis %d out of range", axis);
   VPB_REQUIRE(src != dst, "src and dst must be distinct buffers");
   VPB_REQUIRE(h > 0.0, "spacing must be positive, got %g", h);
@@ -872,6 +1020,7 @@ extern "C" int vpb_spline_sweep_axis(int32_t axis, const double* src, double* ds
   const int64_t n = dims[axis];
   VPB_REQUIRE(n >= 2, "need at least 2 samples per line");
   SplineTileArgs a{src, dst, total / n, (int)n, 1, nullptr, 1, 1, values, scale, h, nullptr, flag};
+  a.dbl = dbl;
   if (axis == 0) {
     a.tdiv = n2;  // lines = (iv2, iv1, ix2), row = iv1
     a.tmod = nv1;

@@ -39,7 +39,7 @@ from .poisson import (
     scratch,
     solve_into,
 )
-from .spline import sweep_spline
+from .spline import double_sweep_ok, sweep_spline, sweep_spline2
 
 
 # Fused x1+x2 plane sweeps and fused v1+v2 column sweeps (set False to run
@@ -281,6 +281,9 @@ class StepState:
                         and (grid.dof(0) * grid.order) % 2 == 0 and FUSE_X)
         # both v sweeps in one pass (bitwise-identical result)
         self.fused_v = grid.method == DG and grid.ndim == 4 and FUSE_V
+        # spline: merged x half steps as one double sweep per x axis ("fast")
+        self.spline_x2 = grid.method == SPLINE and all(
+            double_sweep_ok(grid, d) for d in range(grid.ndim_x))
         lib = _lib.load()
         self.diag_work = torch.empty(int(lib.vpb_diag_work_len(_lib.dims(grid.dims4))),
                                      dtype=torch.float64, device=dev)
@@ -463,6 +466,17 @@ def enqueue_steps(field: DistributionField, tau: float, nsteps: int, st: StepSta
             xplane2_dg(grid, field._phys.view(-1), out, t1, t2, fa, fb)
         swap(out)
 
+    def x_double_spline(fl) -> None:
+        """Spline: closing x half step of one step + opening one of the next
+        as one double sweep per x axis (vpb_spline_sweep_axis2); a
+        non-finite result is reported against the closing sub-step."""
+        for d in range(nx):
+            out = st.buf
+            mark(f"sweep_{xn[d]}x2")
+            sweep_spline2(grid, d, field._phys.view(-1), out, st.x_tables(d, tau), half,
+                          grid.axes[d].h, fl[close_k + d:close_k + d + 1])
+            swap(out)
+
     def field_solve_of(m: int) -> None:
         fl = flags[m]
         if st.fused_rho:
@@ -519,6 +533,8 @@ def enqueue_steps(field: DistributionField, tau: float, nsteps: int, st: StepSta
                 x_half(flags[m], close_k, False, None)  # "close" of the last step
         elif merge and st.fused_x:
             x_double(flags[m], flags[m + 1], st.fused_rho, stats[m + 1])
+        elif merge and st.spline_x2 and ARITH == "fast":
+            x_double_spline(flags[m])
         else:
             x_half(flags[m], close_k, False, None)
             x_half(flags[m + 1], 0, st.fused_rho, stats[m + 1])

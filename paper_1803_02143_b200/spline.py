@@ -77,3 +77,28 @@ def sweep_spline(grid, axis: int, src: torch.Tensor, dst: torch.Tensor, values: 
                                   _device.stream()),
         "vpb_spline_sweep_axis",
     )
+
+
+def sweep_spline2(grid, axis: int, src: torch.Tensor, dst: torch.Tensor, values: torch.Tensor,
+                  scale: float, h: float, flag: torch.Tensor | None) -> None:
+    """Two consecutive sweeps with the same shifts in one pass
+    (``vpb_spline_sweep_axis2``; equal to two :func:`sweep_spline` calls up
+    to round-off)."""
+    lib = _lib.load()
+    _lib.check(
+        lib.vpb_spline_sweep_axis2(device_axis(grid, axis), src.data_ptr(), dst.data_ptr(),
+                                   _lib.dims(grid.dims4), values.data_ptr(), float(scale),
+                                   float(h), None if flag is None else flag.data_ptr(),
+                                   _device.stream()),
+        "vpb_spline_sweep_axis2",
+    )
+
+
+def double_sweep_ok(grid, axis: int) -> bool:
+    """Whether :func:`sweep_spline2` supports this axis of the grid."""
+    n = grid.dof(axis)
+    if n % 16 or n < 32:
+        return False
+    if device_axis(grid, axis) == 0:
+        return n % 32 == 0 and n // 32 in (1, 2, 4, 8)
+    return True

@@ -564,9 +564,12 @@ def test_advance_record_matches_diagnostics_of_the_final_state(order, dofs):
 
 @pytest.mark.parametrize("prob,method,dofs,order", [
     ("landau4d", "spline", 16, 0), ("landau2d", "dg", 32, 4), ("landau2d", "spline", 32, 0)])
-def test_advance_without_fused_x_pass_equals_strang_steps(prob, method, dofs, order):
+def test_advance_without_fused_x_pass_equals_strang_steps(monkeypatch, prob, method, dofs,
+                                                          order):
     """Grids without the fused x pass (spline, 1x1v) run advance() as plain
-    steps: bitwise the strang_step loop, records via diagnostics()."""
+    steps ("exact" arithmetic): bitwise the strang_step loop, records via
+    diagnostics()."""
+    monkeypatch.setattr(driver, "ARITH", "exact")
     problem = vpb.problem_spec(prob)
     grid = vpb.make_grid(problem, method, dofs, dg_order=order)
     f1 = vpb.initialize(problem, grid)
@@ -577,3 +580,55 @@ def test_advance_without_fused_x_pass_equals_strang_steps(prob, method, dofs, or
     ref = vpb.diagnostics(f1, 0.3)
     for k in KEYS:
         assert getattr(rec, k) == getattr(ref, k), k
+
+
+# ---------------------------------------------------------------------------
+# spline: merged x half steps as one double sweep per axis (vpb_spline_sweep_axis2)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("prob,dofs,tau", [
+    ("landau4d", (32, 64, 32, 48), 0.1),      # rows kernel NPT 1, strided tiles
+    ("landau4d", (128, 32, 48, 32), 0.37),    # NPT 4, |shift| of several points
+    ("landau4d", (256, 48, 32, 32), 0.1),     # NPT 8
+    ("landau2d", (64, 96), 0.2),              # 1x1v: contiguous x
+])
+def test_spline_double_sweep_advance_matches_strang_steps(monkeypatch, prob, dofs, tau):
+    monkeypatch.setattr(driver, "ARITH", "fast")
+    problem = vpb.problem_spec(prob)
+    grid = vpb.make_grid(problem, "spline", dofs)
+    driver._state_cached.cache_clear()
+    assert driver.step_state(grid).spline_x2
+    f1 = vpb.initialize(problem, grid)
+    for _ in range(4):
+        f1 = vpb.strang_step(f1, tau, consume=True)
+    f2 = vpb.advance(vpb.initialize(problem, grid), tau, 4)
+    driver._state_cached.cache_clear()
+    a, b = f1.numpy(), f2.numpy()
+    assert max_rel(b, a) <= 1e-13
+
+
+@pytest.mark.parametrize("axis", [0, 1, 2, 3])
+def test_spline_double_sweep_equals_two_sweeps(axis):
+    from paper_1803_02143_b200.spline import sweep_spline, sweep_spline2
+    prob = vpb.problem_spec("landau4d")
+    grid = vpb.make_grid(prob, "spline", (64, 32, 48, 32))
+    f = vpb.initialize(prob, grid)
+    rng = np.random.default_rng(5)
+    f.data.copy_(torch.from_numpy(rng.standard_normal(f.data.numel())))
+    st = driver.step_state(grid)
+    if axis < 2:
+        vals, scale = st.vpoints[axis], 0.37
+    else:
+        n = grid.dof(0) * grid.dof(1)
+        vals = torch.from_numpy(rng.uniform(-3, 3, n)).cuda()
+        scale = 0.3
+    h = grid.axes[axis].h
+    t1 = torch.empty_like(f.data)
+    t2 = torch.empty_like(f.data)
+    sweep_spline(grid, axis, f.data, t1, vals, scale, h, None)
+    sweep_spline(grid, axis, t1, t2, vals, scale, h, None)
+    d = torch.empty_like(f.data)
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    sweep_spline2(grid, axis, f.data, d, vals, scale, h, flag)
+    assert flag.item() == 0
+    a, b = t2.cpu().numpy(), d.cpu().numpy()
+    assert np.max(np.abs(a - b)) <= 1e-13 * np.max(np.abs(a))
