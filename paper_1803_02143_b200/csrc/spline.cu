@@ -892,6 +892,17 @@ static int launch_spline(SplineTileArgs a, bool contig, bool exact, cudaStream_t
     const int64_t want = (a.nlines + kRowWarps - 1) / kRowWarps;
     const unsigned rblocks = (unsigned)std::min<int64_t>(want, 148 * 8);
     const dim3 thr(32 * kRowWarps);
+    static const bool dbl_two = getenv("VPB_SPLINE_DBL_LPW2") != nullptr;
+    if (a.dbl && dbl_two && (npt == 2 || npt == 4)) {
+      // two half-warp lines per warp: half the scan shuffles per line
+      const int64_t want2 = (a.nlines / 2 + kRowWarps - 1) / kRowWarps;
+      const unsigned rb2 = (unsigned)std::min<int64_t>(want2, 148 * 8);
+      if (npt == 2)
+        spline_rows_kernel<4, 2, true><<<rb2, thr, 0, st>>>(a);
+      else
+        spline_rows_kernel<8, 2, true><<<rb2, thr, 0, st>>>(a);
+      return launched("spline_rows_kernel");
+    }
     if (a.dbl) {
       switch (npt) {
         case 1: spline_rows_kernel<1, 1, true><<<rblocks, thr, 0, st>>>(a); break;
