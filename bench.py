@@ -315,11 +315,19 @@ def run_sharded(args, cfg_name: str, cfg: dict, d, world: int, rank: int, local:
     N = grid.total_dof
     tau = cfg["tau"]
     if cfg["method"] == "dg":
-        p1, p2 = dist.process_grid(world)
-        dec = dist.Decomposition(grid, p1, p2)
-        solver = dist.ShardedSolver(grid, dec, dist.TorchComm(), [rank])
+        # x1 shards when the merged stencil pass applies (its halo fits a
+        # shard), else the process grid (x1 x x2 at 8 GPUs)
+        solver = dist.ShardedSolver(grid, dist.Decomposition(grid, world, 1), dist.TorchComm(),
+                                    [rank])
+        p1, p2 = world, 1
+        if not (solver._stencil_ready() and solver._merged_halo_fits(tau)):
+            p1, p2 = dist.process_grid(world)
+            solver = dist.ShardedSolver(grid, dist.Decomposition(grid, p1, p2),
+                                        dist.TorchComm(), [rank])
         local_f = lambda: solver.shards[rank].f  # noqa: E731
-        layout = f"x-shard {p1}x{p2} (NCCL halos + rho allgather)"
+        layout = (f"x-shard {p1}x{p2} (NCCL halos + rho allgather"
+                  + ("; merged x passes as halo-exchanged stencil passes)"
+                     if solver._stencil_ready() else ")"))
     else:
         solver = dist.SplineShardedSolver(grid, dist.TorchComm(), [rank], world)
         local_f = lambda: solver.a[rank][0]  # noqa: E731
@@ -327,8 +335,17 @@ def run_sharded(args, cfg_name: str, cfg: dict, d, world: int, rank: int, local:
     solver.initialize(problem)
     stream = torch.cuda.current_stream()
     clocks = ClockSampler(local).start()
-    for _ in range(args.warmup):
-        solver.step(tau)
+
+    def steps(k: int) -> None:
+        # dG: advance() merges the x half steps of consecutive steps into one
+        # halo-exchanged stencil pass per step (x1-sharded layouts)
+        if hasattr(solver, "advance"):
+            solver.advance(tau, k)
+        else:
+            for _ in range(k):
+                solver.step(tau)
+
+    steps(args.warmup)
     from paper_1803_02143_b200 import _lib
 
     barrier(d, local)
@@ -338,8 +355,7 @@ def run_sharded(args, cfg_name: str, cfg: dict, d, world: int, rank: int, local:
     end = torch.cuda.Event(enable_timing=True)
     clocks.begin()
     start.record(stream)
-    for _ in range(args.steps):
-        solver.step(tau)
+    steps(args.steps)
     end.record(stream)
     torch.cuda.synchronize()
     clocks.end()

@@ -214,6 +214,37 @@ int vpb_dg_sweep_xcomp_density(const double* src, double* dst, const int64_t dim
                                double volume, double* work, double* rc_out, double* stats,
                                void* stream);
 
+/* {0, A, B} per table row: one x sweep as the three-cell stencil of
+ * vpb_dg_sweep_xstencil with qmul = 1 (out: DEVICE [n][3][p][p]). */
+int vpb_dg_single_tables(const double* a, const double* b, int64_t n, int32_t order, double* out,
+                         void* stream);
+
+/* Three-cell x-plane stencil pass on an x1-SHARDED field (one rank's box
+ * [v2][v1][x2][x1 local]; x2 whole): output cell c of every x row reads x1
+ * cells c-Q-2 .. c-Q with Q = qmul*q, then the same along x2.  qmul = 2 with
+ * vpb_dg_compose_tables tables = the merged closing + opening x half steps
+ * (vpb_dg_sweep_xcomp); qmul = 1 with vpb_dg_single_tables = one x half step
+ * (_advect_space, driver.py:220-228).  x1 cells -wl..-1 and C1..C1+wr-1 come
+ * from hl / hr in the vpb_halo_pack layout [plane][x2 row][w*p]; the row is
+ * not periodic.  The _density variant adds the epilogue of
+ * vpb_dg_sweep_xplane_density for the shard's cells (rc_out: the shard's
+ * [C2][C1 local] cell-centre slab; stats[0]: its share of the mean / volume). */
+int vpb_dg_sweep_xstencil(const double* src, double* dst, const int64_t dims[4], int32_t order,
+                          const double* k1, const int64_t* q1, const double* alpha1,
+                          const double* k2, const int64_t* q2, const double* alpha2, int32_t qmul,
+                          const double* hl, int32_t wl, const double* hr, int32_t wr,
+                          int32_t* flag, void* stream);
+int64_t vpb_dg_xstencil_density_work_len(const int64_t dims[4], int32_t order);
+int vpb_dg_sweep_xstencil_density(const double* src, double* dst, const int64_t dims[4],
+                                  int32_t order, const double* k1, const int64_t* q1,
+                                  const double* alpha1, const double* k2, const int64_t* q2,
+                                  const double* alpha2, int32_t qmul, const double* hl, int32_t wl,
+                                  const double* hr, int32_t wr, int32_t* flag, const double* wv1,
+                                  const double* wv2, const double* mid_host,
+                                  const double* wcell1_host, const double* wcell2_host,
+                                  double volume, double* work, double* rc_out, double* stats,
+                                  void* stream);
+
 /* One spline sweep along `axis`; shift of line = values[table row]*scale. */
 int vpb_spline_sweep_axis(int32_t axis, const double* src, double* dst, const int64_t dims[4],
                           const double* values, double scale, double h, int32_t* flag,

@@ -91,6 +91,15 @@ SIGNATURES = {
     "vpb_dg_xcomp_density_work_len": (c_int64, [POINTER(c_int64), c_int32]),
     "vpb_dg_sweep_xcomp_density": (c_int, [c_void_p, c_void_p, POINTER(c_int64), c_int32]
                                    + [c_void_p] * 12 + [c_double] + [c_void_p] * 4),
+    "vpb_dg_single_tables": (c_int, [c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p]),
+    "vpb_dg_sweep_xstencil": (c_int, [c_void_p, c_void_p, POINTER(c_int64), c_int32]
+                              + [c_void_p] * 6 + [c_int32, c_void_p, c_int32, c_void_p, c_int32,
+                                                  c_void_p, c_void_p]),
+    "vpb_dg_xstencil_density_work_len": (c_int64, [POINTER(c_int64), c_int32]),
+    "vpb_dg_sweep_xstencil_density": (c_int, [c_void_p, c_void_p, POINTER(c_int64), c_int32]
+                                      + [c_void_p] * 6
+                                      + [c_int32, c_void_p, c_int32, c_void_p, c_int32]
+                                      + [c_void_p] * 6 + [c_double] + [c_void_p] * 4),
     "vpb_slab_copy": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, c_void_p]),
     "vpb_spline_sweep_axis": (c_int, [c_int32, c_void_p, c_void_p, POINTER(c_int64), c_void_p,
                                       c_double, c_double, c_void_p, c_void_p]),

@@ -39,9 +39,11 @@
 
 namespace vpb {
 
-// out[t][0] = A A, out[t][1] = A B + B A, out[t][2] = B B  (row-major P x P)
+// out[t][0] = A A, out[t][1] = A B + B A, out[t][2] = B B  (row-major P x P);
+// single != 0: out[t] = {0, A, B}, one sweep as the same three-cell stencil
+// with offset q instead of 2q (the sharded step's single x half steps)
 __global__ void compose_tables_kernel(const double* __restrict__ a, const double* __restrict__ b,
-                                      int64_t T, int P, double* __restrict__ out) {
+                                      int64_t T, int P, double* __restrict__ out, int single) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t pp = (int64_t)P * P;
   if (e >= T * pp) return;
@@ -50,6 +52,10 @@ __global__ void compose_tables_kernel(const double* __restrict__ a, const double
   const double* A = a + t * pp;
   const double* B = b + t * pp;
   double c0 = 0.0, c1 = 0.0, c2 = 0.0;
+  if (single) {
+    c1 = A[j * P + m];
+    c2 = B[j * P + m];
+  } else
   for (int k = 0; k < P; ++k) {
     c0 = fma(A[j * P + k], A[k * P + m], c0);
     c1 = fma(A[j * P + k], B[k * P + m], c1);
@@ -79,15 +85,28 @@ struct XcMap {
   int nseg, SL;
 };
 
+// Stencil offset and x1 halos.  Source cells of output cell c are
+// c - Q - 2, c - Q - 1, c - Q with Q = qmul * q (qmul = 2: the composed merged
+// pass; 1: a single sweep with tables {0, A, B}).  HALO (x1-sharded field):
+// the row is the shard's cells 0..C1-1, not periodic; cells -wl..-1 come from
+// hl and C1..C1+wr-1 from hr, laid out [plane][x2 row][w*P] (vpb_halo_pack).
+struct XcStencil {
+  int qmul;
+  const double* hl;
+  const double* hr;
+  int wl, wr;
+};
+
 // 224 registers at P >= 3 keep 3 CTAs of 96 threads (config 5) per SM
-template <int P, bool DENS>
+template <int P, bool DENS, bool HALO = false>
 __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? 224 : 168)
     dg_xcomp_kernel(const double* __restrict__ src, double* __restrict__ dst, int n1, int C2,
                     int G, int nst, int64_t nitems, int64_t items_per_block, const XcMap mp,
                     const double* __restrict__ k1, const int64_t* __restrict__ q1,
                     const double* __restrict__ al1, const double* __restrict__ k2,
                     const int64_t* __restrict__ q2, const double* __restrict__ al2,
-                    int32_t* __restrict__ flag, const XDensity dn, int dacc) {
+                    int32_t* __restrict__ flag, const XDensity dn, int dacc,
+                    const XcStencil sx) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int cell = P * n1;  // one x2 cell: P rows of n1 dofs
   const int slot = G * cell;
@@ -116,9 +135,9 @@ __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? 224 : 168)
   };
   const int nv1l = (int)mp.nv1;
   auto iv2_of = [&](int l) { return (int)mp.iv2_0 + l / nv1l; };
-  // first source cell of an item: -2(q2+1) + oa (mod C2)
+  // first source cell of an item: -(qmul q2 + 2) + oa (mod C2)
   auto s0_of = [&](const Item& r) {
-    return (int)wrap_mod(-2 * (q2[iv2_of(r.l)] + 1) + r.oa, C2);
+    return (int)wrap_mod(-((int64_t)sx.qmul * q2[iv2_of(r.l)] + 2) + r.oa, C2);
   };
   // producer (thread 0)
   int p_it = it_begin;
@@ -170,6 +189,9 @@ __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? 224 : 168)
   double T1[3][P][P], T2[3][P][P];
   bool ex1 = true, ex2 = true;
   int off0 = 0, off1 = 0, off2 = 0;  // element offsets of the three x1 source cells
+  // HALO: per source cell 0 = shared-memory row, 1 = left halo, 2 = right halo
+  int hw0 = 0, hw1 = 0, hw2 = 0;
+  int item_s0 = 0;
   double w0[P][P], w1[P][P];         // x1 results of source cells t-2, t-1
   bool bad = false;
   int st = 0;
@@ -196,15 +218,35 @@ __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? 224 : 168)
             T1[s][jj][m] = __ldg(k1 + (iv1 * 3 + s) * P * P + jj * P + m);
             T2[s][jj][m] = __ldg(k2 + (iv2 * 3 + s) * P * P + jj * P + m);
           }
-      const int qq = (int)wrap_mod(2 * q1[iv1], C1);
-      int lo = tid - qq - 2;
-      while (lo < 0) lo += C1;
-      const int mid = lo + 1 == C1 ? 0 : lo + 1;
-      const int up = mid + 1 == C1 ? 0 : mid + 1;
-      off0 = lo * P;
-      off1 = mid * P;
-      off2 = up * P;
+      if constexpr (HALO) {
+        const int lo = tid - sx.qmul * (int)q1[iv1] - 2;
+        auto place = [&](int j, int& off, int& hw) {
+          if (j < 0) {
+            hw = 1;
+            off = (j + sx.wl) * P;
+          } else if (j >= C1) {
+            hw = 2;
+            off = (j - C1) * P;
+          } else {
+            hw = 0;
+            off = j * P;
+          }
+        };
+        place(lo, off0, hw0);
+        place(lo + 1, off1, hw1);
+        place(lo + 2, off2, hw2);
+      } else {
+        const int qq = (int)wrap_mod((int64_t)sx.qmul * q1[iv1], C1);
+        int lo = tid - qq - 2;
+        while (lo < 0) lo += C1;
+        const int mid = lo + 1 == C1 ? 0 : lo + 1;
+        const int up = mid + 1 == C1 ? 0 : mid + 1;
+        off0 = lo * P;
+        off1 = mid * P;
+        off2 = up * P;
+      }
     }
+    if constexpr (HALO) item_s0 = s0_of(r);
     double* outp = dst + ((int64_t)iv2 * mp.nv1_glob + iv1) * plane_elems;
     for (int k = 0; k < r.nch; ++k) {
       const int t0 = k * G;
@@ -218,19 +260,35 @@ __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? 224 : 168)
           const int t = t0 + sc;
           const double* rows = in + sc * cell;
           double g[P][P];
+          int64_t hrow = 0;  // HALO: row index (plane, x2 cell, row 0) in the halo buffers
+          if constexpr (HALO) {
+            int sx2 = item_s0 + t;
+            while (sx2 >= C2) sx2 -= C2;
+            hrow = ((int64_t)r.l * C2 + sx2) * P;
+          }
+          auto load_src = [&](const double* row, int m2, int off, int hw, double (&u)[P]) {
+            if (!HALO || hw == 0) {
+              load_cell_row<P>(row + off, u);
+            } else {
+              const double* h = hw == 1 ? sx.hl + (hrow + m2) * (sx.wl * P) + off
+                                        : sx.hr + (hrow + m2) * (sx.wr * P) + off;
+#pragma unroll
+              for (int m = 0; m < P; ++m) u[m] = __ldg(h + m);
+            }
+          };
           // composed x1 stencil on this source x2 cell: g[m2][jj]
 #pragma unroll
           for (int m2 = 0; m2 < P; ++m2) {
             const double* row = rows + m2 * n1;
             double u2[P];
-            load_cell_row<P>(row + off2, u2);
+            load_src(row, m2, off2, hw2, u2);
             if constexpr (E1) {
 #pragma unroll
               for (int jj = 0; jj < P; ++jj) g[m2][jj] = u2[jj];
             } else {
               double u0[P], u1[P];
-              load_cell_row<P>(row + off0, u0);
-              load_cell_row<P>(row + off1, u1);
+              load_src(row, m2, off0, hw0, u0);
+              load_src(row, m2, off1, hw1, u1);
 #pragma unroll
               for (int jj = 0; jj < P; ++jj) {
                 double acc = T1[0][jj][0] * u0[0];
@@ -349,7 +407,7 @@ struct XcLaunch {
   int64_t ppb, blocks, max_blocks;
 };
 
-template <int P, bool DENS>
+template <int P, bool DENS, bool HALO = false>
 static int plan_xcomp(const int64_t dims[4], int64_t nitems, XcLaunch* L) {
   const int n1 = (int)dims[0];
   const int C1 = n1 / P;
@@ -382,12 +440,12 @@ static int plan_xcomp(const int64_t dims[4], int64_t nitems, XcLaunch* L) {
   }
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(dg_xcomp_kernel<P, DENS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(dg_xcomp_kernel<P, DENS, HALO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          220 * 1024);
     attr = true;
   }
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dg_xcomp_kernel<P, DENS>, L->threads,
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dg_xcomp_kernel<P, DENS, HALO>, L->threads,
                                                 L->smem);
   if (occ < 1) occ = 1;
   L->max_blocks = (int64_t)occ * xplane_sm_count();
@@ -397,18 +455,19 @@ static int plan_xcomp(const int64_t dims[4], int64_t nitems, XcLaunch* L) {
   return VPB_OK;
 }
 
-template <int P, bool DENS>
+template <int P, bool DENS, bool HALO = false>
 static int launch_xcomp(const double* src, double* dst, const int64_t dims[4], int64_t nitems,
                         const XcMap& mp, const double* k1, const int64_t* q1, const double* al1,
                         const double* k2, const int64_t* q2, const double* al2, int32_t* flag,
-                        const XDensity& dn, int dacc, cudaStream_t st, int64_t* nblocks_out) {
+                        const XDensity& dn, int dacc, cudaStream_t st, int64_t* nblocks_out,
+                        const XcStencil& sx = XcStencil{2, nullptr, nullptr, 0, 0}) {
   if (nitems == 0) return VPB_OK;
   XcLaunch L;
-  int rc = plan_xcomp<P, DENS>(dims, nitems, &L);
+  int rc = plan_xcomp<P, DENS, HALO>(dims, nitems, &L);
   if (rc) return rc;
-  dg_xcomp_kernel<P, DENS><<<(unsigned)L.blocks, L.threads, L.smem, st>>>(
+  dg_xcomp_kernel<P, DENS, HALO><<<(unsigned)L.blocks, L.threads, L.smem, st>>>(
       src, dst, (int)dims[0], (int)(dims[1] / P), L.G, L.nst, nitems, L.ppb, mp, k1, q1, al1, k2,
-      q2, al2, flag, dn, dacc);
+      q2, al2, flag, dn, dacc, sx);
   if (nblocks_out) *nblocks_out = L.blocks;
   return launched("dg_xcomp_kernel");
 }
@@ -418,10 +477,10 @@ inline XcMap xcomp_whole_field(const int64_t dims[4], int P) {
   return XcMap{dims[2], 0, 0, dims[2], 1, C2};
 }
 
-template <int P>
+template <int P, bool HALO = false>
 static int xcomp_density_len(const int64_t dims[4], int64_t* len) {
   XcLaunch L;
-  int rc = plan_xcomp<P, true>(dims, dims[2] * dims[3], &L);
+  int rc = plan_xcomp<P, true, HALO>(dims, dims[2] * dims[3], &L);
   if (rc) return rc;
   const int64_t cc = (dims[0] / P) * (dims[1] / P);
   *len = L.blocks * (cc + 1);
@@ -432,15 +491,28 @@ static int xcomp_density_len(const int64_t dims[4], int64_t* len) {
 
 using namespace vpb;
 
+static int compose_tables(const double* a, const double* b, int64_t n, int32_t order,
+                          double* out, int single, void* stream);
+
 extern "C" int vpb_dg_compose_tables(const double* a, const double* b, int64_t n, int32_t order,
                                      double* out, void* stream) {
+  return compose_tables(a, b, n, order, out, 0, stream);
+}
+
+extern "C" int vpb_dg_single_tables(const double* a, const double* b, int64_t n, int32_t order,
+                                    double* out, void* stream) {
+  return compose_tables(a, b, n, order, out, 1, stream);
+}
+
+static int compose_tables(const double* a, const double* b, int64_t n, int32_t order,
+                          double* out, int single, void* stream) {
   VPB_REQUIRE(order >= 1 && order <= kMaxOrder, "order %d outside 1..9", order);
   VPB_REQUIRE(n >= 0, "negative table length");
   if (n == 0) return VPB_OK;
   VPB_REQUIRE(a && b && out, "null pointer");
   const int64_t total = n * order * order;
   compose_tables_kernel<<<(unsigned)((total + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
-      a, b, n, order, out);
+      a, b, n, order, out, single);
   return launched("compose_tables_kernel");
 }
 
@@ -488,6 +560,77 @@ extern "C" int vpb_dg_sweep_xcomp_density(
   VPB_XPLANE_SWITCH(order, rc = launch_xcomp<PP, true>(
                                src, dst, dims, dims[2] * dims[3], xcomp_whole_field(dims, PP), k1,
                                q1, alpha1, k2, q2, alpha2, flag, dn, 0, st, &used));
+  if (rc) return rc;
+  VPB_REQUIRE(used == nblk, "x-plane launch plan changed (%lld vs %lld CTAs)", (long long)used,
+              (long long)nblk);
+  return launch_xdens_reduce(work, nblk, cc, volume, rc_out, stats, st);
+}
+
+// ---------------------------------------------------------------------------
+// Three-cell x-plane stencil on an x1-sharded field (dist.py ShardedSolver):
+// qmul = 2 with composed tables is the merged pair of x half steps, qmul = 1
+// with {0, A, B} tables (vpb_dg_single_tables) one x half step; x1 source
+// cells outside the shard come from the halo buffers (vpb_halo_pack layout).
+// ---------------------------------------------------------------------------
+static int xstencil_args(const double* src, const double* dst, const int64_t dims[4],
+                         int32_t order, int32_t qmul, const double* hl, int32_t wl,
+                         const double* hr, int32_t wr) {
+  int rc = xplane_args_ok(src, dst, dims, order);
+  if (rc) return rc;
+  VPB_REQUIRE(qmul == 1 || qmul == 2, "qmul must be 1 or 2");
+  VPB_REQUIRE(wl >= 0 && wr >= 0 && (wl == 0 || hl) && (wr == 0 || hr), "bad halo");
+  VPB_REQUIRE(wl <= dims[0] / order && wr <= dims[0] / order, "halo wider than the shard");
+  return VPB_OK;
+}
+
+extern "C" int vpb_dg_sweep_xstencil(const double* src, double* dst, const int64_t dims[4],
+                                     int32_t order, const double* k1, const int64_t* q1,
+                                     const double* alpha1, const double* k2, const int64_t* q2,
+                                     const double* alpha2, int32_t qmul, const double* hl,
+                                     int32_t wl, const double* hr, int32_t wr, int32_t* flag,
+                                     void* stream) {
+  int rc = xstencil_args(src, dst, dims, order, qmul, hl, wl, hr, wr);
+  if (rc) return rc;
+  const XDensity none{nullptr, nullptr, nullptr, nullptr, {}, {}};
+  const XcStencil sx{qmul, hl, hr, wl, wr};
+  VPB_XPLANE_SWITCH(order, rc = launch_xcomp<PP, false, true>(
+                               src, dst, dims, dims[2] * dims[3], xcomp_whole_field(dims, PP), k1,
+                               q1, alpha1, k2, q2, alpha2, flag, none, 0, (cudaStream_t)stream,
+                               nullptr, sx));
+  return rc;
+}
+
+extern "C" int64_t vpb_dg_xstencil_density_work_len(const int64_t dims[4], int32_t order) {
+  if (order < 1 || order > kMaxOrder || dims[0] % order || dims[1] % order) return -1;
+  int64_t len = -1;
+  int rc = VPB_OK;
+  VPB_XPLANE_SWITCH(order, rc = (xcomp_density_len<PP, true>(dims, &len)));
+  return rc == VPB_OK ? len : -1;
+}
+
+extern "C" int vpb_dg_sweep_xstencil_density(
+    const double* src, double* dst, const int64_t dims[4], int32_t order, const double* k1,
+    const int64_t* q1, const double* alpha1, const double* k2, const int64_t* q2,
+    const double* alpha2, int32_t qmul, const double* hl, int32_t wl, const double* hr,
+    int32_t wr, int32_t* flag, const double* wv1, const double* wv2, const double* mid_host,
+    const double* wcell1_host, const double* wcell2_host, double volume, double* work,
+    double* rc_out, double* stats, void* stream) {
+  int rc = xstencil_args(src, dst, dims, order, qmul, hl, wl, hr, wr);
+  if (rc) return rc;
+  VPB_REQUIRE(rc_out != nullptr, "null pointer");
+  const int64_t cc = (dims[0] / order) * (dims[1] / order);
+  const int64_t len = vpb_dg_xstencil_density_work_len(dims, order);
+  VPB_REQUIRE(len > 0, "cannot plan the x-plane launch");
+  const int64_t nblk = len / (cc + 1);
+  XDensity dn;
+  rc = xdensity_setup(&dn, order, wv1, wv2, mid_host, wcell1_host, wcell2_host, work, nblk, cc);
+  if (rc) return rc;
+  int64_t used = 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const XcStencil sx{qmul, hl, hr, wl, wr};
+  VPB_XPLANE_SWITCH(order, rc = (launch_xcomp<PP, true, true>(
+                               src, dst, dims, dims[2] * dims[3], xcomp_whole_field(dims, PP), k1,
+                               q1, alpha1, k2, q2, alpha2, flag, dn, 0, st, &used, sx)));
   if (rc) return rc;
   VPB_REQUIRE(used == nblk, "x-plane launch plan changed (%lld vs %lld CTAs)", (long long)used,
               (long long)nblk);

@@ -254,6 +254,38 @@ class CudaOps:
                                              f2.data_ptr(), self._device.stream()),
                 "vpb_dg_sweep_vplane")
 
+    # -- three-cell x-plane stencil with x1 halos (merged / single x half steps)
+    def stencil_tables(self, tab, single: bool) -> torch.Tensor:
+        """[n][3][p][p]: {AA, AB+BA, BB} (merged pair) or {0, A, B} (one sweep)."""
+        L = self._lib
+        p = tab.order
+        out = torch.empty((tab.n, 3, p, p), dtype=torch.float64, device=tab.a.device)
+        fn = self.lib.vpb_dg_single_tables if single else self.lib.vpb_dg_compose_tables
+        L.check(fn(tab.a.data_ptr(), tab.b.data_ptr(), tab.n, p, out.data_ptr(),
+                   self._device.stream()), "vpb_dg_compose_tables")
+        return out
+
+    def xstencil_work(self, dims, order) -> int:
+        return int(self.lib.vpb_dg_xstencil_density_work_len(self._lib.dims(dims), order))
+
+    def xstencil(self, src, dst, dims, order, k1, t1, k2, t2, qmul, hl, wl, hr, wr, flag,
+                 dens=None):
+        """dens: (wv1, wv2, mid, wc1, wc2, volume, work, rc_out, stats) or None."""
+        L = self._lib
+        head = (src.data_ptr(), dst.data_ptr(), L.dims(dims), order, k1.data_ptr(),
+                t1.q.data_ptr(), t1.alpha.data_ptr(), k2.data_ptr(), t2.q.data_ptr(),
+                t2.alpha.data_ptr(), qmul, hl.data_ptr() if wl else None, wl,
+                hr.data_ptr() if wr else None, wr, flag.data_ptr())
+        if dens is None:
+            L.check(self.lib.vpb_dg_sweep_xstencil(*head, self._device.stream()),
+                    "vpb_dg_sweep_xstencil")
+            return
+        wv1, wv2, mid, wc1, wc2, volume, work, rc_out, stats = dens
+        L.check(self.lib.vpb_dg_sweep_xstencil_density(
+            *head, wv1.data_ptr(), wv2.data_ptr(), mid.ctypes.data, wc1.ctypes.data,
+            wc2.ctypes.data, volume, work.data_ptr(), rc_out.data_ptr(), stats.data_ptr(),
+            self._device.stream()), "vpb_dg_sweep_xstencil_density")
+
     def pack(self, axis, f, dims, order, cell0, width, buf):
         L = self._lib
         L.check(self.lib.vpb_halo_pack(axis, f.data_ptr(), L.dims(dims), order, cell0, width,
@@ -521,6 +553,174 @@ class ShardedSolver:
         for k, name in enumerate(self.names):
             if host[k]:
                 raise SubstepError(name, time_label)
+
+    # -- K steps with merged x half steps on the x1-sharded field -------------
+    def _stencil_ready(self) -> bool:
+        return (self.dec.sharded(0) and not self.dec.sharded(1)
+                and hasattr(self.ops, "xstencil") and self.grid.ndim == 4)
+
+    def _stencil_setup(self, tau: float):
+        """Tables of the three-cell x passes and their x1 halo widths."""
+        key = ("stencil", float(tau))
+        if key not in self._xtab:
+            t1, _ = self.x_tables(0, tau)
+            t2, _ = self.x_tables(1, tau)
+            q1 = self.ops.tables_q(t1)
+            out = {}
+            for qmul, single in ((1, True), (2, False)):
+                q = qmul * np.asarray(q1)
+                wl = max(0, int(q.max()) + 2) if q.size else 0
+                wr = max(0, -int(q.min())) if q.size else 0
+                out[qmul] = (self.ops.stencil_tables(t1, single),
+                             self.ops.stencil_tables(t2, single), wl, wr)
+            self._xtab[key] = (t1, t2, out)
+        return self._xtab[key]
+
+    def _merged_halo_fits(self, tau: float) -> bool:
+        _, _, tabs = self._stencil_setup(tau)
+        _, _, wl, wr = tabs[2]
+        cells_min = min(c1 - c0 for r in range(self.dec.world)
+                        for (c0, c1) in [self.dec.cells(r, 0)])
+        return max(wl, wr) <= cells_min
+
+    def _density_consts(self):
+        if getattr(self, "_dens", None) is None:
+            from .grid import gauss_nodes
+            from .poisson import _lagrange_row, geometry
+
+            p = self.order
+            nodes, _ = gauss_nodes(p)
+            mid = np.ascontiguousarray(_lagrange_row(nodes, 0.5))
+            cells = [np.ascontiguousarray(np.asarray(self.grid.axis_weights(a))[:p])
+                     for a in (0, 1)]
+            self._dens = (mid, cells[0], cells[1], geometry(self.grid).volume)
+        return self._dens
+
+    def _x_stencil_pass(self, tau: float, qmul: int, flag_slot, with_density: bool,
+                        flags_row: dict, stats_row: dict, rc_parts: dict) -> None:
+        """One x pass (qmul 1: an x half step; 2: the merged closing + opening
+        half steps) on every local shard: x1 halo exchange, then the
+        three-cell stencil kernel; the density epilogue fills rc_parts."""
+        t1, t2, tabs = self._stencil_setup(tau)
+        k1, k2, wl, wr = tabs[qmul]
+        p = self.order
+        cells_min = min(c1 - c0 for sh in self.shards.values() for (c0, c1) in [sh.cells[0]])
+        if max(wl, wr) > cells_min:
+            raise NotImplementedError(
+                f"halo of {max(wl, wr)} cells exceeds a shard of {cells_min} cells")
+        msgs, bufs = {}, {}
+        for r, sh in self.shards.items():
+            left, right = self.dec.neighbours(r, 0)
+            d = sh.dims
+            cl = d[0] // p
+            hd = list(d)
+            hd[0] = wl * p
+            send_l = torch.empty(int(np.prod(hd)), dtype=sh.f.dtype, device=sh.f.device)
+            recv_l = torch.empty_like(send_l)
+            hd[0] = wr * p
+            send_r = torch.empty(int(np.prod(hd)), dtype=sh.f.dtype, device=sh.f.device)
+            recv_r = torch.empty_like(send_r)
+            if wl:
+                self.ops.pack(0, sh.f, d, p, cl - wl, wl, send_l)
+            if wr:
+                self.ops.pack(0, sh.f, d, p, 0, wr, send_r)
+            msgs[r] = [(KIND_L, right, send_l, left, recv_l),
+                       (KIND_R, left, send_r, right, recv_r)]
+            bufs[r] = (recv_l, recv_r)
+        self.comm.exchange(msgs)
+        mid, wc1, wc2, volume = self._density_consts()
+        for r, sh in self.shards.items():
+            recv_l, recv_r = bufs[r]
+            fl = flags_row[r][flag_slot:flag_slot + 1]
+            dens = None
+            if with_density:
+                d = sh.dims
+                work = torch.empty(self.ops.xstencil_work(d, p), dtype=torch.float64,
+                                   device=sh.f.device)
+                rc = torch.empty((d[1] // p) * (d[0] // p), dtype=torch.float64,
+                                 device=sh.f.device)
+                dens = (self.wv1, self.wv2, mid, wc1, wc2, volume, work, rc, stats_row[r])
+                rc_parts[r] = rc
+            self.ops.xstencil(sh.f, sh.buf, sh.dims, p, k1, t1, k2, t2, qmul, recv_l, wl,
+                              recv_r, wr, fl, dens)
+            sh.swap()
+
+    def _gather_rc(self, rc_parts: dict) -> torch.Tensor:
+        """Shard cell-centre density slabs [C2][C1 local] -> full [C2][C1]."""
+        p = self.order
+        C1, C2 = self.n1 // p, self.n2 // p
+        m = max((b0 - a0) * C2 for r in range(self.dec.world)
+                for (a0, b0) in [self.dec.cells(r, 0)])
+        locs = {}
+        for r, rc in rc_parts.items():
+            pad = torch.zeros(m, dtype=torch.float64, device=rc.device)
+            pad[: rc.numel()] = rc
+            locs[r] = pad
+        parts = self.comm.allgather(locs)
+        full = torch.empty((C2, C1), dtype=torch.float64, device=self.device)
+        for r, part in enumerate(parts):
+            a0, b0 = self.dec.cells(r, 0)
+            full[:, a0:b0] = part[: (b0 - a0) * C2].view(C2, b0 - a0)
+        return full.view(-1)
+
+    def advance(self, tau: float, nsteps: int, first_step: int | None = None) -> None:
+        """``nsteps`` Strang steps (driver.advance on the sharded field).
+
+        x1-sharded fields run the single-GPU pass structure: one x pass per
+        step boundary (the closing x half step of step m and the opening one
+        of step m+1 as composed three-cell stencils, "fast" arithmetic), each
+        after one x1 halo exchange, with the density as its epilogue; the v
+        passes are local.  Other decompositions run ``step`` in a loop."""
+        from .driver import ARITH, SubstepError
+        from .poisson import _warn_if_not_neutral, solve_into
+
+        if nsteps <= 0:
+            return
+        if not self._stencil_ready() or ARITH != "fast":
+            for m in range(nsteps):
+                self.step(tau, None if first_step is None else (first_step + m) * tau)
+            return
+        dev = self.device
+        flags = {r: torch.zeros((nsteps, 8), dtype=torch.int32, device=dev) for r in self.shards}
+        stats = {r: torch.zeros((nsteps, 4), dtype=torch.float64, device=dev)
+                 for r in self.shards}
+        solve_flags = torch.zeros((nsteps, 1), dtype=torch.int32, device=dev)
+        rc_parts = {}
+        self._x_stencil_pass(tau, 1, 0, True, {r: flags[r][0] for r in self.shards},
+                             {r: stats[r][0] for r in self.shards}, rc_parts)
+        for m in range(nsteps):
+            rc = self._gather_rc(rc_parts)
+            solve_into(rc, self.grid, self.e, None, solve_flags[m], centred=True)
+            for r, sh in self.shards.items():
+                tabs = [self.ops.tables(self._local_e(sh, d), tau, self.grid.axes[2 + d].h,
+                                        self.grid.dg_degree) for d in range(2)]
+                self.ops.vplane(sh.f, sh.buf, sh.dims, self.order, tabs[0], tabs[1],
+                                flags[r][m][3:4], flags[r][m][4:5])
+                sh.swap()
+            if m + 1 < nsteps and self._merged_halo_fits(tau):
+                # closing of step m + opening of step m+1, one pass
+                rc_parts = {}
+                self._x_stencil_pass(tau, 2, 5, True, {r: flags[r][m] for r in self.shards},
+                                     {r: stats[r][m + 1] for r in self.shards}, rc_parts)
+            elif m + 1 < nsteps:  # the doubled reach needs more halo than a shard holds
+                self._x_stencil_pass(tau, 1, 5, False, {r: flags[r][m] for r in self.shards},
+                                     {}, {})
+                rc_parts = {}
+                self._x_stencil_pass(tau, 1, 0, True, {r: flags[r][m + 1] for r in self.shards},
+                                     {r: stats[r][m + 1] for r in self.shards}, rc_parts)
+            else:
+                self._x_stencil_pass(tau, 1, 5, False, {r: flags[r][m] for r in self.shards},
+                                     {}, {})
+        for r in self.shards:
+            flags[r][:, 2:3] = torch.maximum(flags[r][:, 2:3], solve_flags)
+        fl = self.comm.allreduce(flags, "max").cpu().numpy()
+        st = self.comm.allreduce(stats, "sum").cpu().numpy()
+        for m in range(nsteps):
+            _warn_if_not_neutral(float(st[m, 0]))
+            for k, name in enumerate(self.names):
+                if fl[m, k]:
+                    raise SubstepError(name, None if first_step is None
+                                       else (first_step + m) * tau)
 
     def diagnostics(self, time: float = 0.0) -> dict:
         """Global conserved quantities (driver.py:279-316)."""

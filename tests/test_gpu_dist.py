@@ -57,6 +57,30 @@ def test_sharded_steps_match_single_gpu_step(p1, p2):
         assert got[k] == pytest.approx(getattr(rec, k), rel=1e-12), k
 
 
+@pytest.mark.parametrize("p1,tau", [(2, TAU), (4, TAU), (2, 1.7), (4, 0.0)])
+def test_sharded_advance_with_merged_stencil_passes_matches_single_gpu(p1, tau):
+    """x1-sharded advance(): x1 halo exchange + the three-cell stencil kernel
+    (single x half steps and merged pairs, density epilogue) against the
+    single-GPU advance() in the same ("fast") arithmetic."""
+    prob, grid, solver, f0 = setup(p1, 1)
+    assert solver._stencil_ready()
+    solver.advance(tau, 4)
+    f = vpb.advance(f0, tau, 4)
+    assert max_rel(solver.gather(), f.numpy()) <= 1e-13
+    got = solver.diagnostics(4 * tau)
+    rec = vpb.diagnostics(f, 4 * tau)
+    for k in ("mass", "l1_norm", "l2_norm", "kinetic_energy", "electric_energy"):
+        assert got[k] == pytest.approx(getattr(rec, k), rel=1e-12), k
+
+
+def test_sharded_advance_reports_nonfinite_substep():
+    prob, grid, solver, f0 = setup(2, 1)
+    sh = solver.shards[1]
+    sh.f[1234] = float("nan")
+    with pytest.raises(vpb.SubstepError, match=r"x1 half \(open\)"):
+        solver.advance(TAU, 3, first_step=2)
+
+
 def test_sharded_initialize_is_the_shard_of_the_global_initial_state():
     prob, grid, solver, f0 = setup(4, 2)
     solver.initialize(prob)
