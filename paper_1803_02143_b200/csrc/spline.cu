@@ -283,6 +283,64 @@ __device__ __forceinline__ void iir_solve(double* y, const int YS, const int n, 
   }
 }
 
+// Two recursive-filter solves (the double sweep's (6 T^-1)^2 up to the gain)
+// in one causal and one anticausal pass: y1 <- u + z1 y1, y2 <- y1 + z1 y2
+// advance together, so every point is loaded and stored once per direction
+// and the two chains overlap.  The periodic start values come from a 64-point
+// warm-up over the wrapping end (y1 needs 32 terms, y2 32 terms of an
+// accurate y1: z1^32 ~ 5e-19).  Requires n >= 64 (else two iir_solve calls).
+__device__ __forceinline__ void iir_solve2(double* y, const int YS, const int n, const double z1) {
+  constexpr int U = 8;
+  double p1 = 0.0, p2 = 0.0;
+  for (int k = n - 64; k < n; k += U) {
+    double u[U];
+#pragma unroll
+    for (int r = 0; r < U; ++r) u[r] = y[(k + r) * YS];
+#pragma unroll
+    for (int r = 0; r < U; ++r) {
+      p1 = fma(z1, p1, u[r]);
+      p2 = fma(z1, p2, p1);
+    }
+  }
+  for (int k = 0; k < n; k += U) {
+    double u[U];
+#pragma unroll
+    for (int r = 0; r < U; ++r) u[r] = y[(k + r) * YS];
+#pragma unroll
+    for (int r = 0; r < U; ++r) {
+      p1 = fma(z1, p1, u[r]);
+      p2 = fma(z1, p2, p1);
+      u[r] = p2;
+    }
+#pragma unroll
+    for (int r = 0; r < U; ++r) y[(k + r) * YS] = u[r];
+  }
+  double q1 = 0.0, q2 = 0.0;
+  for (int k = 64 - U; k >= 0; k -= U) {
+    double u[U];
+#pragma unroll
+    for (int r = 0; r < U; ++r) u[r] = y[(k + r) * YS];
+#pragma unroll
+    for (int r = U - 1; r >= 0; --r) {
+      q1 = fma(z1, q1, u[r]);
+      q2 = fma(z1, q2, q1);
+    }
+  }
+  for (int k = n - U; k >= 0; k -= U) {
+    double u[U];
+#pragma unroll
+    for (int r = 0; r < U; ++r) u[r] = y[(k + r) * YS];
+#pragma unroll
+    for (int r = U - 1; r >= 0; --r) {
+      q1 = fma(z1, q1, u[r]);
+      q2 = fma(z1, q2, q1);
+      u[r] = q2;
+    }
+#pragma unroll
+    for (int r = 0; r < U; ++r) y[(k + r) * YS] = u[r];
+  }
+}
+
 template <bool CONTIG, bool PCR, bool DBL = false>
 __global__ void __launch_bounds__(kSplineT)
     spline_tile_kernel(SplineTileArgs a, const __grid_constant__ CUtensorMap tmap) {
@@ -382,8 +440,16 @@ __global__ void __launch_bounds__(kSplineT)
       const double* pk = a.fac + 4 * n + 7;
       if (a.iir) {
         const double z1 = pk[kPcrLevels + 2];  // z1^1 of the power table
-        iir_solve(y, YS, n, z1);
-        if constexpr (DBL) iir_solve(y, YS, n, z1);
+        if constexpr (DBL) {
+          if (n >= 64) {
+            iir_solve2(y, YS, n, z1);
+          } else {
+            iir_solve(y, YS, n, z1);
+            iir_solve(y, YS, n, z1);
+          }
+        } else {
+          iir_solve(y, YS, n, z1);
+        }
         wscale = -6.0 * z1;
       } else {
         pcr_level<1>(y, YS, n, pk[0]);

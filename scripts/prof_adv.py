@@ -16,6 +16,7 @@ def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--problem", default="landau4d")
     ap.add_argument("--order", type=int, default=3)
+    ap.add_argument("--method", default="dg")
     ap.add_argument("--dofs", type=int, nargs=4, default=[192, 192, 48, 48])
     ap.add_argument("--tau", type=float, default=0.05)
     ap.add_argument("--steps", type=int, default=3)
@@ -25,7 +26,8 @@ def main() -> None:
     import paper_1803_02143_b200 as vpb
 
     prob = vpb.problem_spec(args.problem)
-    grid = vpb.make_grid(prob, "dg", tuple(args.dofs), dg_order=args.order)
+    grid = vpb.make_grid(prob, args.method, tuple(args.dofs),
+                         dg_order=args.order if args.method == "dg" else 0)
     f = vpb.initialize(prob, grid)
     f = vpb.advance(f, args.tau, args.steps, consume=True)
     torch.cuda.synchronize()
