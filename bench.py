@@ -8,9 +8,10 @@ One "step" is one Strang step of the reference's ``strang_step`` (six
 sweeps, density, field solve, v-shift tables, the non-finite checks).  The
 timed K steps run through ``advance(field, tau, K)``, the public multi-step
 API (the reference's ``run`` loop without diagnostics): adjacent x half steps
-of consecutive steps share one HBM pass; every sweep is still performed and
-the result is bitwise that of K ``strang_step`` calls with the same density
-path.  ``per_call`` in the JSON line times K separate
+of consecutive steps share one HBM pass ("fast" arithmetic: composed
+three-cell stencils, equal to the separate sweeps up to round-off; with
+VPB_ARITH=exact bitwise the K ``strang_step`` calls).  K defaults to the
+configuration's BASELINE step count (config 2: 100 steps).  ``per_call`` in the JSON line times K separate
 ``strang_step(consume=True)`` calls (what the reference's ``bench_step``
 times, /root/reference/pkg/src/slvp/bench.py:54-68); ``--per-step`` makes
 that the headline.  The default workload is BASELINE config 2 (Landau 4D,
@@ -37,9 +38,9 @@ reference's strang_step on every host thread, on a bounded scaled sample of
 the same configuration (oracle/refarm.py).
 
 Multi-GPU (torchrun, N > 1): the dG field is sharded along x1 (x1 x x2 on
-8 GPUs) with NCCL halo exchange and a rho all-gather
-(paper_1803_02143_b200.dist); the global grid is fixed (``scaling:
-strong``).  ``--replicas`` runs N independent full-size replicas instead.
+8 GPUs when the merged pass's halo does not fit an x1 shard) with NCCL halo
+exchange and a rho all-gather (paper_1803_02143_b200.dist,
+ShardedSolver.advance); the global grid is fixed (``scaling: strong``).  ``--replicas`` runs N independent full-size replicas instead.
 """
 
 from __future__ import annotations
@@ -63,15 +64,15 @@ UNIT = "DOF-updates/s"
 
 CONFIGS = {
     # BASELINE.json configs (degree 2 == dg_order 3)
-    "cfg1": dict(problem="landau4d", method="dg", dofs=48, order=3, tau=0.1,
+    "cfg1": dict(problem="landau4d", method="dg", dofs=48, order=3, tau=0.1, nsteps=20,
                  label="BASELINE config 1: Landau 4D, 16^4 cells, degree 2 (48^4 dofs), dt=0.1"),
-    "cfg2": dict(problem="landau4d", method="dg", dofs=192, order=3, tau=0.05,
+    "cfg2": dict(problem="landau4d", method="dg", dofs=192, order=3, tau=0.05, nsteps=100,
                  label="BASELINE config 2: Landau 4D, 64^4 cells, degree 2 (192^4 = 1.36e9 dofs), dt=0.05"),
-    "cfg3": dict(problem="twostream4d_baseline", method="dg", dofs=128, order=2, tau=0.1,
+    "cfg3": dict(problem="twostream4d_baseline", method="dg", dofs=128, order=2, tau=0.1, nsteps=200,
                  label="BASELINE config 3: two-stream 4D, 64^4 cells, degree 1 (128^4 dofs), dt=0.1"),
-    "cfg4": dict(problem="landau4d", method="spline", dofs=128, order=0, tau=0.1,
+    "cfg4": dict(problem="landau4d", method="spline", dofs=128, order=0, tau=0.1, nsteps=50,
                  label="BASELINE config 4: Landau 4D cubic spline, 128^4 points, dt=0.1"),
-    "cfg5": dict(problem="landau4d", method="dg", dofs=288, order=3, tau=0.05,
+    "cfg5": dict(problem="landau4d", method="dg", dofs=288, order=3, tau=0.05, nsteps=20,
                  label="BASELINE config 5: Landau 4D, 96^4 cells, degree 2 (288^4 = 6.9e9 dofs), dt=0.05"),
 }
 
@@ -641,7 +642,9 @@ def run_vpb(args, cfg_name: str, cfg: dict) -> None:
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default: the configuration's BASELINE step count, "
+                         "cfg1 20, cfg2 100, cfg3 200, cfg4 50, cfg5 20)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="vpb", choices=["vpb", "reference"])
@@ -661,6 +664,8 @@ def main() -> None:
         print("note: warmup raised to 3 (timing rules)", file=sys.stderr)
         args.warmup = 3
     cfg = CONFIGS[args.config]
+    if args.steps is None:
+        args.steps = cfg["nsteps"]
     if args.impl == "reference":
         run_reference_arm(args, args.config, cfg)
     else:
