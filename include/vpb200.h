@@ -225,8 +225,9 @@ int vpb_dg_single_tables(const double* a, const double* b, int64_t n, int32_t or
  * vpb_dg_compose_tables tables = the merged closing + opening x half steps
  * (vpb_dg_sweep_xcomp); qmul = 1 with vpb_dg_single_tables = one x half step
  * (_advect_space, driver.py:220-228).  x1 cells -wl..-1 and C1..C1+wr-1 come
- * from hl / hr in the vpb_halo_pack layout [plane][x2 row][w*p]; the row is
- * not periodic.  The _density variant adds the epilogue of
+ * from hl / hr in the vpb_halo_pack layout [plane][x2 row][w*p] (16-byte
+ * aligned; p*p*w even, i.e. even widths for odd p), staged into shared
+ * memory with the rows; the row is not periodic.  The _density variant adds the epilogue of
  * vpb_dg_sweep_xplane_density for the shard's cells (rc_out: the shard's
  * [C2][C1 local] cell-centre slab; stats[0]: its share of the mean / volume). */
 int vpb_dg_sweep_xstencil(const double* src, double* dst, const int64_t dims[4], int32_t order,
@@ -234,7 +235,8 @@ int vpb_dg_sweep_xstencil(const double* src, double* dst, const int64_t dims[4],
                           const double* k2, const int64_t* q2, const double* alpha2, int32_t qmul,
                           const double* hl, int32_t wl, const double* hr, int32_t wr,
                           int32_t* flag, void* stream);
-int64_t vpb_dg_xstencil_density_work_len(const int64_t dims[4], int32_t order);
+int64_t vpb_dg_xstencil_density_work_len(const int64_t dims[4], int32_t order, int32_t wl,
+                                         int32_t wr);
 int vpb_dg_sweep_xstencil_density(const double* src, double* dst, const int64_t dims[4],
                                   int32_t order, const double* k1, const int64_t* q1,
                                   const double* alpha1, const double* k2, const int64_t* q2,

@@ -95,7 +95,8 @@ SIGNATURES = {
     "vpb_dg_sweep_xstencil": (c_int, [c_void_p, c_void_p, POINTER(c_int64), c_int32]
                               + [c_void_p] * 6 + [c_int32, c_void_p, c_int32, c_void_p, c_int32,
                                                   c_void_p, c_void_p]),
-    "vpb_dg_xstencil_density_work_len": (c_int64, [POINTER(c_int64), c_int32]),
+    "vpb_dg_xstencil_density_work_len": (c_int64, [POINTER(c_int64), c_int32, c_int32,
+                                                   c_int32]),
     "vpb_dg_sweep_xstencil_density": (c_int, [c_void_p, c_void_p, POINTER(c_int64), c_int32]
                                       + [c_void_p] * 6
                                       + [c_int32, c_void_p, c_int32, c_void_p, c_int32]

@@ -109,9 +109,16 @@ __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? 224 : 168)
                     const XcStencil sx) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int cell = P * n1;  // one x2 cell: P rows of n1 dofs
+  const int rl = n1, cells = cell;
   const int slot = G * cell;
   double* inb = reinterpret_cast<double*>(smem_raw);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(inb + nst * slot);
+  // HALO: the chunk's left / right x1 halo cells arrive by their own bulk
+  // copies (contiguous per chunk in the vpb_halo_pack layout) into
+  // [nst][G cells][P rows][w*P] regions next to the ring
+  const int hls = HALO ? G * P * sx.wl * P : 0, hrs = HALO ? G * P * sx.wr * P : 0;
+  double* hlb = inb + nst * slot;
+  double* hrb = hlb + nst * hls;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(hrb + nst * hrs);
 
   const int tid = threadIdx.x;
   const int it_begin = (int)(blockIdx.x * items_per_block);
@@ -150,8 +157,29 @@ __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? 224 : 168)
     while (sb >= C2) sb -= C2;
     const double* base = src + (int64_t)p_r.l * plane_elems;
     double* d = inb + p_st * slot;
-    mbar_arrive_expect_tx(bars + p_st, (uint32_t)ns * cell * 8u);
     const int run1 = min(ns, C2 - sb);
+    if constexpr (HALO) {
+      const int hcl = P * sx.wl * P, hcr = P * sx.wr * P;  // halo doubles per x2 cell
+      mbar_arrive_expect_tx(bars + p_st, (uint32_t)ns * (cell + hcl + hcr) * 8u);
+      const int64_t hb = (int64_t)p_r.l * C2;
+      if (hcl) {
+        double* hd = hlb + p_st * hls;
+        bulk_g2s(hd, sx.hl + (hb + sb) * hcl, (uint32_t)run1 * hcl * 8u, bars + p_st);
+        if (run1 < ns)
+          bulk_g2s(hd + run1 * hcl, sx.hl + hb * hcl, (uint32_t)(ns - run1) * hcl * 8u,
+                   bars + p_st);
+      }
+      if (hcr) {
+        double* hd = hrb + p_st * hrs;
+        bulk_g2s(hd, sx.hr + (hb + sb) * hcr, (uint32_t)run1 * hcr * 8u, bars + p_st);
+        if (run1 < ns)
+          bulk_g2s(hd + run1 * hcr, sx.hr + hb * hcr, (uint32_t)(ns - run1) * hcr * 8u,
+                   bars + p_st);
+      }
+    } else {
+      mbar_arrive_expect_tx(bars + p_st, (uint32_t)ns * cell * 8u);
+    }
+    {
     if (DENS)
       bulk_g2s_hint(d, base + (int64_t)sb * cell, (uint32_t)run1 * cell * 8u, bars + p_st,
                     pol_stream);
@@ -163,6 +191,7 @@ __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? 224 : 168)
                       pol_stream);
       else
         bulk_g2s(d + run1 * cell, base, (uint32_t)(ns - run1) * cell * 8u, bars + p_st);
+    }
     }
     if (++p_st == nst) p_st = 0;
     if (++p_k == p_r.nch) {
@@ -189,9 +218,8 @@ __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? 224 : 168)
   double T1[3][P][P], T2[3][P][P];
   bool ex1 = true, ex2 = true;
   int off0 = 0, off1 = 0, off2 = 0;  // element offsets of the three x1 source cells
-  // HALO: per source cell 0 = shared-memory row, 1 = left halo, 2 = right halo
-  int hw0 = 0, hw1 = 0, hw2 = 0;
-  int item_s0 = 0;
+  int hrs0 = 0, hrs1 = 0, hrs2 = 0;  // HALO: row strides of their regions
+
   double w0[P][P], w1[P][P];         // x1 results of source cells t-2, t-1
   bool bad = false;
   int st = 0;
@@ -219,22 +247,25 @@ __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? 224 : 168)
             T2[s][jj][m] = __ldg(k2 + (iv2 * 3 + s) * P * P + jj * P + m);
           }
       if constexpr (HALO) {
+        // source cell j = tid - Q - 2 + k lives in the rows (0 <= j < C1) or in a
+        // halo region; its row m2 of ring cell sc of slot st starts at
+        // hbase_k + ((st G + sc) P + m2) * hrs_k  (branch-free in the loop)
         const int lo = tid - sx.qmul * (int)q1[iv1] - 2;
-        auto place = [&](int j, int& off, int& hw) {
+        auto place = [&](int j, int& base, int& rs) {
           if (j < 0) {
-            hw = 1;
-            off = (j + sx.wl) * P;
+            base = (int)(hlb - inb) + (j + sx.wl) * P;
+            rs = sx.wl * P;
           } else if (j >= C1) {
-            hw = 2;
-            off = (j - C1) * P;
+            base = (int)(hrb - inb) + (j - C1) * P;
+            rs = sx.wr * P;
           } else {
-            hw = 0;
-            off = j * P;
+            base = j * P;
+            rs = n1;
           }
         };
-        place(lo, off0, hw0);
-        place(lo + 1, off1, hw1);
-        place(lo + 2, off2, hw2);
+        place(lo, off0, hrs0);
+        place(lo + 1, off1, hrs1);
+        place(lo + 2, off2, hrs2);
       } else {
         const int qq = (int)wrap_mod((int64_t)sx.qmul * q1[iv1], C1);
         int lo = tid - qq - 2;
@@ -246,7 +277,6 @@ __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? 224 : 168)
         off2 = up * P;
       }
     }
-    if constexpr (HALO) item_s0 = s0_of(r);
     double* outp = dst + ((int64_t)iv2 * mp.nv1_glob + iv1) * plane_elems;
     for (int k = 0; k < r.nch; ++k) {
       const int t0 = k * G;
@@ -258,37 +288,29 @@ __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? 224 : 168)
         constexpr bool E1 = decltype(ex1c)::value, E2 = decltype(ex2c)::value;
         for (int sc = 0; sc < ns; ++sc) {
           const int t = t0 + sc;
-          const double* rows = in + sc * cell;
+          const double* rows = in + sc * cells;
           double g[P][P];
-          int64_t hrow = 0;  // HALO: row index (plane, x2 cell, row 0) in the halo buffers
-          if constexpr (HALO) {
-            int sx2 = item_s0 + t;
-            while (sx2 >= C2) sx2 -= C2;
-            hrow = ((int64_t)r.l * C2 + sx2) * P;
-          }
-          auto load_src = [&](const double* row, int m2, int off, int hw, double (&u)[P]) {
-            if (!HALO || hw == 0) {
-              load_cell_row<P>(row + off, u);
-            } else {
-              const double* h = hw == 1 ? sx.hl + (hrow + m2) * (sx.wl * P) + off
-                                        : sx.hr + (hrow + m2) * (sx.wr * P) + off;
-#pragma unroll
-              for (int m = 0; m < P; ++m) u[m] = __ldg(h + m);
-            }
+          // HALO: (st G + sc) P = first row index of this ring cell in every region
+          const int hrow0 = HALO ? (st * G + sc) * P : 0;
+          auto src_row = [&](const double* row, int m2, int off, int rs) -> const double* {
+            if constexpr (HALO)
+              return inb + off + (hrow0 + m2) * rs;
+            else
+              return row + off;
           };
           // composed x1 stencil on this source x2 cell: g[m2][jj]
 #pragma unroll
           for (int m2 = 0; m2 < P; ++m2) {
-            const double* row = rows + m2 * n1;
+            const double* row = rows + m2 * rl;
             double u2[P];
-            load_src(row, m2, off2, hw2, u2);
+            load_cell_row<P>(src_row(row, m2, off2, hrs2), u2);
             if constexpr (E1) {
 #pragma unroll
               for (int jj = 0; jj < P; ++jj) g[m2][jj] = u2[jj];
             } else {
               double u0[P], u1[P];
-              load_src(row, m2, off0, hw0, u0);
-              load_src(row, m2, off1, hw1, u1);
+              load_cell_row<P>(src_row(row, m2, off0, hrs0), u0);
+              load_cell_row<P>(src_row(row, m2, off1, hrs1), u1);
 #pragma unroll
               for (int jj = 0; jj < P; ++jj) {
                 double acc = T1[0][jj][0] * u0[0];
@@ -408,7 +430,7 @@ struct XcLaunch {
 };
 
 template <int P, bool DENS, bool HALO = false>
-static int plan_xcomp(const int64_t dims[4], int64_t nitems, XcLaunch* L) {
+static int plan_xcomp(const int64_t dims[4], int64_t nitems, XcLaunch* L, int hcells = 0) {
   const int n1 = (int)dims[0];
   const int C1 = n1 / P;
   const int C2 = (int)(dims[1] / P);
@@ -428,7 +450,10 @@ static int plan_xcomp(const int64_t dims[4], int64_t nitems, XcLaunch* L) {
   L->threads = ((C1 + 31) / 32) * 32;
   L->nst = std::max(2, std::min(8, env_st));
   const size_t cell_bytes = (size_t)P * n1 * 8;
-  auto smem_for = [&](int g) { return (size_t)L->nst * g * cell_bytes + L->nst * 8; };
+  // hcells: x1 halo cells (left + right) staged with every x2 cell
+  auto smem_for = [&](int g) {
+    return (size_t)L->nst * g * (cell_bytes + (size_t)hcells * P * P * 8) + L->nst * 8;
+  };
   int G = std::max<int>(2, (int)(env_chunk / cell_bytes));
   G = std::min(G, C2);
   while (G > 1 && (int)smem_for(G) > env_smem) --G;
@@ -463,7 +488,7 @@ static int launch_xcomp(const double* src, double* dst, const int64_t dims[4], i
                         const XcStencil& sx = XcStencil{2, nullptr, nullptr, 0, 0}) {
   if (nitems == 0) return VPB_OK;
   XcLaunch L;
-  int rc = plan_xcomp<P, DENS, HALO>(dims, nitems, &L);
+  int rc = plan_xcomp<P, DENS, HALO>(dims, nitems, &L, HALO ? sx.wl + sx.wr : 0);
   if (rc) return rc;
   dg_xcomp_kernel<P, DENS, HALO><<<(unsigned)L.blocks, L.threads, L.smem, st>>>(
       src, dst, (int)dims[0], (int)(dims[1] / P), L.G, L.nst, nitems, L.ppb, mp, k1, q1, al1, k2,
@@ -478,9 +503,9 @@ inline XcMap xcomp_whole_field(const int64_t dims[4], int P) {
 }
 
 template <int P, bool HALO = false>
-static int xcomp_density_len(const int64_t dims[4], int64_t* len) {
+static int xcomp_density_len(const int64_t dims[4], int64_t* len, int hcells = 0) {
   XcLaunch L;
-  int rc = plan_xcomp<P, true, HALO>(dims, dims[2] * dims[3], &L);
+  int rc = plan_xcomp<P, true, HALO>(dims, dims[2] * dims[3], &L, hcells);
   if (rc) return rc;
   const int64_t cc = (dims[0] / P) * (dims[1] / P);
   *len = L.blocks * (cc + 1);
@@ -579,6 +604,12 @@ static int xstencil_args(const double* src, const double* dst, const int64_t dim
   if (rc) return rc;
   VPB_REQUIRE(qmul == 1 || qmul == 2, "qmul must be 1 or 2");
   VPB_REQUIRE(wl >= 0 && wr >= 0 && (wl == 0 || hl) && (wr == 0 || hr), "bad halo");
+  VPB_REQUIRE((order * order * wl) % 2 == 0 && (order * order * wr) % 2 == 0,
+              "halo cells of %d x %d dofs per x2 cell must be 16-byte multiples (even widths "
+              "for odd orders)", order, order);
+  VPB_REQUIRE((reinterpret_cast<uintptr_t>(hl) & 15) == 0 &&
+                  (reinterpret_cast<uintptr_t>(hr) & 15) == 0,
+              "halo buffers must be 16-byte aligned");
   VPB_REQUIRE(wl <= dims[0] / order && wr <= dims[0] / order, "halo wider than the shard");
   return VPB_OK;
 }
@@ -600,11 +631,12 @@ extern "C" int vpb_dg_sweep_xstencil(const double* src, double* dst, const int64
   return rc;
 }
 
-extern "C" int64_t vpb_dg_xstencil_density_work_len(const int64_t dims[4], int32_t order) {
+extern "C" int64_t vpb_dg_xstencil_density_work_len(const int64_t dims[4], int32_t order,
+                                                    int32_t wl, int32_t wr) {
   if (order < 1 || order > kMaxOrder || dims[0] % order || dims[1] % order) return -1;
   int64_t len = -1;
   int rc = VPB_OK;
-  VPB_XPLANE_SWITCH(order, rc = (xcomp_density_len<PP, true>(dims, &len)));
+  VPB_XPLANE_SWITCH(order, rc = (xcomp_density_len<PP, true>(dims, &len, wl + wr)));
   return rc == VPB_OK ? len : -1;
 }
 
@@ -619,7 +651,7 @@ extern "C" int vpb_dg_sweep_xstencil_density(
   if (rc) return rc;
   VPB_REQUIRE(rc_out != nullptr, "null pointer");
   const int64_t cc = (dims[0] / order) * (dims[1] / order);
-  const int64_t len = vpb_dg_xstencil_density_work_len(dims, order);
+  const int64_t len = vpb_dg_xstencil_density_work_len(dims, order, wl, wr);
   VPB_REQUIRE(len > 0, "cannot plan the x-plane launch");
   const int64_t nblk = len / (cc + 1);
   XDensity dn;

@@ -265,8 +265,9 @@ class CudaOps:
                    self._device.stream()), "vpb_dg_compose_tables")
         return out
 
-    def xstencil_work(self, dims, order) -> int:
-        return int(self.lib.vpb_dg_xstencil_density_work_len(self._lib.dims(dims), order))
+    def xstencil_work(self, dims, order, wl, wr) -> int:
+        return int(self.lib.vpb_dg_xstencil_density_work_len(self._lib.dims(dims), order, wl,
+                                                             wr))
 
     def xstencil(self, src, dst, dims, order, k1, t1, k2, t2, qmul, hl, wl, hr, wr, flag,
                  dens=None):
@@ -571,6 +572,9 @@ class ShardedSolver:
                 q = qmul * np.asarray(q1)
                 wl = max(0, int(q.max()) + 2) if q.size else 0
                 wr = max(0, -int(q.min())) if q.size else 0
+                if self.order % 2:  # halo blocks staged by bulk copies: 16-byte multiples
+                    wl += wl % 2
+                    wr += wr % 2
                 out[qmul] = (self.ops.stencil_tables(t1, single),
                              self.ops.stencil_tables(t2, single), wl, wr)
             self._xtab[key] = (t1, t2, out)
@@ -635,7 +639,7 @@ class ShardedSolver:
             dens = None
             if with_density:
                 d = sh.dims
-                work = torch.empty(self.ops.xstencil_work(d, p), dtype=torch.float64,
+                work = torch.empty(self.ops.xstencil_work(d, p, wl, wr), dtype=torch.float64,
                                    device=sh.f.device)
                 rc = torch.empty((d[1] // p) * (d[0] // p), dtype=torch.float64,
                                  device=sh.f.device)
