@@ -258,8 +258,7 @@ int vpb_spline_sweep_axis(int32_t axis, const double* src, double* dst, const in
  * evaluation of _kernels.pyx:37-93 commute, so the recursive-filter solve
  * runs twice and the evaluation is the 7-tap self-convolution of the weights
  * at offset 2 j0.  Equal to two vpb_spline_sweep_axis calls up to round-off.
- * Needs n % 16 == 0, n >= 32 (and n / 32 in {1, 2, 4, 8} for axis 0);
- * VPB_ERR_UNSUPPORTED otherwise. */
+ * Needs n % 16 == 0, n >= 32; VPB_ERR_UNSUPPORTED otherwise. */
 int vpb_spline_sweep_axis2(int32_t axis, const double* src, double* dst, const int64_t dims[4],
                            const double* values, double scale, double h, int32_t* flag,
                            void* stream);

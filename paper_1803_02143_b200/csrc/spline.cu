@@ -558,12 +558,15 @@ __global__ void __launch_bounds__(kSplineT)
     }
     const int j0 = (int)wrap_mod((int64_t)off - 1, n);
     j0s[t] = j0;
-    if constexpr (DBL && !CONTIG) {
+    if constexpr (DBL) {
       // out_i = sum_m c_m w2[2 j0 + i + m], m = 0..6: a 7-value sliding window
+      // (contiguous axis: out_i overwrites w2[2 j0 + i] in place, rotated)
       const double wv[4] = {w0, w1, w2, w3};
       double c[7];
       spline_weights2(wv, c);
       int jn = (2 * j0) % n;
+      if (CONTIG) j0s[t] = jn;
+      int pw = jn;  // CONTIG: in-place position of out_k
       auto nxt = [&]() {
         const double v = y[jn * YS];
         if (++jn == n) jn = 0;
@@ -572,8 +575,16 @@ __global__ void __launch_bounds__(kSplineT)
       double sv[6], win[6];
 #pragma unroll
       for (int r = 0; r < 6; ++r) win[r] = sv[r] = nxt();
-      const int64_t outer = L / a.S, inner = L - outer * a.S;
+      const int64_t outer = CONTIG ? 0 : L / a.S, inner = CONTIG ? 0 : L - outer * a.S;
       const int64_t obase = outer * a.S * n + inner;
+      auto put = [&](int k, double o) {
+        if (CONTIG) {
+          y[pw] = o;
+          if (++pw == n) pw = 0;
+        } else {
+          __stcs(a.dst + obase + (int64_t)k * a.S, o);
+        }
+      };
       auto emit = [&](double v6) {
         double o = c[0] * win[0];
 #pragma unroll
@@ -594,7 +605,7 @@ __global__ void __launch_bounds__(kSplineT)
 #pragma unroll
         for (int r = 0; r < E; ++r) o[r] = emit(v[r]);
 #pragma unroll
-        for (int r = 0; r < E; ++r) __stcs(a.dst + obase + (int64_t)(k + r) * a.S, o[r]);
+        for (int r = 0; r < E; ++r) put(k + r, o[r]);
       }
       for (; k < n; ++k) {
         const int back = k - (n - 6);
@@ -607,7 +618,7 @@ __global__ void __launch_bounds__(kSplineT)
           for (int r = 1; r < 6; ++r)
             if (back == r) v6 = sv[r];
         }
-        __stcs(a.dst + obase + (int64_t)k * a.S, emit(v6));
+        put(k, emit(v6));
       }
     } else {
 
@@ -924,6 +935,8 @@ static int launch_spline(SplineTileArgs a, bool contig, bool exact, cudaStream_t
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(spline_tile_kernel<false, true, true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(spline_tile_kernel<true, true, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr = true;
   }
   static const bool force_exact = getenv("VPB_SPLINE_EXACT") != nullptr;
@@ -949,7 +962,12 @@ static int launch_spline(SplineTileArgs a, bool contig, bool exact, cudaStream_t
   }
   static const bool no_rows = getenv("VPB_SPLINE_TILES") != nullptr;
   const int npt = a.n / 32;
-  const bool rows_ok = contig && pcr && !no_rows && a.n % 32 == 0 &&
+  // double sweeps on the contiguous axis: one line per lane in a padded
+  // shared-memory tile with the fused double recursion (1.19 ms at config 4)
+  // beats the warp-per-line rows kernel (1.30 ms, shuffle-latency bound);
+  // VPB_SPLINE_DBL_ROWS=1 selects the rows kernel
+  static const bool dbl_rows = getenv("VPB_SPLINE_DBL_ROWS") != nullptr;
+  const bool rows_ok = contig && pcr && !no_rows && !(a.dbl && !dbl_rows) && a.n % 32 == 0 &&
                        (npt == 1 || npt == 2 || npt == 4 || npt == 8) &&
                        (reinterpret_cast<uintptr_t>(a.src) & 15) == 0;
   if (rows_ok) {
@@ -988,11 +1006,10 @@ static int launch_spline(SplineTileArgs a, bool contig, bool exact, cudaStream_t
     return launched("spline_rows_kernel");
   }
   if (a.dbl) {
-    if (contig) {
-      set_error("double spline sweep along the contiguous axis needs n / 32 in {1, 2, 4, 8}");
-      return VPB_ERR_UNSUPPORTED;
-    }
-    spline_tile_kernel<false, true, true><<<(unsigned)blocks, kSplineT, smem, st>>>(a, tmap);
+    if (contig)
+      spline_tile_kernel<true, true, true><<<(unsigned)blocks, kSplineT, smem, st>>>(a, tmap);
+    else
+      spline_tile_kernel<false, true, true><<<(unsigned)blocks, kSplineT, smem, st>>>(a, tmap);
     return launched("spline_tile_kernel");
   }
   if (contig) {

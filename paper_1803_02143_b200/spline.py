@@ -97,8 +97,4 @@ def sweep_spline2(grid, axis: int, src: torch.Tensor, dst: torch.Tensor, values:
 def double_sweep_ok(grid, axis: int) -> bool:
     """Whether :func:`sweep_spline2` supports this axis of the grid."""
     n = grid.dof(axis)
-    if n % 16 or n < 32:
-        return False
-    if device_axis(grid, axis) == 0:
-        return n % 32 == 0 and n // 32 in (1, 2, 4, 8)
-    return True
+    return n % 16 == 0 and n >= 32

@@ -608,6 +608,23 @@ def test_spline_double_sweep_advance_matches_strang_steps(monkeypatch, prob, dof
 
 @pytest.mark.parametrize("axis", [0, 1, 2, 3])
 def test_spline_double_sweep_equals_two_sweeps(axis):
+    _double_vs_two(axis)
+
+
+def test_spline_double_sweep_rows_kernel_equals_two_sweeps(monkeypatch):
+    """The warp-per-line rows kernel variant of the contiguous-axis double
+    sweep (VPB_SPLINE_DBL_ROWS; read once per process, so run in a child)."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, 'tests'); import test_gpu_step as t; "
+            "t._double_vs_two(0)")
+    env = dict(__import__("os").environ, VPB_SPLINE_DBL_ROWS="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+
+
+def _double_vs_two(axis):
     from paper_1803_02143_b200.spline import sweep_spline, sweep_spline2
     prob = vpb.problem_spec("landau4d")
     grid = vpb.make_grid(prob, "spline", (64, 32, 48, 32))
