@@ -314,6 +314,12 @@ class CudaOps:
 
         solve_into(rho, grid, e, stats, flag)
 
+    def field_solve_centred(self, grid, rc, e, flag):
+        """E from the cell-centre density of the fused x passes."""
+        from .poisson import solve_into
+
+        solve_into(rc, grid, e, None, flag, centred=True)
+
     def diag_work(self, dims) -> int:
         return int(self.lib.vpb_diag_work_len(self._lib.dims(dims)))
 
@@ -590,14 +596,16 @@ class ShardedSolver:
     def _density_consts(self):
         if getattr(self, "_dens", None) is None:
             from .grid import gauss_nodes
-            from .poisson import _lagrange_row, geometry
+            from .poisson import _lagrange_row
 
             p = self.order
             nodes, _ = gauss_nodes(p)
             mid = np.ascontiguousarray(_lagrange_row(nodes, 0.5))
             cells = [np.ascontiguousarray(np.asarray(self.grid.axis_weights(a))[:p])
                      for a in (0, 1)]
-            self._dens = (mid, cells[0], cells[1], geometry(self.grid).volume)
+            ax = self.grid.axes
+            volume = (ax[0].upper - ax[0].lower) * (ax[1].upper - ax[1].lower)
+            self._dens = (mid, cells[0], cells[1], float(volume))
         return self._dens
 
     def _x_stencil_pass(self, tau: float, qmul: int, flag_slot, with_density: bool,
@@ -676,7 +684,7 @@ class ShardedSolver:
         after one x1 halo exchange, with the density as its epilogue; the v
         passes are local.  Other decompositions run ``step`` in a loop."""
         from .driver import ARITH, SubstepError
-        from .poisson import _warn_if_not_neutral, solve_into
+        from .poisson import _warn_if_not_neutral
 
         if nsteps <= 0:
             return
@@ -694,7 +702,7 @@ class ShardedSolver:
                              {r: stats[r][0] for r in self.shards}, rc_parts)
         for m in range(nsteps):
             rc = self._gather_rc(rc_parts)
-            solve_into(rc, self.grid, self.e, None, solve_flags[m], centred=True)
+            self.ops.field_solve_centred(self.grid, rc, self.e, solve_flags[m])
             for r, sh in self.shards.items():
                 tabs = [self.ops.tables(self._local_e(sh, d), tau, self.grid.axes[2 + d].h,
                                         self.grid.dg_degree) for d in range(2)]

@@ -103,6 +103,68 @@ class NumpyOps:
         sl[axis] = slice(wl * order, wl * order + dims[axis])
         self._store(dst, dims, out[tuple(sl)], flag)
 
+    # -- three-cell x-plane stencil passes (ShardedSolver.advance) ------------
+    def stencil_tables(self, tab, single: bool):
+        a, b = tab.a, tab.b
+        if single:
+            return np.stack([np.zeros_like(a), a, b], axis=1)
+        return np.stack([a @ a, a @ b + b @ a, b @ b], axis=1)
+
+    def xstencil_work(self, dims, order, wl, wr):
+        return 1
+
+    def xstencil(self, src, dst, dims, order, k1, t1, k2, t2, qmul, hl, wl, hr, wr, flag,
+                 dens=None):
+        """x1 stencil with halos (cells c-Q-2 .. c-Q, Q = qmul q), then the
+        periodic x2 stencil, on the logical box; optional density epilogue."""
+        p = order
+        n1, n2, nv1, nv2 = dims
+        c1n, c2n = n1 // p, n2 // p
+        pieces = []
+        if wl:
+            pieces.append(_box(hl, (wl * p, n2, nv1, nv2)))
+        pieces.append(_box(src, dims))
+        if wr:
+            pieces.append(_box(hr, (wr * p, n2, nv1, nv2)))
+        ext = np.concatenate(pieces, axis=0).reshape(wl + c1n + wr, p, n2, nv1, nv2)
+        g = np.zeros((c1n, p, n2, nv1, nv2))
+        for iv1 in range(nv1):
+            qq = qmul * int(t1.q[iv1])
+            for k in range(3):
+                j = np.arange(c1n) - qq - 2 + k + wl
+                g[:, :, :, iv1, :] += np.einsum("jm,cmxv->cjxv", k1[iv1, k],
+                                                ext[:, :, :, iv1, :][j], optimize=False)
+        g2 = g.reshape(c1n, p, c2n, p, nv1, nv2)
+        o = np.zeros_like(g2)
+        for iv2 in range(nv2):
+            qq = qmul * int(t2.q[iv2])
+            for k in range(3):
+                j = (np.arange(c2n) - qq - 2 + k) % c2n
+                o[..., iv2] += np.einsum("jm,aibmv->aibjv", k2[iv2, k],
+                                         g2[..., iv2][:, :, j], optimize=False)
+        out = o.reshape(n1, n2, nv1, nv2)
+        self._store(dst, dims, out, flag)
+        if dens is not None:
+            wv1, wv2, mid, wc1, wc2, volume, work, rc_out, stats = dens
+            wa, wb = wv1.numpy(), wv2.numpy()
+            rc = np.einsum("aibjvw,i,j,v,w->ba", o, mid, mid, wa, wb, optimize=False)
+            rc_out.copy_(torch.from_numpy(np.ascontiguousarray(rc).reshape(-1)))
+            mean = np.einsum("aibjvw,i,j,v,w->", o, wc1, wc2, wa, wb, optimize=False)
+            stats[0] = float(mean) / volume
+
+    def vplane(self, src, dst, dims, order, t1, t2, f1, f2):
+        tmp = torch.empty_like(src)
+        self.sweep(2, src, tmp, dims, order, t1, f1)
+        self.sweep(3, tmp, dst, dims, order, t2, f2)
+
+    def field_solve_centred(self, grid, rc, e, flag):
+        og = core.OGrid(tuple(a.lower for a in grid.axes), tuple(a.upper for a in grid.axes),
+                        tuple(a.count for a in grid.axes), grid.method, grid.dg_degree)
+        c1n, c2n = grid.axes[0].count, grid.axes[1].count
+        logical = rc.numpy().reshape(c2n, c1n).T
+        comps = core.solve_poisson_centred(logical, og)
+        e.copy_(torch.from_numpy(np.concatenate([c.T.reshape(-1) for c in comps])))
+
     def density_work(self, dims):
         return 1
 

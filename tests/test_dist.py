@@ -104,6 +104,57 @@ def test_sharded_step_reports_nonfinite_on_every_shard():
         solver.step(TAU)
 
 
+@pytest.mark.parametrize("p1,tau", [(2, TAU), (4, TAU), (2, 1.3)])
+def test_virtual_sharded_advance_matches_oracle_steps(p1, tau):
+    """advance(): x1 halo exchange + merged three-cell stencil passes with the
+    density epilogue (oracle restatement of the kernels) vs oracle steps."""
+    grid, og = grids()
+    dec = dist.Decomposition(grid, p1, 1)
+    solver = dist.ShardedSolver(grid, dec, dist.VirtualComm(dec.world), range(dec.world),
+                                ops=NumpyOps(), device=torch.device("cpu"))
+    assert solver._stencil_ready()
+    solver.scatter(core.initialize(PROB, og))
+    solver.advance(tau, 3)
+    f = core.initialize(PROB, og)
+    for _ in range(3):
+        f = core.strang_step(f, og, tau)
+    assert max_rel(solver.gather(), f) <= 1e-13
+
+
+def _advance_worker(rank, world, port, outdir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as tdist
+
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        grid, og = grids()
+        dec = dist.Decomposition(grid, world, 1)
+        solver = dist.ShardedSolver(grid, dec, dist.TorchComm(), [rank], ops=NumpyOps(),
+                                    device=torch.device("cpu"))
+        solver.scatter(core.initialize(PROB, og))
+        solver.advance(TAU, 3)
+        np.save(os.path.join(outdir, f"a{rank}.npy"), solver.local_logical(rank))
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_two_rank_gloo_sharded_advance_equals_in_process(tmp_path):
+    """The TorchComm path of advance() (halo send/recv, centred-density
+    all-gather, flag / mean reductions) == the in-process VirtualComm run."""
+    port = _free_port()
+    mp.start_processes(_advance_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True,
+                       start_method="spawn")
+    grid, og = grids()
+    dec = dist.Decomposition(grid, 2, 1)
+    solver = dist.ShardedSolver(grid, dec, dist.VirtualComm(2), range(2), ops=NumpyOps(),
+                                device=torch.device("cpu"))
+    solver.scatter(core.initialize(PROB, og))
+    solver.advance(TAU, 3)
+    for r in range(2):
+        assert np.array_equal(np.load(tmp_path / f"a{r}.npy"), solver.local_logical(r))
+
+
 # ---- two real processes over gloo ---------------------------------------
 def _free_port() -> int:
     with socket.socket() as s:
