@@ -98,8 +98,11 @@ struct XcStencil {
 };
 
 // 224 registers at P >= 3 keep 3 CTAs of 96 threads (config 5) per SM
+#ifndef VPB_XCOMP_MAXNREG
+#define VPB_XCOMP_MAXNREG 224
+#endif
 template <int P, bool DENS, bool HALO = false>
-__global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? 224 : 168)
+__global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? VPB_XCOMP_MAXNREG : 168)
     dg_xcomp_kernel(const double* __restrict__ src, double* __restrict__ dst, int n1, int C2,
                     int G, int nst, int64_t nitems, int64_t items_per_block, const XcMap mp,
                     const double* __restrict__ k1, const int64_t* __restrict__ q1,
