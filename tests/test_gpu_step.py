@@ -396,6 +396,9 @@ ADVANCE_CASES = [
     (1, (12, 10, 8, 6), 0.37),
     (3, (24, 18, 15, 12), 0.37),    # v1 = 0 plane: alpha == 0 (exact shift) along x1
     (2, (16, 12, 6, 10), 0.0),      # tau = 0: every row an exact shift
+    (5, (20, 15, 10, 10), 0.37),    # high orders (register spills in the fused passes)
+    (7, (28, 14, 14, 7), 0.6),
+    (9, (18, 18, 9, 9), 0.37),
 ]
 
 
