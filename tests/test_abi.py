@@ -81,6 +81,26 @@ def test_argument_validation_without_device(lib):
     assert rc == 1
     assert lib.vpb_density_work_len(dims) > 0
     assert lib.vpb_diag_work_len(dims) == 3 * 48 * 48
+    # merged x passes: aliasing, orders, qmul, halo widths (all host-side checks)
+    rc = lib.vpb_dg_sweep_xcomp(16, 16, dims, 3, 1, 2, 3, 4, 5, 6, None, None)
+    assert rc == 1 and b"distinct" in lib.vpb_last_error()
+    rc = lib.vpb_dg_sweep_xcomp(16, 32, dims, 12, 1, 2, 3, 4, 5, 6, None, None)
+    assert rc == 1 and b"order" in lib.vpb_last_error()
+    rc = lib.vpb_dg_compose_tables(1, 2, 5, 0, 3, None)
+    assert rc == 1
+    rc = lib.vpb_dg_sweep_xstencil(16, 32, dims, 3, 1, 2, 3, 4, 5, 6, 3, None, 0, None, 0,
+                                   None, None)
+    assert rc == 1 and b"qmul" in lib.vpb_last_error()
+    # odd order: halo blocks must stay 16-byte multiples (even widths)
+    rc = lib.vpb_dg_sweep_xstencil(16, 32, dims, 3, 1, 2, 3, 4, 5, 6, 2, 64, 1, 64, 2,
+                                   None, None)
+    assert rc == 1 and b"16-byte" in lib.vpb_last_error()
+    rc = lib.vpb_dg_sweep_xstencil(16, 32, dims, 3, 1, 2, 3, 4, 5, 6, 2, 64, 20, 64, 2,
+                                   None, None)
+    assert rc == 1 and b"wider than the shard" in lib.vpb_last_error()
+    # spline double sweep: axis range
+    rc = lib.vpb_spline_sweep_axis2(5, 16, 32, dims, 1, 0.1, 0.5, None, None)
+    assert rc == 1
 
 
 def test_product_path_fails_loudly_without_cuda():
