@@ -12,6 +12,7 @@
 // spatial grid is at most a few hundred points per axis, so a tiled small
 // GEMM is both simpler and faster than an FFT plan at this size).
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -145,15 +146,72 @@ __global__ void zgemm_kernel(int64_t M, int64_t N, int64_t K, ZOp A, ZOp B, ZOp 
   }
 }
 
+// Shared-memory tiled variant: an 8 x 8 output tile per 64-thread CTA (more
+// CTAs than the 16 x 16 one-output-per-thread kernel for the <= 288-point
+// transforms of the field solve), K in steps of 16 staged through shared
+// memory; the k order of every sum is unchanged (ascending).
+constexpr int kZT = 8, kZK = 16;
+__global__ void __launch_bounds__(kZT * kZT)
+    zgemm_tiled_kernel(int64_t M, int64_t N, int64_t K, ZOp A, ZOp B, ZOp S, int has_scale,
+                       double* __restrict__ Cp, int64_t crs, int64_t ccs, int64_t czs,
+                       int real_out, int32_t* __restrict__ flag) {
+  __shared__ double2 as[kZT][kZK + 1];
+  __shared__ double2 bs[kZK][kZT + 1];
+  const int tx = threadIdx.x % kZT, ty = threadIdx.x / kZT;
+  const int64_t j = (int64_t)blockIdx.x * kZT + tx;
+  const int64_t i = (int64_t)blockIdx.y * kZT + ty;
+  const int z = blockIdx.z;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int64_t k0 = 0; k0 < K; k0 += kZK) {
+    // 64 threads stage an 8 x 16 slab of A and a 16 x 8 slab of B
+    for (int e = threadIdx.x; e < kZT * kZK; e += kZT * kZT) {
+      const int r = e / kZK, c = e % kZK;
+      const int64_t ai = (int64_t)blockIdx.y * kZT + r, ak = k0 + c;
+      as[r][c] = (ai < M && ak < K) ? zload(A, ai, ak, z) : make_double2(0.0, 0.0);
+      const int br = e / kZT, bc = e % kZT;
+      const int64_t bk = k0 + br, bj = (int64_t)blockIdx.x * kZT + bc;
+      double2 b = make_double2(0.0, 0.0);
+      if (bk < K && bj < N) {
+        b = zload(B, bk, bj, z);
+        if (has_scale) b = zmul(zload(S, bk, bj, z), b);
+      }
+      bs[br][bc] = b;
+    }
+    __syncthreads();
+    const int kn = (int)min((int64_t)kZK, K - k0);
+    for (int k = 0; k < kn; ++k) {
+      const double2 a = as[ty][k], b = bs[k][tx];
+      acc.x += a.x * b.x - a.y * b.y;
+      acc.y += a.x * b.y + a.y * b.x;
+    }
+    __syncthreads();
+  }
+  if (i >= M || j >= N) return;
+  int64_t e = i * crs + j * ccs + z * czs;
+  if (real_out) {
+    Cp[e] = acc.x;
+    report_flag(not_finite(acc.x), flag);
+  } else {
+    reinterpret_cast<double2*>(Cp)[e] = acc;
+  }
+}
+
 static int zgemm(int64_t M, int64_t N, int64_t K, int batch, ZOp A, ZOp B, const ZOp* S,
                  double* C, int64_t crs, int64_t ccs, int64_t czs, int real_out, int32_t* flag,
                  cudaStream_t st) {
-  dim3 blk(16, 16);
-  dim3 grd((unsigned)((N + 15) / 16), (unsigned)((M + 15) / 16), (unsigned)batch);
   ZOp s0 = S ? *S : ZOp{nullptr, 0, 0, 0, 0};
-  zgemm_kernel<<<grd, blk, 0, st>>>(M, N, K, A, B, s0, S != nullptr, C, crs, ccs, czs, real_out,
-                                    flag);
-  return launched("zgemm_kernel");
+  static const bool naive = getenv("VPB_ZGEMM_NAIVE") != nullptr;
+  if (naive) {
+    dim3 blk(16, 16);
+    dim3 grd((unsigned)((N + 15) / 16), (unsigned)((M + 15) / 16), (unsigned)batch);
+    zgemm_kernel<<<grd, blk, 0, st>>>(M, N, K, A, B, s0, S != nullptr, C, crs, ccs, czs,
+                                      real_out, flag);
+    return launched("zgemm_kernel");
+  }
+  dim3 grd((unsigned)((N + kZT - 1) / kZT), (unsigned)((M + kZT - 1) / kZT), (unsigned)batch);
+  zgemm_tiled_kernel<<<grd, kZT * kZT, 0, st>>>(M, N, K, A, B, s0, S != nullptr, C, crs, ccs,
+                                                czs, real_out, flag);
+  return launched("zgemm_tiled_kernel");
 }
 
 // Weighted mean of rho for the neutrality warning (poisson.py:143-160).
