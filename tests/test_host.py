@@ -208,3 +208,26 @@ def test_diagnostics_csv_and_meta_match_the_reference_cli_format(tmp_path):
     meta = out.with_suffix(".meta").read_text().split("\n")
     assert meta[:3] == [f"version = {vpb.__version__}", "command = run cfg.toml", "backend = cuda"]
     assert meta[3:6] == ["grid = dg", "tau = 0.05", "note = synthetic"]
+
+
+def test_bench_accounting_helpers():
+    """bench.py: sweeps per launch of each kernel group label, per-config
+    step defaults, and the committed ncu traffic lookup."""
+    import importlib.util
+    import json
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    spec = importlib.util.spec_from_file_location("bench_mod", root / "bench.py")
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    assert bench.sweeps_per_launch("sweep_x12x12_rho") == 4
+    assert bench.sweeps_per_launch("sweep_v12") == 2
+    assert bench.sweeps_per_launch("sweep_x1x2") == 2
+    assert bench.sweeps_per_launch("sweep_x1") == 1
+    assert {k: v["nsteps"] for k, v in bench.CONFIGS.items()} == {
+        "cfg1": 20, "cfg2": 100, "cfg3": 200, "cfg4": 50, "cfg5": 20}
+    traffic = json.loads((root / "profiles" / "traffic.json").read_text())
+    got = bench.load_traffic("cfg2", "sweep_x12x12_rho")
+    assert got == float(traffic["cfg2"]["sweep_x12x12_rho"]["dram_bytes_per_launch"])
+    assert bench.load_traffic("cfg2", "no_such_kernel") is None
