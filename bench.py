@@ -24,18 +24,24 @@ stream; max over ranks.  The field (10.9 GB) is ~87x the 126 MB L2, so no
 explicit L2 flush is needed.  SM clocks / throttle reasons are sampled with
 nvidia-smi during the timed region.
 
-``e2e``: the same steps with f resident in pinned HOST memory, i.e. each
-step copies f host->device, runs the step, and copies f back (what a
-reference user holding f on the host sees).
+``e2e``: Strang steps of a field resident in pinned HOST memory through the
+public ``host_steps(HostField, tau, K)`` (what a reference user holding f on
+the host sees): every step copies f host->device and back, pipelined per v2
+block against the plane-local x passes, with the D2H of step m and the H2D
+of step m+1 running concurrently (paper_1803_02143_b200/hoststep.py).
 
 ``roofline``: the dominant kernel (most device time per step) measured by
 CUDA events around its launches in the timed steps; algorithmic bytes = 16
 B per dof per sweep (one fp64 read + one write).
 
-``cpu_baseline`` / ``--impl reference``: the reference's own compiled line
-kernels (built into oracle/_ref from _kernels.pyx) driven like the
-reference's strang_step on every host thread, on a bounded scaled sample of
-the same configuration (oracle/refarm.py).
+``cpu_baseline`` / ``--impl reference``: the UNMODIFIED reference package
+(pip-installed into oracle/_ref/site by oracle/build.py) through its own
+public API: ``slvp.strang_step(consume=True)`` on every host thread, full
+steps of the same configuration under its bench_step protocol
+(oracle/refstep.py); cpu_baseline = one warm-up + one timed step, the
+reference arm = one warm-up + as many steps as fit in --ref-budget.  Only a
+configuration that does not fit host RAM falls back to the scaled slab
+sample (oracle/refarm.py), labelled EXTRAPOLATED.
 
 Multi-GPU (torchrun, N > 1): the dG field is sharded along x1 (x1 x x2 on
 8 GPUs when the merged pass's halo does not fit an x1 shard) with NCCL halo
@@ -107,6 +113,20 @@ def l2_note(copy_bytes: int) -> str:
         return f"inputs ({copy_bytes / 1e9:.3g} GB per copy of f) >> 126 MB L2; no flush"
     return (f"inputs ({copy_bytes / 1e6:.3g} MB per copy of f) fit in L2: warm-L2 timing of a "
             "launch-bound configuration, not a headline number")
+
+
+def group_times(ev: list, labels: list) -> dict:
+    """label -> [total ms, count] from consecutive CUDA events (a label runs
+    until the next event)."""
+    groups: dict = {}
+    for i in range(len(ev) - 1):
+        if labels[i] is None:
+            continue
+        dt = ev[i].elapsed_time(ev[i + 1])
+        g = groups.setdefault(labels[i], [0.0, 0])
+        g[0] += dt
+        g[1] += 1
+    return groups
 
 
 def load_traffic(cfg_name: str, label: str):
@@ -261,40 +281,75 @@ def allreduce_max(d, value: float) -> float:
 # ---------------------------------------------------------------------------
 # reference arm
 # ---------------------------------------------------------------------------
-def cpu_reference(cfg: dict) -> dict:
+def _host_ram_bytes() -> int:
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
+def cpu_reference(cfg: dict, *, warmup: int = 1, max_steps: int = 1,
+                  budget_s: float = 240.0, threads: int | None = None) -> dict:
+    """The unmodified reference ``slvp.strang_step`` (oracle/_ref/site) timed
+    on full steps of the configuration on this box's host cores
+    (oracle/refstep.py).  A configuration whose reference run does not fit
+    host RAM (the reference keeps ~3 copies of f) falls back to the scaled
+    slab sample of the reference's compiled kernels (oracle/refarm.py) and
+    says so in ``sample``."""
+    need = 3 * 8 * int(cfg["dofs"]) ** 4
+    avail = _host_ram_bytes()
+    from oracle import build
+
+    if build.load_ref_pkg() is not None and (avail == 0 or need < 0.8 * avail):
+        from oracle import refstep
+
+        return refstep.time_steps(cfg["problem"], cfg["method"], cfg["dofs"], cfg["order"],
+                                  cfg["tau"], threads=threads, warmup=warmup,
+                                  max_steps=max_steps, budget_s=budget_s)
     from oracle import refarm
 
-    return refarm.reference_step_rate(cfg["problem"], cfg["method"], cfg["dofs"], cfg["order"],
-                                      cfg["tau"])
+    r = refarm.reference_step_rate(cfg["problem"], cfg["method"], cfg["dofs"], cfg["order"],
+                                   cfg["tau"], threads=threads)
+    r["sample"] = ("EXTRAPOLATED (full-size reference run needs %.0f GB, host has %.0f GB "
+                   "available): " % (need / 1e9, avail / 1e9)) + r["sample"]
+    r["steps_timed"] = 0
+    return r
 
 
 def run_reference_arm(args, cfg_name: str, cfg: dict) -> None:
+    """``--impl reference``: the reference's own strang_step on every host
+    thread, full steps of the same configuration (bench_step protocol), as
+    many as fit in ``--ref-budget`` seconds (at most ``--steps``), after one
+    warm-up step.  Plus a 1-core figure (config 1, full steps)."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    from oracle import core
-
-    samples = []
-    for i in range(args.warmup + args.steps):
-        r = cpu_reference(cfg)
-        if i >= args.warmup:
-            samples.append(r)
-    vals = [s["dof_per_s"] for s in samples]
-    value = float(np.median(vals))
-    ms = float(np.median([s["step_s"] for s in samples])) * 1e3
-    last = samples[-1]
+    r = cpu_reference(cfg, warmup=1, max_steps=args.steps, budget_s=args.ref_budget)
+    one = cpu_reference(CONFIGS["cfg1"], warmup=1, max_steps=3, budget_s=30.0, threads=1)
+    value = r["dof_per_s"]
     line = {
         "impl": "reference",
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "steps": int(r.get("steps_timed", 0)), "warmup": int(r.get("warmup", 0)),
+        "requested": {"steps": args.steps, "warmup": args.warmup,
+                      "note": "full reference steps take tens of seconds: one warm-up step, "
+                              "then as many timed steps as fit in --ref-budget"},
+        "ms_per_step": r["step_s"] * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (BASELINE initial condition, no dataset)",
         "config": {"workload": cfg_name, "description": cfg["label"],
                    "dofs": int(cfg["dofs"]) ** 4, "parallelism": "cpu-threads"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": last["threads"],
-                         "kind": last["kind"], "sample": last["sample"]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": r["threads"],
+                         "kind": r["kind"], "sample": r["sample"]},
+        "samples_s": r.get("samples_s"),
+        "one_core": {"value": one["dof_per_s"], "unit": UNIT, "cores": 1,
+                     "config": "cfg1", "ms_per_step": one["step_s"] * 1e3,
+                     "sample": one["sample"]},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "host_threads": core.host_threads(),
+        "host_threads": r["threads"],
     }
     print(json.dumps(line), flush=True)
 
@@ -321,14 +376,14 @@ def run_sharded(args, cfg_name: str, cfg: dict, d, world: int, rank: int, local:
         solver = dist.ShardedSolver(grid, dist.Decomposition(grid, world, 1), dist.TorchComm(),
                                     [rank])
         p1, p2 = world, 1
-        if not (solver._stencil_ready() and solver._merged_halo_fits(tau)):
+        if not (solver._stencil_ready(tau) and solver._merged_halo_fits(tau)):
             p1, p2 = dist.process_grid(world)
             solver = dist.ShardedSolver(grid, dist.Decomposition(grid, p1, p2),
                                         dist.TorchComm(), [rank])
         local_f = lambda: solver.shards[rank].f  # noqa: E731
         layout = (f"x-shard {p1}x{p2} (NCCL halos + rho allgather"
                   + ("; merged x passes as halo-exchanged stencil passes)"
-                     if solver._stencil_ready() else ")"))
+                     if solver._stencil_ready(tau) else ")"))
     else:
         solver = dist.SplineShardedSolver(grid, dist.TorchComm(), [rank], world)
         local_f = lambda: solver.a[rank][0]  # noqa: E731
@@ -337,11 +392,20 @@ def run_sharded(args, cfg_name: str, cfg: dict, d, world: int, rank: int, local:
     stream = torch.cuda.current_stream()
     clocks = ClockSampler(local).start()
 
-    def steps(k: int) -> None:
+    labels: list = []
+    ev: list = []
+
+    def mark(label):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        ev.append(e)
+        labels.append(label)
+
+    def steps(k: int, timer=None) -> None:
         # dG: advance() merges the x half steps of consecutive steps into one
         # halo-exchanged stencil pass per step (x1-sharded layouts)
         if hasattr(solver, "advance"):
-            solver.advance(tau, k)
+            solver.advance(tau, k, timer=timer)
         else:
             for _ in range(k):
                 solver.step(tau)
@@ -352,20 +416,37 @@ def run_sharded(args, cfg_name: str, cfg: dict, d, world: int, rank: int, local:
     barrier(d, local)
     torch.cuda.synchronize()
     n_launch0 = _lib.load().vpb_launch_count()
+    solver._halo_bytes = 0
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
     clocks.begin()
     start.record(stream)
-    steps(args.steps)
+    steps(args.steps, timer=mark if hasattr(solver, "advance") else None)
     end.record(stream)
     torch.cuda.synchronize()
     clocks.end()
     clocks.stop()
     gpu_launches = _lib.load().vpb_launch_count() - n_launch0  # rank 0's kernels
+    halo_bytes = getattr(solver, "_halo_bytes", 0) / max(1, args.steps)
     barrier(d, local)
     total_ms = allreduce_max(d, start.elapsed_time(end))
     ms_per_step = total_ms / args.steps
     value = N * args.steps / (total_ms * 1e-3)
+    # per-group device time on this rank; the dominant sweep kernel on the
+    # same basis as the 1-GPU line: 16 B per LOCAL dof per launch
+    groups = group_times(ev, labels)
+    n_local = local_f().numel()
+    per_kernel = {k: {"avg_ms": v[0] / v[1], "launch_groups": v[1],
+                      "share_of_step": v[0] / total_ms} for k, v in sorted(groups.items())}
+    sweeps = {k: v for k, v in groups.items() if k.startswith("sweep_")}
+    peak, peak_kind = load_peaks()
+    dom = max(sweeps, key=lambda k: sweeps[k][0]) if sweeps else None
+    for k in sweeps:
+        t = per_kernel[k]["avg_ms"] * 1e-3
+        per_kernel[k]["achieved_gbs"] = BYTES_PER_DOF_SWEEP * n_local / t / 1e9
+        per_kernel[k]["frac"] = per_kernel[k]["achieved_gbs"] / peak
+        per_kernel[k]["sweeps_per_launch"] = sweeps_per_launch(k)
+    dom_frac = allreduce_max(d, per_kernel[dom]["frac"]) if dom else None
     # e2e: each rank's slab from pinned host memory, step, back to the host
     e2e = None
     if not args.no_e2e:
@@ -389,8 +470,7 @@ def run_sharded(args, cfg_name: str, cfg: dict, d, world: int, rank: int, local:
                "h2d_bytes_per_step": nbytes * world, "d2h_bytes_per_step": nbytes * world,
                "steps": k_e2e, "ms_per_step": e2e_ms / k_e2e,
                "path": "per-rank pinned host slab -> H2D -> sharded step -> D2H"}
-    peak, peak_kind = load_peaks()
-    step_gbs = 6 * BYTES_PER_DOF_SWEEP * N / (ms_per_step * 1e-3) / 1e9
+    step_gbs_local = 6 * BYTES_PER_DOF_SWEEP * n_local / (ms_per_step * 1e-3) / 1e9
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -400,9 +480,22 @@ def run_sharded(args, cfg_name: str, cfg: dict, d, world: int, rank: int, local:
             "config": {"workload": cfg_name, "description": cfg["label"], "dofs": N,
                        "parallelism": layout,
                        "l2": l2_note(8 * N // world)},
-            "roofline": {"bound": "hbm", "achieved": step_gbs / world, "peak": peak,
-                         "unit": "GB/s", "frac": step_gbs / world / peak, "traffic": None,
-                         "kernel": "whole step per GPU (96 B/dof)", "peak_source": peak_kind},
+            "roofline": {"bound": "hbm",
+                         "achieved": (per_kernel[dom]["achieved_gbs"] if dom else None),
+                         "peak": peak, "unit": "GB/s", "frac": per_kernel[dom]["frac"] if dom
+                         else None, "frac_max_over_ranks": dom_frac,
+                         "traffic": None, "kernel": dom,
+                         "algorithmic_bytes_per_launch": BYTES_PER_DOF_SWEEP * n_local,
+                         "basis": "rank 0's dominant sweep kernel, 16 B per local dof per "
+                                  "launch / average launch time (same basis as the 1-GPU line)",
+                         "step_frac": step_gbs_local / peak,
+                         "step_bytes": 6 * BYTES_PER_DOF_SWEEP * n_local,
+                         "peak_source": peak_kind},
+            "kernels": per_kernel,
+            "comm_bytes_per_step": {"halo_send": halo_bytes,
+                                    "rho_allgather": 8 * (grid.dims4[0] // max(1, cfg["order"]))
+                                    * (grid.dims4[1] // max(1, cfg["order"]))
+                                    if cfg["method"] == "dg" else None},
             "e2e": e2e, "cpu_baseline": None, "clocks": clocks.summary(),
             "gpu_launches": int(gpu_launches),
         }), flush=True)
@@ -522,14 +615,7 @@ def run_vpb(args, cfg_name: str, cfg: dict) -> None:
                     "value": world * N * args.steps / (pc_ms * 1e-3), "unit": UNIT}
 
     # per-group device time
-    groups: dict = {}
-    for i in range(len(ev) - 1):
-        if labels[i] is None:
-            continue
-        dt = ev[i].elapsed_time(ev[i + 1])
-        g = groups.setdefault(labels[i], [0.0, 0])
-        g[0] += dt
-        g[1] += 1
+    groups = group_times(ev, labels)
     sweeps = {k: v for k, v in groups.items() if k.startswith("sweep_")}
     dom = max(sweeps, key=lambda k: sweeps[k][0])
     dom_avg_ms = sweeps[dom][0] / sweeps[dom][1]
@@ -560,31 +646,38 @@ def run_vpb(args, cfg_name: str, cfg: dict) -> None:
     # --- e2e through the public API with host-resident f
     e2e = None
     if not args.no_e2e:
-        host = torch.empty(N, dtype=torch.float64, pin_memory=True)
-        host.copy_(field.data)
-        torch.cuda.synchronize()
+        from paper_1803_02143_b200 import hoststep
+
+        host = hoststep.HostField.from_field(field)
         k_e2e = max(1, min(args.steps, args.e2e_steps))
+        hoststep.host_steps(host, tau, 1, blocks=args.e2e_blocks)  # warm-up (buffers, tables)
         barrier(d, local)
         torch.cuda.synchronize()
         s0 = torch.cuda.Event(enable_timing=True)
         s1 = torch.cuda.Event(enable_timing=True)
         s0.record(stream)
-        for _ in range(k_e2e):
-            field.data.copy_(host, non_blocking=True)
-            vpb.strang_step(field, tau, consume=True)
-            host.copy_(field.data, non_blocking=True)
+        w0 = time.perf_counter()
+        # check_steps inside host_steps synchronises after the last D2H, so the
+        # end event is recorded on the compute stream after every copy completed
+        hoststep.host_steps(host, tau, k_e2e, blocks=args.e2e_blocks)
         s1.record(stream)
         torch.cuda.synchronize()
+        wall_ms = (time.perf_counter() - w0) * 1e3
         e2e_ms = allreduce_max(d, s0.elapsed_time(s1))
         e2e = {"value": world * N * k_e2e / (e2e_ms * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N, "steps": k_e2e,
-               "ms_per_step": e2e_ms / k_e2e,
-               "path": "pinned host f -> H2D -> strang_step -> D2H, every step"}
+               "ms_per_step": e2e_ms / k_e2e, "wall_ms_per_step": wall_ms / k_e2e,
+               "pcie_gbs_per_direction": 8 * N / (e2e_ms / k_e2e * 1e-3) / 1e9,
+               "blocks": args.e2e_blocks,
+               "path": "host_steps(HostField): f in pinned host memory between steps; per "
+                       "step every v2 block goes H2D -> opening x pass, whole-field density/"
+                       "field solve/v pass, closing x pass -> D2H; H2D of step m+1 overlaps "
+                       "D2H of step m block by block (hoststep.py)"}
         del host
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        r = cpu_reference(cfg)
+        r = cpu_reference(cfg, warmup=1, max_steps=1)
         cpu = {"value": r["dof_per_s"], "unit": UNIT, "cores": r["threads"], "kind": r["kind"],
                "sample": r["sample"]}
 
@@ -649,7 +742,8 @@ def main() -> None:
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="vpb", choices=["vpb", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=4)
+    ap.add_argument("--e2e-blocks", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--graph", action="store_true",
                     help="time per-step calls replayed from CUDA graphs (driver.StepGraph)")
@@ -657,6 +751,8 @@ def main() -> None:
                     help="time one strang_step call per step instead of advance()")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent replicas instead of the sharded field")
+    ap.add_argument("--ref-budget", type=float, default=240.0,
+                    help="--impl reference: seconds of timed full reference steps")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per launch of the dominant kernel (from profiles/)")
     args = ap.parse_args()

@@ -9,6 +9,17 @@
   ``_kernels_py``; the generated shim supplies the oracle's restatement of
   it (pinned bitwise against the reference's factors by the golden tests).
   Nothing from /root/reference is copied: only build outputs land in _ref/.
+* ``_ref/site/slvp``: the WHOLE reference package, installed with the
+  base contract's own command (``pip install --no-index --no-build-isolation
+  --no-deps --target``) from a scratch copy under /tmp (its build writes
+  into the source tree, /root/reference is read-only).  This is the
+  unmodified reference (``slvp.strang_step``, its compiled ``_kernels``);
+  the reference CPU arm of bench.py and the full-size GPU parity tests run
+  it on the GPU box's host cores.
+* ``_ref/reftests``: the reference's own test-suite, staged next to the
+  install so ``tests/test_gpu_reference_suite.py`` can run it with the CUDA
+  line kernels registered as the reference backend ``"cuda"``.
+  Both are git-ignored build outputs that travel to the GPU box.
 """
 
 from __future__ import annotations
@@ -65,9 +76,65 @@ def build_ref(force: bool = False) -> Path | None:
     return so
 
 
+REF_PKG = Path("/root/reference/pkg")
+
+
+def ref_site_dir() -> Path:
+    return HERE / "_ref" / "site"
+
+
+def ref_tests_dir() -> Path:
+    return HERE / "_ref" / "reftests"
+
+
+def build_ref_pkg(force: bool = False) -> Path | None:
+    """pip-install the reference package into _ref/site (needs /root/reference)."""
+    import shutil
+    import tempfile
+
+    site = ref_site_dir()
+    so = list((site / "slvp").glob("_kernels*.so")) if (site / "slvp").exists() else []
+    if not REF_PKG.exists():
+        return site if so else None
+    if so and not force:
+        return site
+    scratch = Path(tempfile.mkdtemp(prefix="slvp_pkg_"))
+    try:
+        for name in ("src", "setup.py", "pyproject.toml", "README.md"):
+            src = REF_PKG / name
+            (shutil.copytree if src.is_dir() else shutil.copy)(src, scratch / name)
+        if site.exists():
+            shutil.rmtree(site)
+        env = dict(__import__("os").environ, CC=GCC, LDSHARED=f"{GCC} -shared")
+        subprocess.run([sys.executable, "-m", "pip", "install", "--no-index",
+                        "--no-build-isolation", "--no-deps", "--find-links", "/opt/wheelhouse",
+                        "--target", str(site), str(scratch)], check=True, env=env,
+                       stdout=subprocess.DEVNULL)
+    finally:
+        shutil.rmtree(scratch, ignore_errors=True)
+    tests = ref_tests_dir()
+    if tests.exists():
+        shutil.rmtree(tests)
+    shutil.copytree(REF_PKG / "tests", tests)
+    return site
+
+
+def load_ref_pkg():
+    """Import the installed reference package ``slvp`` (None when not built)."""
+    site = ref_site_dir()
+    if not list((site / "slvp").glob("_kernels*.so")):
+        return None
+    if str(site) not in sys.path:
+        sys.path.insert(0, str(site))
+    import slvp  # type: ignore
+
+    return slvp
+
+
 def build(force: bool = False) -> None:
     build_oracle(force)
     build_ref(force)
+    build_ref_pkg(force)
 
 
 if __name__ == "__main__":

@@ -562,9 +562,30 @@ class ShardedSolver:
                 raise SubstepError(name, time_label)
 
     # -- K steps with merged x half steps on the x1-sharded field -------------
-    def _stencil_ready(self) -> bool:
-        return (self.dec.sharded(0) and not self.dec.sharded(1)
-                and hasattr(self.ops, "xstencil") and self.grid.ndim == 4)
+    def _stencil_ready(self, tau: float | None = None) -> bool:
+        """Whether advance() can run the three-cell stencil passes: an
+        x1-only decomposition of a 2x2v field, every shard meeting the
+        stencil kernel's preconditions (``xplane_args_ok`` in fused.cu: a
+        cell row of x1 dofs is a 16-byte multiple; ``plan_xcomp`` in
+        xcomp.cu: at most 128 local x1 cells), and -- given tau -- the
+        single half step's x1 halo fitting every shard.  Otherwise advance()
+        runs step() (the halo sweeps) in a loop."""
+        if not (self.dec.sharded(0) and not self.dec.sharded(1)
+                and hasattr(self.ops, "xstencil") and self.grid.ndim == 4):
+            return False
+        p = self.order
+        for r in range(self.dec.world):
+            c0, c1 = self.dec.cells(r, 0)
+            if ((c1 - c0) * p * p) % 2 or c1 - c0 > 128:
+                return False
+        if tau is not None:
+            _, _, tabs = self._stencil_setup(tau)
+            _, _, wl, wr = tabs[1]
+            cells_min = min(c1 - c0 for r in range(self.dec.world)
+                            for (c0, c1) in [self.dec.cells(r, 0)])
+            if max(wl, wr) > cells_min:
+                return False
+        return True
 
     def _stencil_setup(self, tau: float):
         """Tables of the three-cell x passes and their x1 halo widths."""
@@ -616,6 +637,8 @@ class ShardedSolver:
         t1, t2, tabs = self._stencil_setup(tau)
         k1, k2, wl, wr = tabs[qmul]
         p = self.order
+        mark = getattr(self, "_mark", None) or (lambda label: None)
+        mark("halo_x1")
         cells_min = min(c1 - c0 for sh in self.shards.values() for (c0, c1) in [sh.cells[0]])
         if max(wl, wr) > cells_min:
             raise NotImplementedError(
@@ -640,7 +663,10 @@ class ShardedSolver:
                        (KIND_R, left, send_r, right, recv_r)]
             bufs[r] = (recv_l, recv_r)
         self.comm.exchange(msgs)
+        self._halo_bytes = getattr(self, "_halo_bytes", 0) + sum(
+            8 * (m[0][2].numel() * (wl > 0) + m[1][2].numel() * (wr > 0)) for m in msgs.values())
         mid, wc1, wc2, volume = self._density_consts()
+        mark(("sweep_x12x12" if qmul == 2 else "sweep_x12") + ("_rho" if with_density else ""))
         for r, sh in self.shards.items():
             recv_l, recv_r = bufs[r]
             fl = flags_row[r][flag_slot:flag_slot + 1]
@@ -675,7 +701,8 @@ class ShardedSolver:
             full[:, a0:b0] = part[: (b0 - a0) * C2].view(C2, b0 - a0)
         return full.view(-1)
 
-    def advance(self, tau: float, nsteps: int, first_step: int | None = None) -> None:
+    def advance(self, tau: float, nsteps: int, first_step: int | None = None,
+                timer=None) -> None:
         """``nsteps`` Strang steps (driver.advance on the sharded field).
 
         x1-sharded fields run the single-GPU pass structure: one x pass per
@@ -688,7 +715,17 @@ class ShardedSolver:
 
         if nsteps <= 0:
             return
-        if not self._stencil_ready() or ARITH != "fast":
+        self._mark = timer
+        try:
+            self._advance(tau, nsteps, first_step, ARITH, SubstepError, _warn_if_not_neutral)
+        finally:
+            self._mark = None
+            if timer is not None:
+                timer(None)
+
+    def _advance(self, tau, nsteps, first_step, ARITH, SubstepError, _warn_if_not_neutral):
+        mark = self._mark or (lambda label: None)
+        if ARITH != "fast" or not self._stencil_ready(tau):
             for m in range(nsteps):
                 self.step(tau, None if first_step is None else (first_step + m) * tau)
             return
@@ -701,11 +738,15 @@ class ShardedSolver:
         self._x_stencil_pass(tau, 1, 0, True, {r: flags[r][0] for r in self.shards},
                              {r: stats[r][0] for r in self.shards}, rc_parts)
         for m in range(nsteps):
+            mark("rho_allgather")
             rc = self._gather_rc(rc_parts)
+            mark("field_solve")
             self.ops.field_solve_centred(self.grid, rc, self.e, solve_flags[m])
             for r, sh in self.shards.items():
+                mark("tables_v12")
                 tabs = [self.ops.tables(self._local_e(sh, d), tau, self.grid.axes[2 + d].h,
                                         self.grid.dg_degree) for d in range(2)]
+                mark("sweep_v12")
                 self.ops.vplane(sh.f, sh.buf, sh.dims, self.order, tabs[0], tabs[1],
                                 flags[r][m][3:4], flags[r][m][4:5])
                 sh.swap()
@@ -723,6 +764,7 @@ class ShardedSolver:
             else:
                 self._x_stencil_pass(tau, 1, 5, False, {r: flags[r][m] for r in self.shards},
                                      {}, {})
+        mark("flags")
         for r in self.shards:
             flags[r][:, 2:3] = torch.maximum(flags[r][:, 2:3], solve_flags)
         fl = self.comm.allreduce(flags, "max").cpu().numpy()

@@ -393,9 +393,11 @@ def enqueue_steps(field: DistributionField, tau: float, nsteps: int, st: StepSta
     ``flags[m]`` / ``stats[m]`` receive step m's flag words (slots as
     ``st.names``) and density mean.  With ``merge`` (and the fused x pass),
     the closing x half step of step m and the opening one of step m+1 run as
-    one HBM pass (``vpb_dg_sweep_xplane2``: four sweeps chained in registers
-    and shared memory, bitwise equal to running them separately); the state
-    between the two steps is then never written to HBM.
+    one HBM pass; the state between the two steps is then never written to
+    HBM.  "exact" arithmetic: ``vpb_dg_sweep_xplane2``, four sweeps chained
+    in registers and shared memory, bitwise equal to running them
+    separately; "fast" (default): ``vpb_dg_sweep_xcomp``, composed
+    three-cell stencils, equal up to round-off.
 
     ``moments`` (8 doubles, needs ``st.fused_rho``): the closing pass of the
     last step also produces the diagnostics of the final state
@@ -691,15 +693,31 @@ def strang_step(field: DistributionField, tau: float, workers: int = 1, consume:
 
 def advance(field: DistributionField, tau: float, nsteps: int, consume: bool = False,
             first_step: int | None = None, record_time: float | None = None):
-    """``nsteps`` Strang steps; the result is bitwise that of ``nsteps``
-    :func:`strang_step` calls, with the same errors and warnings.
+    """``nsteps`` Strang steps (driver.py:245-265 each, the reference's
+    ``run`` loop between records, driver.py:371-377).
 
     Adjacent x half steps of consecutive steps share one HBM pass
     (:func:`enqueue_steps`), so the states between the steps are never
     written out; use :func:`strang_step` when every intermediate state is
-    needed.  Non-finite checks and neutrality warnings are evaluated after
-    the last step, in step order; with ``first_step`` the errors carry the
-    time label ``(first_step + m) * tau`` of step m (as run() labels them).
+    needed.  What the result equals depends on the arithmetic mode
+    (:func:`set_arithmetic`):
+
+    * ``"exact"``: bitwise ``nsteps`` :func:`strang_step` calls, with the
+      same errors and warnings;
+    * ``"fast"`` (default): the closing x half step of step m and the
+      opening one of step m+1 are applied as composed three-cell stencils
+      per x axis, so the result equals the strang_step chain up to
+      round-off (tests: <= 1e-13 of max|f| against the chain, <= 1e-12 per
+      step against the reference).  The intermediate states are never
+      formed, so a non-finite value CREATED inside a merged pass (an
+      overflow of finite inputs) is reported as the closing ``x1 half
+      (close)`` of step m, where the reference might name step m+1's
+      ``x1 half (open)``; non-finite inputs are caught by the pass that
+      produced them, as in the reference.
+
+    Non-finite checks and neutrality warnings are evaluated after the last
+    step, in step order; with ``first_step`` the errors carry the time label
+    ``(first_step + m) * tau`` of step m (as run() labels them).
 
     With ``record_time`` the result is ``(field, DiagnosticsRecord)``: the
     diagnostics of the final state (== ``diagnostics(field, record_time)``

@@ -20,6 +20,7 @@ def main() -> None:
     ap.add_argument("--dofs", type=int, nargs=4, default=[192, 192, 48, 48])
     ap.add_argument("--tau", type=float, default=0.05)
     ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--advance", action="store_true", help="advance() (merged x passes)")
     args = ap.parse_args()
     import torch
 
@@ -28,8 +29,11 @@ def main() -> None:
     prob = vpb.problem_spec(args.problem)
     grid = vpb.make_grid(prob, args.method, tuple(args.dofs), dg_order=args.order)
     f = vpb.initialize(prob, grid)
-    for _ in range(args.steps):
-        f = vpb.strang_step(f, args.tau, consume=True)
+    if args.advance:
+        f = vpb.advance(f, args.tau, args.steps, consume=True)
+    else:
+        for _ in range(args.steps):
+            f = vpb.strang_step(f, args.tau, consume=True)
     torch.cuda.synchronize()
     print("ok", grid.dofs)
 

@@ -39,10 +39,5 @@ def _build_oracle():
 
     build.build_oracle()
     build.build_ref()
+    build.build_ref_pkg()
 
-
-def max_rel(a, b) -> float:
-    a = np.asarray(a)
-    b = np.asarray(b)
-    scale = float(np.max(np.abs(b)))
-    return float(np.max(np.abs(a - b))) / (scale if scale > 0 else 1.0)

@@ -13,7 +13,10 @@ driven through its public API.  Outputs:
   steps.npz    short trajectories (f after each step + diagnostics) on small
                2x2v / 1x1v grids for every method/order the tests cover
   series.npz   diagnostics time series at BASELINE config 1 (48^4, 20 steps)
-               and reduced-size configs 3 and 4, plus per-step f checksums
+               and reduced-size configs 3 (200 steps) and 4 (50 steps), plus
+               per-step f checksums
+  snapshots.npz  VLF1 files written by the reference's write_snapshot (raw
+               bytes) and the arrays they hold
 
 Nothing here is used at run time on the GPU box; the .npz files are.
 """
@@ -147,8 +150,8 @@ def series_fixture(slvp) -> dict:
     cases = [
         # tag, problem, method, dofs, order, tau, nsteps, ic
         ("cfg1", "landau4d", "dg", 48, 3, 0.1, 20, None),
-        ("cfg3_small", "twostream4d", "dg", 32, 2, 0.1, 20, "baseline"),
-        ("cfg4_small", "landau4d", "spline", 32, 0, 0.1, 10, None),
+        ("cfg3_small", "twostream4d", "dg", 32, 2, 0.1, 200, "baseline"),
+        ("cfg4_small", "landau4d", "spline", 32, 0, 0.1, 50, None),
     ]
     workers = len(os.sched_getaffinity(0))
     for tag, prob, method, dofs, order, tau, nsteps, ic in cases:
@@ -170,12 +173,50 @@ def series_fixture(slvp) -> dict:
     return out
 
 
+def snapshot_fixture(slvp) -> dict:
+    """VLF1 files written by the reference's write_snapshot (field.py:260-271),
+    raw bytes, plus the logical array each one holds."""
+    from slvp.grid import SPACE, VELOCITY, Axis, GridSpec
+
+    out = {}
+    tmp = Path(tempfile.mkdtemp(prefix="vlf_"))
+    cases = [
+        # tag, problem, method, dofs, order, steps
+        ("landau4d_dg3", "landau4d", "dg", 12, 3, 1),
+        ("landau4d_spline", "landau4d", "spline", 8, 0, 1),
+        ("landau2d_dg2", "landau2d", "dg", 16, 2, 2),
+    ]
+    for tag, prob, method, dofs, order, nsteps in cases:
+        problem = slvp.problem_spec(prob)
+        grid = slvp.make_grid(problem, method, dofs, dg_order=order)
+        field = slvp.initialize(problem, grid)
+        for _ in range(nsteps):
+            field = slvp.strang_step(field, 0.1, workers=2, consume=True)
+        path = tmp / f"{tag}.vlf"
+        slvp.write_snapshot(field, path)
+        out[tag + "_bytes"] = np.frombuffer(path.read_bytes(), dtype=np.uint8)
+        out[tag + "_array"] = np.ascontiguousarray(field.array)
+        out[tag + "_steps"] = np.array(nsteps)
+    # the frozen 4x4 spline header case of tests/test_grid.py:309-320
+    grid = GridSpec((Axis(0.0, 2.0, 4, SPACE), Axis(-1.0, 1.0, 4, VELOCITY)), "spline")
+    field = slvp.DistributionField.from_values(grid, np.arange(16.0).reshape(4, 4))
+    path = tmp / "h4x4.vlf"
+    slvp.write_snapshot(field, path)
+    out["h4x4_bytes"] = np.frombuffer(path.read_bytes(), dtype=np.uint8)
+    shutil.rmtree(tmp, ignore_errors=True)
+    return out
+
+
 def main() -> None:
     slvp = load_reference()
+    if "--snapshots-only" in sys.argv:
+        np.savez_compressed(HERE / "snapshots.npz", **snapshot_fixture(slvp))
+        return
+    np.savez_compressed(HERE / "snapshots.npz", **snapshot_fixture(slvp))
     np.savez_compressed(HERE / "kernels.npz", **kernels_fixture(slvp))
     np.savez_compressed(HERE / "steps.npz", **steps_fixture(slvp))
     np.savez_compressed(HERE / "series.npz", **series_fixture(slvp))
-    for f in ("kernels.npz", "steps.npz", "series.npz"):
+    for f in ("kernels.npz", "steps.npz", "series.npz", "snapshots.npz"):
         print(f, (HERE / f).stat().st_size)
 
 

@@ -121,6 +121,36 @@ def test_virtual_sharded_advance_matches_oracle_steps(p1, tau):
     assert max_rel(solver.gather(), f) <= 1e-13
 
 
+@pytest.mark.parametrize("p1", [3, 5])
+def test_virtual_sharded_advance_uneven_split_falls_back_to_step(p1):
+    """8 x1 cells over 3 / 5 ranks: shards of 2-3 / 1-2 cells.  Odd local dof
+    rows (3 cells * 3 * 3) miss the stencil kernel's 16-byte precondition and
+    the single half step's halo may exceed a 1-cell shard: advance() must
+    run the per-sweep halo path, not raise."""
+    grid, og = grids()
+    dec = dist.Decomposition(grid, p1, 1)
+    solver = dist.ShardedSolver(grid, dec, dist.VirtualComm(dec.world), range(dec.world),
+                                ops=NumpyOps(), device=torch.device("cpu"))
+    assert not solver._stencil_ready(TAU)
+    solver.scatter(core.initialize(PROB, og))
+    solver.advance(TAU, 2)
+    f = core.initialize(PROB, og)
+    for _ in range(2):
+        f = core.strang_step(f, og, TAU)
+    assert max_rel(solver.gather(), f) <= 1e-13
+
+
+def test_stencil_ready_checks_halo_fit():
+    """Even 2-cell shards (4 ranks x 2 cells) meet the row precondition, but
+    a shift of several cells needs a wider halo than a shard: not ready."""
+    grid, og = grids()
+    dec = dist.Decomposition(grid, 4, 1)
+    solver = dist.ShardedSolver(grid, dec, dist.VirtualComm(dec.world), range(dec.world),
+                                ops=NumpyOps(), device=torch.device("cpu"))
+    assert solver._stencil_ready(TAU)
+    assert not solver._stencil_ready(12.0)
+
+
 def _advance_worker(rank, world, port, outdir):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)

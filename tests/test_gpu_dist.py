@@ -73,6 +73,19 @@ def test_sharded_advance_with_merged_stencil_passes_matches_single_gpu(p1, tau):
         assert got[k] == pytest.approx(getattr(rec, k), rel=1e-12), k
 
 
+@pytest.mark.parametrize("p1", [3, 5])
+def test_sharded_advance_uneven_split_falls_back_to_halo_sweeps(p1):
+    """Uneven x1 splits (16 cells over 3 or 5 ranks: shards of 5-6 / 3-4
+    cells, some with an odd dof row of 5*3*3 values) miss the stencil
+    kernel's 16-byte row precondition: advance() must take the per-sweep
+    halo path instead of raising (the reference has no such restriction)."""
+    prob, grid, solver, f0 = setup(p1, 1)
+    assert not solver._stencil_ready(TAU)
+    solver.advance(TAU, 3)
+    f = vpb.advance(f0, TAU, 3)
+    assert max_rel(solver.gather(), f.numpy()) <= 1e-13
+
+
 def test_sharded_advance_reports_nonfinite_substep():
     prob, grid, solver, f0 = setup(2, 1)
     sh = solver.shards[1]

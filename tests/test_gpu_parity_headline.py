@@ -1,0 +1,218 @@
+"""Parity of the HEADLINE path -- ``advance()`` / ``run()`` in the default
+"fast" arithmetic (merged x half steps as composed three-cell stencils, the
+density epilogue, the fused diagnostics record) -- against the UNMODIFIED
+reference ``slvp`` run on this box's host cores (oracle/_ref/site, built by
+oracle/build.py from /root/reference/pkg) and against the reference-written
+series in tests/golden/series.npz.
+
+North-star bars (BASELINE.json), written here:
+  * f: per-step max relative error ||f - f_ref||_inf / ||f_ref||_inf <= 1e-12;
+    also the floored pointwise error |f - f_ref| / max(|f_ref|, 1e-4 ||f_ref||_inf)
+    <= 1e-10 (velocity tails down to 1e-4 of the peak: there the absolute error
+    must stay below 1e-14 of the peak, 100x tighter than the max-norm bar; the
+    dG errors are at the
+    ulp-of-the-peak level everywhere, the spline ones a few ulps);
+  * electric energy: |EE - EE_ref| / |EE_ref| <= 1e-10 per record;
+  * mass: |m_t - m_0| / m_0 <= 1e-13.
+
+``advance(f0, tau, m)`` is recomputed from the initial state for every m so
+that the state after EVERY step of the merged-pass path is compared (the
+merged path never writes the states between its steps).
+
+Full-size cases (BASELINE configs 2, 3, 4 at their real grids) compare on the
+device against reference trajectories computed here on the host.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1803_02143_b200 as vpb
+from oracle import refstep
+from vpb_testutil import floored_rel, max_rel, torch_max_rel
+
+pytestmark = pytest.mark.gpu
+
+F_TOL = 1e-12
+EE_TOL = 1e-10
+MASS_TOL = 1e-13
+FLOOR = 1e-4
+FLOOR_TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def slvp():
+    mod = refstep.load()  # raises when the reference was not built
+    return mod
+
+
+@pytest.fixture(autouse=True)
+def _fast_mode():
+    old = vpb.arithmetic()
+    vpb.set_arithmetic("fast")
+    yield
+    vpb.set_arithmetic(old)
+
+
+def _reference_states(slvp, prob, method, dofs, order, tau, nsteps, keep=None):
+    """[(m, logical f_m as a numpy array, reference record)] for the kept steps."""
+    grid, field = refstep.make_field(slvp, prob, method, dofs, order)
+    threads = refstep.host_threads()
+    out = []
+    for m in range(1, nsteps + 1):
+        field = slvp.strang_step(field, tau, workers=threads, consume=True)
+        if keep is None or m in keep:
+            out.append((m, np.array(field.array), slvp.diagnostics(field, m * tau)))
+    return out
+
+
+def _vpb_initial(prob, method, dofs, order):
+    problem = vpb.problem_spec(prob)
+    grid = vpb.make_grid(problem, method, dofs, dg_order=order)
+    return vpb.initialize(problem, grid)
+
+
+def test_advance_fast_config1_every_step_vs_reference(slvp, golden):
+    """BASELINE config 1 (48^4, degree 2, dt=0.1, 20 steps) through the
+    headline advance() with the fused diagnostics record, every step."""
+    recs = golden("series")["cfg1_rec"]
+    ref = _reference_states(slvp, "landau4d", "dg", 48, 3, 0.1, 20)
+    f0 = _vpb_initial("landau4d", "dg", 48, 3)
+    m0 = vpb.diagnostics(f0, 0.0).mass
+    worst = worst_fl = 0.0
+    for m, fr, rr in ref:
+        g, rec = vpb.advance(f0, 0.1, m, record_time=m * 0.1)
+        got = g.numpy()
+        err = max_rel(got, fr)
+        fl = floored_rel(got, fr, FLOOR)
+        worst, worst_fl = max(worst, err), max(worst_fl, fl)
+        assert err <= F_TOL, (m, err)
+        assert fl <= FLOOR_TOL, (m, fl)
+        assert abs(rec.electric_energy - recs[m][1]) <= EE_TOL * abs(recs[m][1]), m
+        assert abs(rec.electric_energy - rr.electric_energy) <= EE_TOL * rr.electric_energy, m
+        assert abs(rec.mass - m0) <= MASS_TOL * m0, (m, rec.mass - m0)
+    print(f"config1 advance(fast): worst max-rel {worst:.2e}, floored {worst_fl:.2e}")
+
+
+def test_run_loop_config1_matches_reference_series(golden):
+    """run(diag_every=1) and run(diag_every=5): the reference's run loop
+    (driver.py:341-378) -> EE / mass series of the reference."""
+    recs = golden("series")["cfg1_rec"]
+    problem = vpb.problem_spec("landau4d")
+    grid = vpb.make_grid(problem, "dg", 48, dg_order=3)
+    for every in (1, 5):
+        cfg = vpb.RunConfig(problem=problem, grid=grid, tau=0.1, t_end=2.0, diag_every=every)
+        got, _ = vpb.run(cfg)
+        assert len(got) == 1 + 20 // every
+        m0 = got[0].mass
+        for i, rec in enumerate(got):
+            m = i * every
+            assert abs(rec.time - recs[m][0]) <= 1e-12
+            assert abs(rec.electric_energy - recs[m][1]) <= EE_TOL * abs(recs[m][1]), (every, m)
+            assert abs(rec.mass - m0) <= MASS_TOL * m0, (every, m)
+
+
+@pytest.mark.parametrize("tag,prob,method,dofs,order,nsteps,every", [
+    ("cfg3_small", "twostream4d_baseline", "dg", 32, 2, 200, 10),
+    ("cfg4_small", "landau4d", "spline", 32, 0, 50, 5),
+])
+def test_reduced_configs_full_length_through_run(slvp, golden, tag, prob, method, dofs, order,
+                                                 nsteps, every):
+    """Config 3 (two-stream, through the growth phase: 200 steps) and config
+    4 (spline, 50 steps) at reduced size, full length, through run() ->
+    advance() between records: EE per record and f checksums against the
+    reference series, f against the live reference at every record."""
+    z = golden("series")
+    recs, sums = z[tag + "_rec"], z[tag + "_sums"]
+    assert recs.shape[0] == nsteps + 1, "series.npz predates the full-length fixtures"
+    problem = vpb.problem_spec(prob)
+    grid = vpb.make_grid(problem, method, dofs, dg_order=order)
+    tau = 0.1
+    times = tuple(m * tau for m in range(every, nsteps + 1, every))
+    cfg = vpb.RunConfig(problem=problem, grid=grid, tau=tau, t_end=nsteps * tau,
+                        diag_every=every, snapshot_times=times)
+    got, snaps = vpb.run(cfg)
+    ref = dict((m, (f, r)) for m, f, r in _reference_states(
+        slvp, prob, method, dofs, order, tau, nsteps, keep=set(range(every, nsteps + 1, every))))
+    m0 = got[0].mass
+    for i, rec in enumerate(got[1:], start=1):
+        m = i * every
+        assert abs(rec.electric_energy - recs[m][1]) <= EE_TOL * abs(recs[m][1]), (tag, m)
+        assert abs(rec.mass - m0) <= MASS_TOL * abs(m0), (tag, m, rec.mass - m0)
+        f = snaps[i - 1][1].numpy()
+        np.testing.assert_allclose([f.sum(), (f * f).sum(), np.abs(f).max()], sums[m - 1],
+                                   rtol=1e-12)
+        assert max_rel(f, ref[m][0]) <= F_TOL, (tag, m)
+        assert floored_rel(f, ref[m][0], FLOOR) <= FLOOR_TOL, (tag, m)
+
+
+def test_config3_small_advance_full_length(slvp, golden):
+    """BASELINE config 3's two-stream IC (32^4 dofs, degree 1, dt=0.1), all
+    200 steps through advance() in blocks of 10 (merged passes inside each
+    block, fused diagnostics record at its end): EE per record vs the
+    reference series (the instability grows EE by 200x over the run), f vs
+    the live reference every 10 steps."""
+    z = golden("series")
+    recs, sums = z["cfg3_small_rec"], z["cfg3_small_sums"]
+    assert recs.shape[0] == 201, "series.npz predates the full-length fixtures"
+    every, nsteps, tau = 10, 200, 0.1
+    ref = dict((m, (f, r)) for m, f, r in _reference_states(
+        slvp, "twostream4d_baseline", "dg", 32, 2, tau, nsteps,
+        keep=set(range(every, nsteps + 1, every))))
+    f = _vpb_initial("twostream4d_baseline", "dg", 32, 2)
+    m0 = vpb.diagnostics(f, 0.0).mass
+    worst = 0.0
+    for m in range(every, nsteps + 1, every):
+        f, rec = vpb.advance(f, tau, every, consume=True, first_step=m - every + 1,
+                             record_time=m * tau)
+        assert abs(rec.electric_energy - recs[m][1]) <= EE_TOL * abs(recs[m][1]), m
+        assert abs(rec.mass - m0) <= MASS_TOL * abs(m0), (m, rec.mass - m0)
+        got = f.numpy()
+        np.testing.assert_allclose([got.sum(), (got * got).sum(), np.abs(got).max()],
+                                   sums[m - 1], rtol=1e-12)
+        err = max_rel(got, ref[m][0])
+        worst = max(worst, err)
+        assert err <= F_TOL, (m, err)
+        assert floored_rel(got, ref[m][0], FLOOR) <= FLOOR_TOL, m
+    print(f"config3-small 200 steps advance(fast): worst max-rel {worst:.2e}")
+
+
+# ---- BASELINE sizes: reference trajectories on the host, compared on device --
+FULL = [
+    ("cfg3", "twostream4d_baseline", "dg", 128, 2, 0.1, 3),
+    ("cfg2", "landau4d", "dg", 192, 3, 0.05, 2),
+    ("cfg4", "landau4d", "spline", 128, 0, 0.1, 2),
+]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("tag,prob,method,dofs,order,tau,nsteps", FULL)
+def test_fullsize_advance_vs_reference(slvp, tag, prob, method, dofs, order, tau, nsteps):
+    """The headline advance() at the full BASELINE grid against the
+    reference's strang_step run on the host: f after every step (max-rel and
+    floored pointwise, on the device), EE and mass of every step."""
+    grid_r, fr = refstep.make_field(slvp, prob, method, dofs, order)
+    threads = refstep.host_threads()
+    f0 = _vpb_initial(prob, method, dofs, order)
+    rec0 = vpb.diagnostics(f0, 0.0)
+    dev = f0.data.device
+    for m in range(1, nsteps + 1):
+        fr = slvp.strang_step(fr, tau, workers=threads, consume=True)
+        rr = slvp.diagnostics(fr, m * tau)
+        g, rec = vpb.advance(f0, tau, m, record_time=m * tau)
+        ref = torch.from_numpy(fr.array).to(dev)  # logical view, strides kept
+        got = g.array
+        err = torch_max_rel(got, ref)
+        fl = floored_rel(got, ref, FLOOR)
+        del ref, got
+        print(f"{tag} step {m}: max-rel {err:.2e} floored {fl:.2e} "
+              f"EE {rec.electric_energy:.15g} ref {rr.electric_energy:.15g}")
+        assert err <= F_TOL, (tag, m, err)
+        assert fl <= FLOOR_TOL, (tag, m, fl)
+        assert abs(rec.electric_energy - rr.electric_energy) <= EE_TOL * rr.electric_energy
+        assert abs(rec.mass - rec0.mass) <= MASS_TOL * rec0.mass, (tag, m)
+        assert abs(rr.mass - rec0.mass) <= MASS_TOL * rec0.mass, (tag, m)
+        del g
+        torch.cuda.empty_cache()
