@@ -246,6 +246,20 @@ int vpb_dg_sweep_xstencil_density(const double* src, double* dst, const int64_t 
                                   const double* wcell1_host, const double* wcell2_host,
                                   double volume, double* work, double* rc_out, double* stats,
                                   void* stream);
+/* The halo stencil pass (with or without the density epilogue: wv1 may be
+ * NULL) on v2 rows [v2_0, v2_0 + v2_rows) of the shard, so the sharded step
+ * can overlap the x1 halo exchange of the next block of rows with this
+ * block (dist.ShardedSolver.advance).  phase bit 1: first
+ * block of the pass (zero `work`), bit 2: last (reduce to rc_out / stats). */
+int vpb_dg_sweep_xstencil_rows(const double* src, double* dst, const int64_t dims[4],
+                               int32_t order, int64_t v2_0, int64_t v2_rows, const double* k1,
+                               const int64_t* q1, const double* alpha1, const double* k2,
+                               const int64_t* q2, const double* alpha2, int32_t qmul,
+                               const double* hl, int32_t wl, const double* hr, int32_t wr,
+                               int32_t* flag, const double* wv1, const double* wv2,
+                               const double* mid_host, const double* wcell1_host,
+                               const double* wcell2_host, double volume, double* work,
+                               double* rc_out, double* stats, int32_t phase, void* stream);
 
 /* One spline sweep along `axis`; shift of line = values[table row]*scale. */
 int vpb_spline_sweep_axis(int32_t axis, const double* src, double* dst, const int64_t dims[4],

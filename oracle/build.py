@@ -116,6 +116,9 @@ def build_ref_pkg(force: bool = False) -> Path | None:
     if tests.exists():
         shutil.rmtree(tests)
     shutil.copytree(REF_PKG / "tests", tests)
+    # the reference's pytest settings (pkg/pyproject.toml [tool.pytest.ini_options])
+    (tests / "pytest.ini").write_text(
+        "[pytest]\nmarkers =\n    slow: long-running end-to-end runs\n")
     return site
 
 

@@ -341,6 +341,157 @@ __device__ __forceinline__ void iir_solve2(double* y, const int YS, const int n,
   }
 }
 
+// Evaluation weights of one line (_kernels.pyx:62-87), the gain g folded in.
+__device__ __forceinline__ void spline_eval_weights(const SplineTileArgs& a, int64_t L, int n,
+                                                    double g, double (&w)[4], int& j0) {
+  const int64_t trow = a.idx ? a.idx[L] : (L / a.tdiv) % a.tmod;
+  const double shift = __dmul_rn(a.values[trow], a.scale);
+  const double sh = __ddiv_rn(shift, a.h);
+  double off = floor(-sh);
+  double th = __dsub_rn(-sh, off);
+  if (th >= 1.0) {
+    off = __dadd_rn(off, 1.0);
+    th = 0.0;
+  }
+  const double omt = __dsub_rn(1.0, th);
+  w[0] = g * __ddiv_rn(__dmul_rn(__dmul_rn(omt, omt), omt), 6.0);
+  w[1] = g * __ddiv_rn(__dadd_rn(__dsub_rn(4.0, __dmul_rn(__dmul_rn(6.0, th), th)),
+                                 __dmul_rn(__dmul_rn(__dmul_rn(3.0, th), th), th)),
+                       6.0);
+  w[2] = g * __ddiv_rn(__dadd_rn(__dsub_rn(4.0, __dmul_rn(__dmul_rn(6.0, omt), omt)),
+                                 __dmul_rn(__dmul_rn(__dmul_rn(3.0, omt), omt), omt)),
+                       6.0);
+  w[3] = g * __ddiv_rn(__dmul_rn(__dmul_rn(th, th), th), 6.0);
+  j0 = (int)wrap_mod((int64_t)off - 1, n);
+}
+
+// Contiguous-axis double sweep, one line per lane in a [line][RS] tile:
+// the two recursive-filter solves (iir_solve2) with the 7-tap evaluation of
+// the double sweep fused into the anticausal pass, so the solved values are
+// never re-read from shared memory: walking backwards, w_j is ready when
+// w_{j+1..j+6} are still in registers, and out at in-place position j
+// (= sum_m c_m w_{j+m}, the rotated layout of the unfused path) replaces
+// the causal value just consumed at j.  The six positions whose window
+// wraps past the end (j >= n-6) are emitted last, from saved values.
+//
+// Bank conflicts: with the row stride RS = n + 2 (even, for 16-byte bulk
+// copy destinations) lanes t and t + 8 of a half-warp hit the same bank
+// pair at equal point index.  Lanes with bit 3 set therefore walk their line
+// starting at point 1 (logical index j lives at physical (j + s) mod n,
+// s = (lane >> 3) & 1): the periodic filters may start anywhere (their
+// periodic start values are sums over the 64 preceding points), so only the
+// rounding of the two half-warps' lines differs.  Requires n >= 64, n % 8 == 0.
+// Returns true when an output is not finite.
+__device__ __forceinline__ bool iir2_eval_fused(double* y, const int n, const double z1,
+                                                const double (&c)[7], const int s) {
+  constexpr int U = 8;
+  auto at = [&](int j) -> double& {  // logical j in [0, n + 8) -> physical slot
+    int q = j + s;
+    if (q >= n) q -= n;
+    return y[q];
+  };
+  // ---- causal pass (both chains), periodic start from the 64 points before 0
+  double p1 = 0.0, p2 = 0.0;
+  for (int k = n - 64; k < n; k += U) {
+    double u[U];
+#pragma unroll
+    for (int r = 0; r < U; ++r) u[r] = at(k + r);
+#pragma unroll
+    for (int r = 0; r < U; ++r) {
+      p1 = fma(z1, p1, u[r]);
+      p2 = fma(z1, p2, p1);
+    }
+  }
+  for (int k = 0; k < n; k += U) {
+    double u[U];
+#pragma unroll
+    for (int r = 0; r < U; ++r) u[r] = at(k + r);
+#pragma unroll
+    for (int r = 0; r < U; ++r) {
+      p1 = fma(z1, p1, u[r]);
+      p2 = fma(z1, p2, p1);
+      u[r] = p2;
+    }
+#pragma unroll
+    for (int r = 0; r < U; ++r) at(k + r) = u[r];
+  }
+  // ---- anticausal pass, periodic start from the 64 points after n - 1
+  double q1 = 0.0, q2 = 0.0;
+  for (int k = 64 - U; k >= 0; k -= U) {
+    double u[U];
+#pragma unroll
+    for (int r = 0; r < U; ++r) u[r] = at(k + r);
+#pragma unroll
+    for (int r = U - 1; r >= 0; --r) {
+      q1 = fma(z1, q1, u[r]);
+      q2 = fma(z1, q2, q1);
+    }
+  }
+  ExpMax em;
+  double win[6];  // w_{j+1} .. w_{j+6}
+  double tail[6]; // w_{n-6} .. w_{n-1} (the wrapped windows' second halves)
+  // first block: j = n-1 .. n-8; outputs only for j <= n-7
+  {
+    const int k = n - U;
+    double u[U];
+#pragma unroll
+    for (int r = 0; r < U; ++r) u[r] = at(k + r);
+#pragma unroll
+    for (int r = U - 1; r >= 0; --r) {
+      q1 = fma(z1, q1, u[r]);
+      q2 = fma(z1, q2, q1);
+      u[r] = q2;  // w_{k+r}
+    }
+#pragma unroll
+    for (int r = 0; r < 6; ++r) tail[r] = u[r + 2];  // w_{n-6..n-1}
+    // outputs j = n-7, n-8 (windows w_{j..j+6} inside this block)
+#pragma unroll
+    for (int r = 1; r >= 0; --r) {
+      double o = c[0] * u[r];
+#pragma unroll
+      for (int m = 1; m < 7; ++m) o = fma(c[m], u[r + m], o);
+      em.add(o);
+      at(k + r) = o;
+    }
+#pragma unroll
+    for (int m = 0; m < 6; ++m) win[m] = u[m];  // w_{n-8} .. w_{n-3}
+  }
+  for (int k = n - 2 * U; k >= 0; k -= U) {
+    double u[U], o[U];
+#pragma unroll
+    for (int r = 0; r < U; ++r) u[r] = at(k + r);
+#pragma unroll
+    for (int r = U - 1; r >= 0; --r) {
+      q1 = fma(z1, q1, u[r]);
+      q2 = fma(z1, q2, q1);
+      const double w = q2;  // w_{k+r}; window w_{k+r+1 ..} in win
+      double acc = c[0] * w;
+#pragma unroll
+      for (int m = 1; m < 7; ++m) acc = fma(c[m], win[m - 1], acc);
+#pragma unroll
+      for (int m = 5; m > 0; --m) win[m] = win[m - 1];
+      win[0] = w;
+      o[r] = acc;
+      em.add(acc);
+    }
+#pragma unroll
+    for (int r = 0; r < U; ++r) at(k + r) = o[r];
+  }
+  // win = w_0 .. w_5: the wrapped outputs j = n-6 .. n-1
+#pragma unroll
+  for (int r = 0; r < 6; ++r) {
+    double o = c[0] * tail[r];
+#pragma unroll
+    for (int m = 1; m < 7; ++m) {
+      const int t = r + m;  // window index: t < 6 -> tail[t], else w_{t-6} = win[t-6]
+      o = fma(c[m], t < 6 ? tail[t] : win[t - 6], o);
+    }
+    em.add(o);
+    at(n - 6 + r) = o;
+  }
+  return em.bad();
+}
+
 template <bool CONTIG, bool PCR, bool DBL = false>
 __global__ void __launch_bounds__(kSplineT)
     spline_tile_kernel(SplineTileArgs a, const __grid_constant__ CUtensorMap tmap) {
@@ -423,6 +574,7 @@ __global__ void __launch_bounds__(kSplineT)
 
   // ---- per-line solve (Thomas + Sherman-Morrison) and evaluation -----------
   bool bad = false;
+  bool fused_eval = false;  // contiguous double sweep: evaluated inside the solve
   if (t < lines) {
     const double* mult = a.fac;
     const double* denom = a.fac + n;
@@ -441,7 +593,16 @@ __global__ void __launch_bounds__(kSplineT)
       if (a.iir) {
         const double z1 = pk[kPcrLevels + 2];  // z1^1 of the power table
         if constexpr (DBL) {
-          if (n >= 64) {
+          if (CONTIG && n >= 64 && n % 8 == 0) {
+            // solve + evaluation in one sweep pair over the row (see iir2_eval_fused)
+            double w4[4], c[7];
+            int j0;
+            spline_eval_weights(a, L0 + t, n, -6.0 * z1, w4, j0);
+            spline_weights2(w4, c);
+            j0s[t] = (2 * j0) % n;
+            bad |= iir2_eval_fused(y, n, z1, c, (t >> 3) & 1);
+            fused_eval = true;
+          } else if (n >= 64) {
             iir_solve2(y, YS, n, z1);
           } else {
             iir_solve(y, YS, n, z1);
@@ -530,6 +691,7 @@ __global__ void __launch_bounds__(kSplineT)
     for (int k = 0; k < n; ++k) y[k * YS] = __dsub_rn(y[k * YS], __dmul_rn(fac, __ldg(z + k)));
     }  // Thomas
 
+    if (!fused_eval) {
     // evaluation weights (_kernels.pyx:62-87)
     const int64_t L = L0 + t;
     const int64_t row = a.idx ? a.idx[L] : (L / a.tdiv) % a.tmod;
@@ -683,6 +845,7 @@ __global__ void __launch_bounds__(kSplineT)
       }
     }
     }  // single sweep
+    }  // !fused_eval
   }
   __syncwarp();
   if (CONTIG) {
@@ -716,30 +879,6 @@ __global__ void __launch_bounds__(kSplineT)
 // round-off; replaces the shared-memory tile (one line per lane), whose
 // five PCR passes were shared-memory bound at 6 warps per SM.
 constexpr int kRowWarps = 8;
-
-// Evaluation weights of one line (_kernels.pyx:62-87), the gain g folded in.
-__device__ __forceinline__ void spline_eval_weights(const SplineTileArgs& a, int64_t L, int n,
-                                                    double g, double (&w)[4], int& j0) {
-  const int64_t trow = a.idx ? a.idx[L] : (L / a.tdiv) % a.tmod;
-  const double shift = __dmul_rn(a.values[trow], a.scale);
-  const double sh = __ddiv_rn(shift, a.h);
-  double off = floor(-sh);
-  double th = __dsub_rn(-sh, off);
-  if (th >= 1.0) {
-    off = __dadd_rn(off, 1.0);
-    th = 0.0;
-  }
-  const double omt = __dsub_rn(1.0, th);
-  w[0] = g * __ddiv_rn(__dmul_rn(__dmul_rn(omt, omt), omt), 6.0);
-  w[1] = g * __ddiv_rn(__dadd_rn(__dsub_rn(4.0, __dmul_rn(__dmul_rn(6.0, th), th)),
-                                 __dmul_rn(__dmul_rn(__dmul_rn(3.0, th), th), th)),
-                       6.0);
-  w[2] = g * __ddiv_rn(__dadd_rn(__dsub_rn(4.0, __dmul_rn(__dmul_rn(6.0, omt), omt)),
-                                 __dmul_rn(__dmul_rn(__dmul_rn(3.0, omt), omt), omt)),
-                       6.0);
-  w[3] = g * __ddiv_rn(__dmul_rn(__dmul_rn(th, th), th), 6.0);
-  j0 = (int)wrap_mod((int64_t)off - 1, n);
-}
 
 // H = 32 / LPW lanes per line, LPW lines per warp at a time (independent
 // scans interleave; shallower scans), NPT = n / H points per lane.

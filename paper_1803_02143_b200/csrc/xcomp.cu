@@ -97,10 +97,24 @@ struct XcStencil {
   int wl, wr;
 };
 
-// 224 registers at P >= 3 keep 3 CTAs of 96 threads (config 5) per SM
-#ifndef VPB_XCOMP_MAXNREG
-#define VPB_XCOMP_MAXNREG 224
+// Register budget.  A sub-partition holds 16K registers: at 224 per thread
+// two warps fit (8 per SM; config 5's 3-warp CTAs: 2 per SM = 6 warps), at
+// 168 three (12 per SM).  VPB_XCOMP_T2S keeps the composed x2 tables in
+// shared memory (read by broadcast loads that the compiler may not hoist),
+// which frees the 27 doubles per thread that make 168 reachable at P = 3.
+#ifndef VPB_XCOMP_T2S
+#define VPB_XCOMP_T2S 0
 #endif
+#ifndef VPB_XCOMP_MAXNREG
+#define VPB_XCOMP_MAXNREG (VPB_XCOMP_T2S ? 168 : 224)
+#endif
+
+// broadcast shared-memory load that stays in the loop (not hoisted to a register)
+__device__ __forceinline__ double lds_keep(const double* p) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"((unsigned)__cvta_generic_to_shared(p)));
+  return v;
+}
 template <int P, bool DENS, bool HALO = false>
 __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? VPB_XCOMP_MAXNREG : 168)
     dg_xcomp_kernel(const double* __restrict__ src, double* __restrict__ dst, int n1, int C2,
@@ -218,7 +232,14 @@ __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? VPB_XCOMP_MAXNREG : 
 
   const int C1 = n1 / P;
   const bool active = tid < C1;
-  double T1[3][P][P], T2[3][P][P];
+  double T1[3][P][P];
+#if VPB_XCOMP_T2S
+  __shared__ double t2s[3 * P * P];  // this item's composed x2 table {AA, AB+BA, BB}
+#define VPB_T2(s, j, m) lds_keep(t2s + ((s) * P + (j)) * P + (m))
+#else
+  double T2[3][P][P];
+#define VPB_T2(s, j, m) T2[s][j][m]
+#endif
   bool ex1 = true, ex2 = true;
   int off0 = 0, off1 = 0, off2 = 0;  // element offsets of the three x1 source cells
   int hrs0 = 0, hrs1 = 0, hrs2 = 0;  // HALO: row strides of their regions
@@ -247,7 +268,9 @@ __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? VPB_XCOMP_MAXNREG : 
 #pragma unroll
           for (int m = 0; m < P; ++m) {
             T1[s][jj][m] = __ldg(k1 + (iv1 * 3 + s) * P * P + jj * P + m);
+#if !VPB_XCOMP_T2S
             T2[s][jj][m] = __ldg(k2 + (iv2 * 3 + s) * P * P + jj * P + m);
+#endif
           }
       if constexpr (HALO) {
         // source cell j = tid - Q - 2 + k lives in the rows (0 <= j < C1) or in a
@@ -280,6 +303,11 @@ __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? VPB_XCOMP_MAXNREG : 
         off2 = up * P;
       }
     }
+#if VPB_XCOMP_T2S
+    // every thread finished the previous item (barrier after its last chunk)
+    for (int e = tid; e < 3 * P * P; e += blockDim.x) t2s[e] = __ldg(k2 + iv2 * 3 * P * P + e);
+    __syncthreads();
+#endif
     double* outp = dst + ((int64_t)iv2 * mp.nv1_glob + iv1) * plane_elems;
     for (int k = 0; k < r.nch; ++k) {
       const int t0 = k * G;
@@ -329,23 +357,44 @@ __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? VPB_XCOMP_MAXNREG : 
           }
           if (t >= 2) {
             double o[P][P];
+            if constexpr (E2) {
 #pragma unroll
-            for (int j2 = 0; j2 < P; ++j2)
+              for (int j2 = 0; j2 < P; ++j2)
 #pragma unroll
-              for (int jj = 0; jj < P; ++jj) {
-                if constexpr (E2) {
-                  o[j2][jj] = g[j2][jj];
-                } else {
-                  double acc = T2[0][j2][0] * w0[0][jj];
+                for (int jj = 0; jj < P; ++jj) o[j2][jj] = g[j2][jj];
+            } else {
+              // each table coefficient is loaded once and applied to the P
+              // x1 nodes (same per-output operation order as a jj-outer loop)
 #pragma unroll
-                  for (int m = 1; m < P; ++m) acc = fma(T2[0][j2][m], w0[m][jj], acc);
+              for (int j2 = 0; j2 < P; ++j2) {
+                double acc[P];
+                {
+                  const double c = VPB_T2(0, j2, 0);
 #pragma unroll
-                  for (int m = 0; m < P; ++m) acc = fma(T2[1][j2][m], w1[m][jj], acc);
-#pragma unroll
-                  for (int m = 0; m < P; ++m) acc = fma(T2[2][j2][m], g[m][jj], acc);
-                  o[j2][jj] = acc;
+                  for (int jj = 0; jj < P; ++jj) acc[jj] = c * w0[0][jj];
                 }
+#pragma unroll
+                for (int m = 1; m < P; ++m) {
+                  const double c = VPB_T2(0, j2, m);
+#pragma unroll
+                  for (int jj = 0; jj < P; ++jj) acc[jj] = fma(c, w0[m][jj], acc[jj]);
+                }
+#pragma unroll
+                for (int m = 0; m < P; ++m) {
+                  const double c = VPB_T2(1, j2, m);
+#pragma unroll
+                  for (int jj = 0; jj < P; ++jj) acc[jj] = fma(c, w1[m][jj], acc[jj]);
+                }
+#pragma unroll
+                for (int m = 0; m < P; ++m) {
+                  const double c = VPB_T2(2, j2, m);
+#pragma unroll
+                  for (int jj = 0; jj < P; ++jj) acc[jj] = fma(c, g[m][jj], acc[jj]);
+                }
+#pragma unroll
+                for (int jj = 0; jj < P; ++jj) o[j2][jj] = acc[jj];
               }
+            }
             ExpMax eo;
             const int oc = r.oa + t - 2;
             double* ot = outp + (int64_t)oc * cell + tid * P;
@@ -670,4 +719,67 @@ extern "C" int vpb_dg_sweep_xstencil_density(
   VPB_REQUIRE(used == nblk, "x-plane launch plan changed (%lld vs %lld CTAs)", (long long)used,
               (long long)nblk);
   return launch_xdens_reduce(work, nblk, cc, volume, rc_out, stats, st);
+}
+
+// The halo stencil pass on v2 rows [v2_0, v2_0 + v2_rows) of the shard only
+// (the sharded advance pipelines the x1 halo exchange of the next block of
+// rows against this block's pass).  src / dst / hl / hr are the whole-shard
+// buffers; the rows of one call are contiguous in each.  With the density
+// epilogue (wv1 != nullptr) the CTA slabs accumulate over the calls of one
+// pass: phase bit 1 (first call) zeroes the work buffer, bit 2 (last call)
+// reduces it to rc_out / stats.  The launch plan of a block of rows uses at
+// most the whole-shard CTA count (the work buffer's slab count), so every
+// block adds into the same fixed slabs in program order: deterministic for a
+// fixed blocking (and equal to the one-call pass up to summation order).
+extern "C" int vpb_dg_sweep_xstencil_rows(
+    const double* src, double* dst, const int64_t dims[4], int32_t order, int64_t v2_0,
+    int64_t v2_rows, const double* k1, const int64_t* q1, const double* alpha1, const double* k2,
+    const int64_t* q2, const double* alpha2, int32_t qmul, const double* hl, int32_t wl,
+    const double* hr, int32_t wr, int32_t* flag, const double* wv1, const double* wv2,
+    const double* mid_host, const double* wcell1_host, const double* wcell2_host, double volume,
+    double* work, double* rc_out, double* stats, int32_t phase, void* stream) {
+  int rc = xstencil_args(src, dst, dims, order, qmul, hl, wl, hr, wr);
+  if (rc) return rc;
+  VPB_REQUIRE(v2_0 >= 0 && v2_rows >= 0 && v2_0 + v2_rows <= dims[3], "v2 rows outside the shard");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t plane = dims[0] * dims[1];
+  const int64_t row0 = v2_0 * dims[2];  // first (v1, v2) plane of the block
+  const int64_t C2 = dims[1] / order;
+  const double* s = src + row0 * plane;
+  const double* h_l = wl ? hl + row0 * C2 * order * wl * order : nullptr;
+  const double* h_r = wr ? hr + row0 * C2 * order * wr * order : nullptr;
+  const XcMap mp{dims[2], 0, v2_0, dims[2], 1, (int)C2};
+  const XcStencil sx{qmul, h_l, h_r, wl, wr};
+  const int64_t nitems = v2_rows * dims[2];
+  if (wv1 == nullptr) {
+    if (nitems == 0) return VPB_OK;
+    const XDensity none{nullptr, nullptr, nullptr, nullptr, {}, {}};
+    VPB_XPLANE_SWITCH(order, rc = launch_xcomp<PP, false, true>(
+                                 s, dst, dims, nitems, mp, k1, q1, alpha1, k2, q2, alpha2, flag,
+                                 none, 0, st, nullptr, sx));
+    return rc;
+  }
+  VPB_REQUIRE(rc_out != nullptr && stats != nullptr, "null pointer");
+  const int64_t cc = (dims[0] / order) * C2;
+  const int64_t len = vpb_dg_xstencil_density_work_len(dims, order, wl, wr);
+  VPB_REQUIRE(len > 0, "cannot plan the x-plane launch");
+  const int64_t nblk = len / (cc + 1);
+  XDensity dn;
+  rc = xdensity_setup(&dn, order, wv1, wv2, mid_host, wcell1_host, wcell2_host, work, nblk, cc);
+  if (rc) return rc;
+  if (phase & 1) {
+    if (cudaMemsetAsync(work, 0, (size_t)len * sizeof(double), st) != cudaSuccess)
+      return check_launch("cudaMemsetAsync");
+  }
+  if (nitems) {
+    int64_t used = 0;
+    VPB_XPLANE_SWITCH(order, rc = (launch_xcomp<PP, true, true>(
+                                 s, dst, dims, nitems, mp, k1, q1, alpha1, k2, q2, alpha2, flag,
+                                 dn, 1, st, &used, sx)));
+    if (rc) return rc;
+    VPB_REQUIRE(used <= nblk, "x-plane launch plan exceeds the work buffer (%lld > %lld CTAs)",
+                (long long)used, (long long)nblk);
+  }
+  if (phase & 2) return launch_xdens_reduce(work, nblk, cc, volume, rc_out, stats, st);
+  return VPB_OK;
 }

@@ -168,6 +168,13 @@ int launch_xdens_reduce(const double* work, int64_t nblk, int64_t cc, double vol
 
 }  // namespace vpb
 
+#ifdef VPB_ONLY_P3  // quick ptxas experiments: orders 2 and 3 only
+#define VPB_XPLANE_SWITCH(order, ...)                                              \
+  switch (order) {                                                                 \
+    case 2: { constexpr int PP = 2; __VA_ARGS__; } break;                                 \
+    default: { constexpr int PP = 3; __VA_ARGS__; } break;                                \
+  }
+#else
 #define VPB_XPLANE_SWITCH(order, ...)                                              \
   switch (order) {                                                                 \
     case 1: { constexpr int PP = 1; __VA_ARGS__; } break;                                 \
@@ -180,3 +187,4 @@ int launch_xdens_reduce(const double* work, int64_t nblk, int64_t cc, double vol
     case 8: { constexpr int PP = 8; __VA_ARGS__; } break;                                 \
     default: { constexpr int PP = 9; __VA_ARGS__; } break;                                \
   }
+#endif

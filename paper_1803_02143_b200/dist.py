@@ -28,6 +28,7 @@ CPU tests substitute an oracle-backed implementation).
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -152,6 +153,24 @@ class TorchComm:
             for req in self.dist.batch_isend_irecv(ops):
                 req.wait()
 
+    def exchange_async(self, msgs: dict) -> list:
+        """Post the exchange and return its requests: ``wait(reqs)`` later
+        orders the current stream after it (NCCL) / blocks until done (gloo),
+        so device work queued in between overlaps the transfer."""
+        ops = []
+        for _, items in msgs.items():
+            for kind, sp, sbuf, rp, rbuf in items:
+                if sbuf is not None and sbuf.numel():
+                    ops.append(self.dist.P2POp(self.dist.isend, sbuf, sp, self.group, tag=kind))
+                if rbuf is not None and rbuf.numel():
+                    ops.append(self.dist.P2POp(self.dist.irecv, rbuf, rp, self.group, tag=kind))
+        return list(self.dist.batch_isend_irecv(ops)) if ops else []
+
+    @staticmethod
+    def wait(reqs: list) -> None:
+        for req in reqs:
+            req.wait()
+
     def allgather(self, local: dict) -> list:
         (t,) = local.values()
         out = [torch.empty_like(t) for _ in range(self.world)]
@@ -183,6 +202,14 @@ class VirtualComm:
             for kind, _, _, rp, rbuf in items:
                 if rbuf is not None and rbuf.numel():
                     rbuf.copy_(sent[(rank, kind, rp)])
+
+    def exchange_async(self, msgs: dict) -> list:
+        self.exchange(msgs)
+        return []
+
+    @staticmethod
+    def wait(reqs: list) -> None:
+        return None
 
     def allgather(self, local: dict) -> list:
         return [local[r] for r in range(self.world)]
@@ -287,6 +314,26 @@ class CudaOps:
             wc2.ctypes.data, volume, work.data_ptr(), rc_out.data_ptr(), stats.data_ptr(),
             self._device.stream()), "vpb_dg_sweep_xstencil_density")
 
+    def xstencil_rows(self, src, dst, dims, order, v2_0, v2_rows, k1, t1, k2, t2, qmul, hl, wl,
+                      hr, wr, flag, dens=None, phase=3):
+        """The stencil pass on v2 rows [v2_0, v2_0 + v2_rows) (one block of the
+        pipelined pass); dens as in :meth:`xstencil`, accumulated over the
+        blocks of one pass (phase bit 1: first block, bit 2: last)."""
+        L = self._lib
+        head = (src.data_ptr(), dst.data_ptr(), L.dims(dims), order, int(v2_0), int(v2_rows),
+                k1.data_ptr(), t1.q.data_ptr(), t1.alpha.data_ptr(), k2.data_ptr(),
+                t2.q.data_ptr(), t2.alpha.data_ptr(), qmul, hl.data_ptr() if wl else None, wl,
+                hr.data_ptr() if wr else None, wr, flag.data_ptr())
+        if dens is None:
+            tail = (None,) * 5 + (0.0,) + (None,) * 3
+        else:
+            wv1, wv2, mid, wc1, wc2, volume, work, rc_out, stats = dens
+            tail = (wv1.data_ptr(), wv2.data_ptr(), mid.ctypes.data, wc1.ctypes.data,
+                    wc2.ctypes.data, volume, work.data_ptr(), rc_out.data_ptr(), stats.data_ptr())
+        L.check(self.lib.vpb_dg_sweep_xstencil_rows(*head, *tail, int(phase),
+                                                     self._device.stream()),
+                "vpb_dg_sweep_xstencil_rows")
+
     def pack(self, axis, f, dims, order, cell0, width, buf):
         L = self._lib
         L.check(self.lib.vpb_halo_pack(axis, f.data_ptr(), L.dims(dims), order, cell0, width,
@@ -372,6 +419,8 @@ class ShardedSolver:
         self.order = grid.order
         self._xtab = {}
         self._geom = None
+        # v2 row blocks of the pipelined halo exchange + stencil pass (1: off)
+        self.halo_blocks = int(os.environ.get("VPB_HALO_BLOCKS", "4"))
         n1, n2 = grid.dof(0), grid.dof(1)
         self.n1, self.n2 = n1, n2
         dev = self.device
@@ -662,10 +711,15 @@ class ShardedSolver:
             msgs[r] = [(KIND_L, right, send_l, left, recv_l),
                        (KIND_R, left, send_r, right, recv_r)]
             bufs[r] = (recv_l, recv_r)
-        self.comm.exchange(msgs)
         self._halo_bytes = getattr(self, "_halo_bytes", 0) + sum(
             8 * (m[0][2].numel() * (wl > 0) + m[1][2].numel() * (wr > 0)) for m in msgs.values())
         mid, wc1, wc2, volume = self._density_consts()
+        blocks = self._row_blocks()
+        if blocks is not None:
+            self._pipelined_pass(msgs, bufs, blocks, k1, t1, k2, t2, qmul, wl, wr, flag_slot,
+                                 with_density, flags_row, stats_row, rc_parts, mark)
+            return
+        self.comm.exchange(msgs)
         mark(("sweep_x12x12" if qmul == 2 else "sweep_x12") + ("_rho" if with_density else ""))
         for r, sh in self.shards.items():
             recv_l, recv_r = bufs[r]
@@ -681,6 +735,61 @@ class ShardedSolver:
                 rc_parts[r] = rc
             self.ops.xstencil(sh.f, sh.buf, sh.dims, p, k1, t1, k2, t2, qmul, recv_l, wl,
                               recv_r, wr, fl, dens)
+            sh.swap()
+
+    def _row_blocks(self):
+        """v2 row blocks of the pipelined stencil pass (``halo_blocks`` > 1 and
+        ops that run a block of rows), else None (one exchange, one pass)."""
+        nb = int(getattr(self, "halo_blocks", 1))
+        if nb <= 1 or not hasattr(self.ops, "xstencil_rows"):
+            return None
+        nv2 = self.shards[next(iter(self.shards))].dims[3]
+        nb = min(nb, nv2)
+        edges = [round(i * nv2 / nb) for i in range(nb + 1)]
+        return [(edges[i], edges[i + 1] - edges[i]) for i in range(nb) if edges[i + 1] > edges[i]]
+
+    def _pipelined_pass(self, msgs, bufs, blocks, k1, t1, k2, t2, qmul, wl, wr, flag_slot,
+                        with_density, flags_row, stats_row, rc_parts, mark):
+        """Halo exchange and stencil pass in blocks of v2 rows:
+        the exchanges of all blocks are posted first (NCCL runs them in order
+        on its own stream), then the pass of block b waits only for block b's
+        messages, so it overlaps the transfer of blocks b+1, ...  The halo
+        buffers are [plane][x2 row][w P], so a block of v2 rows is one
+        contiguous slice of every message."""
+        p = self.order
+        reqs = []
+        for v0, nv in blocks:
+            sub = {}
+            for r, items in msgs.items():
+                d = self.shards[r].dims
+                per = d[1] * d[2]  # halo rows of one v2 row, per halo dof column
+                sub[r] = []
+                for kind, sp, sbuf, rp, rbuf in items:
+                    w = sbuf.numel() // (per * d[3]) if d[3] else 0
+                    a, b = v0 * per * w, (v0 + nv) * per * w
+                    sub[r].append((kind, sp, sbuf[a:b], rp, rbuf[a:b]))
+            reqs.append(self.comm.exchange_async(sub))
+        mark(("sweep_x12x12" if qmul == 2 else "sweep_x12") + ("_rho" if with_density else ""))
+        work = {}
+        for i, (v0, nv) in enumerate(blocks):
+            self.comm.wait(reqs[i])
+            phase = (1 if i == 0 else 0) | (2 if i + 1 == len(blocks) else 0)
+            for r, sh in self.shards.items():
+                recv_l, recv_r = bufs[r]
+                fl = flags_row[r][flag_slot:flag_slot + 1]
+                dens = None
+                if with_density:
+                    d = sh.dims
+                    if r not in work:
+                        work[r] = torch.empty(self.ops.xstencil_work(d, p, wl, wr),
+                                              dtype=torch.float64, device=sh.f.device)
+                        rc_parts[r] = torch.empty((d[1] // p) * (d[0] // p),
+                                                  dtype=torch.float64, device=sh.f.device)
+                    dens = (self.wv1, self.wv2, *self._density_consts()[:3],
+                            self._density_consts()[3], work[r], rc_parts[r], stats_row[r])
+                self.ops.xstencil_rows(sh.f, sh.buf, sh.dims, p, v0, nv, k1, t1, k2, t2, qmul,
+                                       recv_l, wl, recv_r, wr, fl, dens, phase)
+        for sh in self.shards.values():
             sh.swap()
 
     def _gather_rc(self, rc_parts: dict) -> torch.Tensor:

@@ -152,6 +152,37 @@ class NumpyOps:
             mean = np.einsum("aibjvw,i,j,v,w->", o, wc1, wc2, wa, wb, optimize=False)
             stats[0] = float(mean) / volume
 
+    def xstencil_rows(self, src, dst, dims, order, v2_0, v2_rows, k1, t1, k2, t2, qmul, hl, wl,
+                      hr, wr, flag, dens=None, phase=3):
+        """One block of v2 rows of the pipelined pass: the whole-shard pass
+        on the rows' slices (tables of the rows' v2 indices), the density
+        partials accumulated over the blocks of the pass."""
+        n1, n2, nv1, nv2 = dims
+        plane = n1 * n2 * nv1
+        a, b = v2_0 * plane, (v2_0 + v2_rows) * plane
+        sub = (n1, n2, nv1, v2_rows)
+        hw = n2 * nv1
+        hl_s = hl[v2_0 * hw * wl * order:(v2_0 + v2_rows) * hw * wl * order] if wl else hl
+        hr_s = hr[v2_0 * hw * wr * order:(v2_0 + v2_rows) * hw * wr * order] if wr else hr
+        t2s = _Tab(None, None, np.asarray(t2.q)[v2_0:v2_0 + v2_rows], None)
+        k2s = k2[v2_0:v2_0 + v2_rows]
+        out = dst[a:b]
+        sub_dens = None
+        if dens is not None:
+            wv1, wv2, mid, wc1, wc2, volume, work, rc_out, stats = dens
+            rc_tmp = torch.empty_like(rc_out)
+            st_tmp = torch.zeros_like(stats)
+            sub_dens = (wv1, wv2[v2_0:v2_0 + v2_rows], mid, wc1, wc2, volume, work, rc_tmp,
+                        st_tmp)
+        self.xstencil(src[a:b], out, sub, order, k1, t1, k2s, t2s, qmul, hl_s, wl, hr_s, wr, flag,
+                      sub_dens)
+        if dens is not None:
+            if phase & 1:
+                rc_out.zero_()
+                stats[0] = 0.0
+            rc_out += rc_tmp
+            stats[0] += st_tmp[0]
+
     def vplane(self, src, dst, dims, order, t1, t2, f1, f2):
         tmp = torch.empty_like(src)
         self.sweep(2, src, tmp, dims, order, t1, f1)

@@ -121,6 +121,24 @@ def test_virtual_sharded_advance_matches_oracle_steps(p1, tau):
     assert max_rel(solver.gather(), f) <= 1e-13
 
 
+@pytest.mark.parametrize("blocks", [2, 3, 100])
+def test_pipelined_halo_blocks_match_one_exchange(blocks):
+    """advance() with the halo exchange and stencil pass pipelined in blocks
+    of v2 rows (comm/compute overlap) equals the one-exchange
+    pass up to the summation order of the density partials."""
+    grid, og = grids()
+    out = []
+    for nb in (1, blocks):
+        dec = dist.Decomposition(grid, 2, 1)
+        solver = dist.ShardedSolver(grid, dec, dist.VirtualComm(dec.world), range(dec.world),
+                                    ops=NumpyOps(), device=torch.device("cpu"))
+        solver.halo_blocks = nb
+        solver.scatter(core.initialize(PROB, og))
+        solver.advance(TAU, 3)
+        out.append(solver.gather())
+    assert max_rel(out[1], out[0]) <= 1e-14
+
+
 @pytest.mark.parametrize("p1", [3, 5])
 def test_virtual_sharded_advance_uneven_split_falls_back_to_step(p1):
     """8 x1 cells over 3 / 5 ranks: shards of 2-3 / 1-2 cells.  Odd local dof
