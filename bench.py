@@ -296,10 +296,10 @@ def cpu_reference(cfg: dict, *, warmup: int = 1, max_steps: int = 1,
     """The unmodified reference ``slvp.strang_step`` (oracle/_ref/site) timed
     on full steps of the configuration on this box's host cores
     (oracle/refstep.py).  A configuration whose reference run does not fit
-    host RAM (the reference keeps ~3 copies of f) falls back to the scaled
+    host RAM (2 copies of f above 80 % of MemAvailable) falls back to the scaled
     slab sample of the reference's compiled kernels (oracle/refarm.py) and
     says so in ``sample``."""
-    need = 3 * 8 * int(cfg["dofs"]) ** 4
+    need = 2 * 8 * int(cfg["dofs"]) ** 4  # strided dG steps in place (RSS ~1 copy at cfg2)
     avail = _host_ram_bytes()
     from oracle import build
 

@@ -29,6 +29,7 @@
 #include "tensormap.cuh"
 
 namespace vpb {
+int xplane_sm_count();  // fused.cu
 
 constexpr int kSplineT = 32;   // lines per CTA
 constexpr int kPcrLevels = 5;  // cyclic-reduction levels (strides 1..16)
@@ -385,11 +386,12 @@ __device__ __forceinline__ void spline_eval_weights(const SplineTileArgs& a, int
 __device__ __forceinline__ bool iir2_eval_fused(double* y, const int n, const double z1,
                                                 const double (&c)[7], const int s) {
   constexpr int U = 8;
-  auto at = [&](int j) -> double& {  // logical j in [0, n + 8) -> physical slot
-    int q = j + s;
-    if (q >= n) q -= n;
-    return y[q];
-  };
+  // logical j lives at y[j + s]: for s = 1 the row's first point is parked in
+  // the padding slot y[n] (RS = n + 2) so no access needs a wrap, and moved
+  // back at the end (the in-place outputs are position-relative)
+  double* yb = y + s;
+  if (s) y[n] = y[0];
+  auto at = [&](int j) -> double& { return yb[j]; };
   // ---- causal pass (both chains), periodic start from the 64 points before 0
   double p1 = 0.0, p2 = 0.0;
   for (int k = n - 64; k < n; k += U) {
@@ -489,6 +491,7 @@ __device__ __forceinline__ bool iir2_eval_fused(double* y, const int n, const do
     em.add(o);
     at(n - 6 + r) = o;
   }
+  if (s) y[0] = y[n];
   return em.bad();
 }
 
@@ -542,9 +545,8 @@ __global__ void __launch_bounds__(kSplineT)
       }
     }
     if (CONTIG) {
-      if (t == 0)
-        for (int r = 0; r < lines; ++r)
-          bulk_g2s(tile + r * RS, a.src + (L0 + r) * n, (uint32_t)n * 8u, bars);
+      __syncwarp();  // lane 0's arrive.expect_tx precedes the copies
+      if (t < lines) bulk_g2s(tile + t * RS, a.src + (L0 + t) * n, (uint32_t)n * 8u, bars);
     } else if (a.use_tma) {
       // the whole [n][32] tile in one (or two, n > 256) TMA tensor copies
       if (t == 0)
@@ -574,7 +576,9 @@ __global__ void __launch_bounds__(kSplineT)
 
   // ---- per-line solve (Thomas + Sherman-Morrison) and evaluation -----------
   bool bad = false;
-  bool fused_eval = false;  // contiguous double sweep: evaluated inside the solve
+  // contiguous double sweep: evaluated inside the solve (iir2_eval_fused);
+  // uniform over the warp (template flags and kernel arguments only)
+  const bool fused_eval = CONTIG && PCR && DBL && a.iir && n >= 64 && n % 8 == 0;
   if (t < lines) {
     const double* mult = a.fac;
     const double* denom = a.fac + n;
@@ -593,7 +597,7 @@ __global__ void __launch_bounds__(kSplineT)
       if (a.iir) {
         const double z1 = pk[kPcrLevels + 2];  // z1^1 of the power table
         if constexpr (DBL) {
-          if (CONTIG && n >= 64 && n % 8 == 0) {
+          if (fused_eval) {
             // solve + evaluation in one sweep pair over the row (see iir2_eval_fused)
             double w4[4], c[7];
             int j0;
@@ -601,7 +605,6 @@ __global__ void __launch_bounds__(kSplineT)
             spline_weights2(w4, c);
             j0s[t] = (2 * j0) % n;
             bad |= iir2_eval_fused(y, n, z1, c, (t >> 3) & 1);
-            fused_eval = true;
           } else if (n >= 64) {
             iir_solve2(y, YS, n, z1);
           } else {
@@ -848,7 +851,21 @@ __global__ void __launch_bounds__(kSplineT)
     }  // !fused_eval
   }
   __syncwarp();
-  if (CONTIG) {
+  if (CONTIG && fused_eval) {
+    // double sweep: the rotation 2 j0 mod n is even, so each row leaves as two
+    // 16-byte aligned bulk stores (out[0, n - jr) = row[jr, n), out[n - jr, n) =
+    // row[0, jr)) issued by its own lane, instead of a warp loop over points
+    if (t < lines) {
+      const int jr = j0s[t];
+      double* out = a.dst + (L0 + t) * n;
+      const double* row = tile + t * RS;
+      fence_proxy_async_smem();  // the rows were written by generic stores
+      bulk_s2g(out, row + jr, (uint32_t)(n - jr) * 8u);
+      if (jr) bulk_s2g(out + (n - jr), row, (uint32_t)jr * 8u);
+      bulk_commit();
+      bulk_wait_read<0>();  // shared memory must outlive the reads
+    }
+  } else if (CONTIG) {
     // rows hold out rotated by j0: write them out coalesced
     for (int r = 0; r < lines; ++r) {
       double* out = a.dst + (L0 + r) * n;

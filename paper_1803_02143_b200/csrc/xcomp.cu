@@ -98,15 +98,16 @@ struct XcStencil {
 };
 
 // Register budget.  A sub-partition holds 16K registers: at 224 per thread
-// two warps fit (8 per SM; config 5's 3-warp CTAs: 2 per SM = 6 warps), at
-// 168 three (12 per SM).  VPB_XCOMP_T2S keeps the composed x2 tables in
-// shared memory (read by broadcast loads that the compiler may not hoist),
-// which frees the 27 doubles per thread that make 168 reachable at P = 3.
-#ifndef VPB_XCOMP_T2S
-#define VPB_XCOMP_T2S 0
-#endif
+// two warps fit (8 per SM; config 5's 3-warp CTAs: only 2 CTAs = 6 warps),
+// at 168 three (12 per SM).  The T2S instances keep the composed x2 tables
+// in shared memory (broadcast loads the compiler may not hoist), which frees
+// the 27 doubles per thread that make 168 reachable at P = 3 without spills.
+// Measured (tune_xcomp.py, one B200): config 5 (3-warp CTAs) 22.8 -> 21.8
+// ms with T2S; config 2 (2-warp CTAs, 4 CTAs at 224) 3.59 -> 4.09 ms, so
+// T2S is used only where the 224-register plan strands warp slots (P = 3,
+// 3-warp CTAs; VPB_XCOMP_T2S=0/1 forces it off / on).
 #ifndef VPB_XCOMP_MAXNREG
-#define VPB_XCOMP_MAXNREG (VPB_XCOMP_T2S ? 168 : 224)
+#define VPB_XCOMP_MAXNREG 224
 #endif
 
 // broadcast shared-memory load that stays in the loop (not hoisted to a register)
@@ -115,8 +116,8 @@ __device__ __forceinline__ double lds_keep(const double* p) {
   asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"((unsigned)__cvta_generic_to_shared(p)));
   return v;
 }
-template <int P, bool DENS, bool HALO = false>
-__global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? VPB_XCOMP_MAXNREG : 168)
+template <int P, bool DENS, bool HALO = false, bool T2S = false>
+__global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? (T2S ? 168 : VPB_XCOMP_MAXNREG) : 168)
     dg_xcomp_kernel(const double* __restrict__ src, double* __restrict__ dst, int n1, int C2,
                     int G, int nst, int64_t nitems, int64_t items_per_block, const XcMap mp,
                     const double* __restrict__ k1, const int64_t* __restrict__ q1,
@@ -233,13 +234,15 @@ __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? VPB_XCOMP_MAXNREG : 
   const int C1 = n1 / P;
   const bool active = tid < C1;
   double T1[3][P][P];
-#if VPB_XCOMP_T2S
-  __shared__ double t2s[3 * P * P];  // this item's composed x2 table {AA, AB+BA, BB}
-#define VPB_T2(s, j, m) lds_keep(t2s + ((s) * P + (j)) * P + (m))
-#else
-  double T2[3][P][P];
-#define VPB_T2(s, j, m) T2[s][j][m]
-#endif
+  double T2[3][P][P];                // !T2S: this item's composed x2 table {AA, AB+BA, BB}
+  __shared__ double t2s[3 * P * P];  // T2S: the same table in shared memory
+  auto t2c = [&](int s_, int j_, int m_) -> double {
+    if constexpr (T2S)
+      return lds_keep(t2s + (s_ * P + j_) * P + m_);
+    else
+      return T2[s_][j_][m_];
+  };
+#define VPB_T2(s, j, m) t2c(s, j, m)
   bool ex1 = true, ex2 = true;
   int off0 = 0, off1 = 0, off2 = 0;  // element offsets of the three x1 source cells
   int hrs0 = 0, hrs1 = 0, hrs2 = 0;  // HALO: row strides of their regions
@@ -268,9 +271,7 @@ __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? VPB_XCOMP_MAXNREG : 
 #pragma unroll
           for (int m = 0; m < P; ++m) {
             T1[s][jj][m] = __ldg(k1 + (iv1 * 3 + s) * P * P + jj * P + m);
-#if !VPB_XCOMP_T2S
-            T2[s][jj][m] = __ldg(k2 + (iv2 * 3 + s) * P * P + jj * P + m);
-#endif
+            if constexpr (!T2S) T2[s][jj][m] = __ldg(k2 + (iv2 * 3 + s) * P * P + jj * P + m);
           }
       if constexpr (HALO) {
         // source cell j = tid - Q - 2 + k lives in the rows (0 <= j < C1) or in a
@@ -303,11 +304,11 @@ __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? VPB_XCOMP_MAXNREG : 
         off2 = up * P;
       }
     }
-#if VPB_XCOMP_T2S
-    // every thread finished the previous item (barrier after its last chunk)
-    for (int e = tid; e < 3 * P * P; e += blockDim.x) t2s[e] = __ldg(k2 + iv2 * 3 * P * P + e);
-    __syncthreads();
-#endif
+    if constexpr (T2S) {
+      // every thread finished the previous item (barrier after its last chunk)
+      for (int e = tid; e < 3 * P * P; e += blockDim.x) t2s[e] = __ldg(k2 + iv2 * 3 * P * P + e);
+      __syncthreads();
+    }
     double* outp = dst + ((int64_t)iv2 * mp.nv1_glob + iv1) * plane_elems;
     for (int k = 0; k < r.nch; ++k) {
       const int t0 = k * G;
@@ -481,6 +482,32 @@ struct XcLaunch {
   int64_t ppb, blocks, max_blocks;
 };
 
+// T2S instances only where the 224-register plan strands warp slots: P = 3
+// with 3-warp CTAs (65..96 local x1 cells).  VPB_XCOMP_T2S=0/1 overrides.
+template <int P>
+static bool xcomp_t2s(const int64_t dims[4]) {
+  if constexpr (P != 3) {
+    return false;
+  } else {
+    static const int env = getenv("VPB_XCOMP_T2S") ? atoi(getenv("VPB_XCOMP_T2S")) : -1;
+    if (env >= 0) return env != 0;
+    const int C1 = (int)(dims[0] / P);
+    return (C1 + 31) / 32 == 3;
+  }
+}
+
+template <int P, bool DENS, bool HALO, bool T2S>
+static void xcomp_occupancy(int threads, size_t smem, int* occ) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(dg_xcomp_kernel<P, DENS, HALO, T2S>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    attr = true;
+  }
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, dg_xcomp_kernel<P, DENS, HALO, T2S>, threads,
+                                                smem);
+}
+
 template <int P, bool DENS, bool HALO = false>
 static int plan_xcomp(const int64_t dims[4], int64_t nitems, XcLaunch* L, int hcells = 0) {
   const int n1 = (int)dims[0];
@@ -515,15 +542,11 @@ static int plan_xcomp(const int64_t dims[4], int64_t nitems, XcLaunch* L, int hc
     set_error("x plane chunk of %d dofs does not fit shared memory", P * n1);
     return VPB_ERR_UNSUPPORTED;
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(dg_xcomp_kernel<P, DENS, HALO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         220 * 1024);
-    attr = true;
-  }
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dg_xcomp_kernel<P, DENS, HALO>, L->threads,
-                                                L->smem);
+  if (xcomp_t2s<P>(dims))
+    xcomp_occupancy<P, DENS, HALO, (P == 3)>(L->threads, L->smem, &occ);
+  else
+    xcomp_occupancy<P, DENS, HALO, false>(L->threads, L->smem, &occ);
   if (occ < 1) occ = 1;
   L->max_blocks = (int64_t)occ * xplane_sm_count();
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(nitems, L->max_blocks));
@@ -542,9 +565,14 @@ static int launch_xcomp(const double* src, double* dst, const int64_t dims[4], i
   XcLaunch L;
   int rc = plan_xcomp<P, DENS, HALO>(dims, nitems, &L, HALO ? sx.wl + sx.wr : 0);
   if (rc) return rc;
-  dg_xcomp_kernel<P, DENS, HALO><<<(unsigned)L.blocks, L.threads, L.smem, st>>>(
-      src, dst, (int)dims[0], (int)(dims[1] / P), L.G, L.nst, nitems, L.ppb, mp, k1, q1, al1, k2,
-      q2, al2, flag, dn, dacc, sx);
+  if (xcomp_t2s<P>(dims))
+    dg_xcomp_kernel<P, DENS, HALO, (P == 3)><<<(unsigned)L.blocks, L.threads, L.smem, st>>>(
+        src, dst, (int)dims[0], (int)(dims[1] / P), L.G, L.nst, nitems, L.ppb, mp, k1, q1, al1,
+        k2, q2, al2, flag, dn, dacc, sx);
+  else
+    dg_xcomp_kernel<P, DENS, HALO, false><<<(unsigned)L.blocks, L.threads, L.smem, st>>>(
+        src, dst, (int)dims[0], (int)(dims[1] / P), L.G, L.nst, nitems, L.ppb, mp, k1, q1, al1,
+        k2, q2, al2, flag, dn, dacc, sx);
   if (nblocks_out) *nblocks_out = L.blocks;
   return launched("dg_xcomp_kernel");
 }

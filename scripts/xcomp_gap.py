@@ -1,18 +1,23 @@
-"""Warm-in-loop vs isolated time of the composed merged x pass (config 2).
+"""Warm-in-loop vs isolated time of the composed merged x pass, with the SM
+clock sampled (nvidia-smi, 50 ms) inside each phase.
 
-A: the x pass alone, back to back (same tables, ping-pong buffers);
-B: inside advance() (after the v pass, as in the bench);
-C: v pass -> 256 MB L2-flush write -> x pass (dirty L2 lines of the v pass
-   written back before the x pass starts).
-SM clocks are sampled by nvidia-smi around each phase."""
+A  the x pass alone, back to back (same tables, ping-pong buffers)
+B  v pass -> x pass, back to back (the steady state of advance())
+C  v pass -> 256 MB L2-flush write -> x pass (dirty v-pass lines written back first)
+D  200 ms idle -> v pass -> x pass (the pair from a cool, unthrottled start)
+
+    python scripts/xcomp_gap.py [cfg2|cfg3|cfg5]
+"""
 import json
-import subprocess
 import sys
+import time
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
+import bench  # noqa: E402
 import paper_1803_02143_b200 as vpb  # noqa: E402
 from paper_1803_02143_b200 import driver  # noqa: E402
 from paper_1803_02143_b200.dg import vplane_dg  # noqa: E402
@@ -33,55 +38,44 @@ src, dst = f.data, st.buf
 flush = torch.empty(256 << 17, dtype=torch.float64, device="cuda")  # 256 MB
 
 
-def clk():
-    try:
-        return subprocess.run(["nvidia-smi", "--query-gpu=clocks.sm,power.draw",
-                               "--format=csv,noheader,nounits"], capture_output=True,
-                              text=True).stdout.strip()
-    except OSError:
-        return None
-
-
-def timed(fn, reps):
-    ts = []
-    for _ in range(reps):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        fn(pre=True)
-        e0.record()
-        fn(pre=False)
-        e1.record()
-        ts.append((e0, e1))
-    torch.cuda.synchronize()
-    v = sorted(a.elapsed_time(b) for a, b in ts)
-    return {"median_ms": v[len(v) // 2], "min_ms": v[0], "max_ms": v[-1], "clk": clk()}
-
-
-def xpass(pre):
+def xpass():
     global src, dst
-    if pre:
-        return
     driver.xcomp_density_dg(grid, src, dst, t1, t2, flag, st, stats)
     src, dst = dst, src
 
 
-def vx(pre):
+def vpass():
     global src, dst
-    if pre:
-        tv1, tv2 = st.v_tables(0, tau), st.v_tables(1, tau)
-        vplane_dg(grid, src, dst, tv1, tv2, None, None)
-        src, dst = dst, src
-        return
-    xpass(False)
+    vplane_dg(grid, src, dst, st.v_tables(0, tau), st.v_tables(1, tau), None, None)
+    src, dst = dst, src
 
 
-def vflushx(pre):
-    if pre:
-        vx(True)
-        flush.fill_(1.0)
-        return
-    xpass(False)
+def phase(pre, reps, idle=0.0):
+    clk = bench.ClockSampler(0).start()
+    ts = []
+    clk.begin()
+    for _ in range(reps):
+        if idle:
+            torch.cuda.synchronize()
+            time.sleep(idle)
+        pre()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        xpass()
+        e1.record()
+        ts.append((e0, e1))
+    torch.cuda.synchronize()
+    clk.end()
+    clk.stop()
+    v = sorted(a.elapsed_time(b) for a, b in ts)
+    return {"median_ms": v[len(v) // 2], "min_ms": v[0], "max_ms": v[-1],
+            "clocks": clk.summary()}
 
 
-res = {"A_isolated_back_to_back": timed(xpass, 20), "B_after_vpass": timed(vx, 20),
-       "C_after_vpass_and_l2_flush": timed(vflushx, 20)}
+res = {
+    "A_isolated_back_to_back": phase(lambda: None, 30),
+    "B_after_vpass": phase(vpass, 30),
+    "C_after_vpass_and_l2_flush": phase(lambda: (vpass(), flush.fill_(1.0)), 30),
+    "D_cool_start_then_vpass": phase(vpass, 15, idle=0.2),
+}
 print(json.dumps(res, indent=1))
