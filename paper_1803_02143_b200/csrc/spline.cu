@@ -366,130 +366,159 @@ __device__ __forceinline__ void spline_eval_weights(const SplineTileArgs& a, int
   j0 = (int)wrap_mod((int64_t)off - 1, n);
 }
 
-// Contiguous-axis double sweep, one line per lane in a [line][RS] tile:
-// the two recursive-filter solves (iir_solve2) with the 7-tap evaluation of
-// the double sweep fused into the anticausal pass, so the solved values are
-// never re-read from shared memory: walking backwards, w_j is ready when
-// w_{j+1..j+6} are still in registers, and out at in-place position j
-// (= sum_m c_m w_{j+m}, the rotated layout of the unfused path) replaces
-// the causal value just consumed at j.  The six positions whose window
-// wraps past the end (j >= n-6) are emitted last, from saved values.
+// Contiguous-axis sweep (single, or the double sweep of merged half steps),
+// one line per lane in a [line][RS] tile: the recursive-filter solve
+// (iir_solve / iir_solve2) with the evaluation fused into the anticausal
+// pass, so the solved values are never re-read from shared memory: walking
+// backwards, w_j is ready while w_{j+1} .. w_{j+TAPS-1} are still in
+// registers, and out at position j (= sum_m c_m w_{j+m}; single sweep: the
+// reference's 4-tap order with separate roundings, _kernels.pyx:88-93) goes
+// to in-place slot j + sigma, whose causal value has already been consumed.
+// The TAPS-1 positions whose window wraps past the end are emitted last,
+// from saved values.  sigma = rotation & 1 makes the row's rotation
+// (j0, or 2 j0 for the double sweep) plus sigma even, so the row leaves by
+// two 16-byte aligned bulk stores (the caller's write-out).
 //
 // Bank conflicts: with the row stride RS = n + 2 (even, for 16-byte bulk
 // copy destinations) lanes t and t + 8 of a half-warp hit the same bank
 // pair at equal point index.  Lanes with bit 3 set therefore walk their line
 // starting at point 1 (logical index j lives at physical (j + s) mod n,
 // s = (lane >> 3) & 1): the periodic filters may start anywhere (their
-// periodic start values are sums over the 64 preceding points), so only the
+// periodic start values are sums over the preceding points), so only the
 // rounding of the two half-warps' lines differs.  Requires n >= 64, n % 8 == 0.
 // Returns true when an output is not finite.
-__device__ __forceinline__ bool iir2_eval_fused(double* y, const int n, const double z1,
-                                                const double (&c)[7], const int s) {
+template <bool DBL>
+__device__ __forceinline__ bool iir_eval_fused(double* y, const int n, const double z1,
+                                               const double (&c)[DBL ? 7 : 4], const int s,
+                                               const int sigma) {
   constexpr int U = 8;
+  constexpr int TAPS = DBL ? 7 : 4;
+  constexpr int D = TAPS - 1;      // deferred (wrapped) outputs
+  constexpr int WARM = DBL ? 64 : 32;
   // logical j lives at y[j + s]: for s = 1 the row's first point is parked in
   // the padding slot y[n] (RS = n + 2) so no access needs a wrap, and moved
   // back at the end (the in-place outputs are position-relative)
   double* yb = y + s;
   if (s) y[n] = y[0];
-  auto at = [&](int j) -> double& { return yb[j]; };
-  // ---- causal pass (both chains), periodic start from the 64 points before 0
+  auto eval = [&](double w, const double (&win)[D]) -> double {
+    if constexpr (DBL) {
+      double o = c[0] * w;
+#pragma unroll
+      for (int m = 1; m < TAPS; ++m) o = fma(c[m], win[m - 1], o);
+      return o;
+    } else {  // out = w0 w_j + w1 w_{j+1} + w2 w_{j+2} + w3 w_{j+3}, left to right
+      double o = __dmul_rn(c[0], w);
+      o = __dadd_rn(o, __dmul_rn(c[1], win[0]));
+      o = __dadd_rn(o, __dmul_rn(c[2], win[1]));
+      return __dadd_rn(o, __dmul_rn(c[3], win[2]));
+    }
+  };
+  // ---- causal pass, periodic start from the WARM points before 0
   double p1 = 0.0, p2 = 0.0;
-  for (int k = n - 64; k < n; k += U) {
+  for (int k = n - WARM; k < n; k += U) {
     double u[U];
 #pragma unroll
-    for (int r = 0; r < U; ++r) u[r] = at(k + r);
+    for (int r = 0; r < U; ++r) u[r] = yb[k + r];
 #pragma unroll
     for (int r = 0; r < U; ++r) {
       p1 = fma(z1, p1, u[r]);
-      p2 = fma(z1, p2, p1);
+      if constexpr (DBL) p2 = fma(z1, p2, p1);
     }
   }
   for (int k = 0; k < n; k += U) {
     double u[U];
 #pragma unroll
-    for (int r = 0; r < U; ++r) u[r] = at(k + r);
+    for (int r = 0; r < U; ++r) u[r] = yb[k + r];
 #pragma unroll
     for (int r = 0; r < U; ++r) {
       p1 = fma(z1, p1, u[r]);
-      p2 = fma(z1, p2, p1);
-      u[r] = p2;
+      if constexpr (DBL) {
+        p2 = fma(z1, p2, p1);
+        u[r] = p2;
+      } else {
+        u[r] = p1;
+      }
     }
 #pragma unroll
-    for (int r = 0; r < U; ++r) at(k + r) = u[r];
+    for (int r = 0; r < U; ++r) yb[k + r] = u[r];
   }
-  // ---- anticausal pass, periodic start from the 64 points after n - 1
+  // ---- anticausal pass, periodic start from the WARM points after n - 1
   double q1 = 0.0, q2 = 0.0;
-  for (int k = 64 - U; k >= 0; k -= U) {
+  for (int k = WARM - U; k >= 0; k -= U) {
     double u[U];
 #pragma unroll
-    for (int r = 0; r < U; ++r) u[r] = at(k + r);
+    for (int r = 0; r < U; ++r) u[r] = yb[k + r];
 #pragma unroll
     for (int r = U - 1; r >= 0; --r) {
       q1 = fma(z1, q1, u[r]);
-      q2 = fma(z1, q2, q1);
+      if constexpr (DBL) q2 = fma(z1, q2, q1);
     }
   }
+  auto chain = [&](double u) -> double {
+    q1 = fma(z1, q1, u);
+    if constexpr (DBL) {
+      q2 = fma(z1, q2, q1);
+      return q2;
+    } else {
+      return q1;
+    }
+  };
   ExpMax em;
-  double win[6];  // w_{j+1} .. w_{j+6}
-  double tail[6]; // w_{n-6} .. w_{n-1} (the wrapped windows' second halves)
-  // first block: j = n-1 .. n-8; outputs only for j <= n-7
+  double win[D];   // w_{j+1} .. w_{j+D}
+  double tail[D];  // w_{n-D} .. w_{n-1} (the wrapped windows' first parts)
+  // first block: j = n-8 .. n-1; outputs only for j <= n-TAPS
   {
     const int k = n - U;
     double u[U];
 #pragma unroll
-    for (int r = 0; r < U; ++r) u[r] = at(k + r);
+    for (int r = 0; r < U; ++r) u[r] = yb[k + r];
 #pragma unroll
-    for (int r = U - 1; r >= 0; --r) {
-      q1 = fma(z1, q1, u[r]);
-      q2 = fma(z1, q2, q1);
-      u[r] = q2;  // w_{k+r}
+    for (int r = U - 1; r >= 0; --r) u[r] = chain(u[r]);  // w_{k+r}
+#pragma unroll
+    for (int r = 0; r < D; ++r) tail[r] = u[U - D + r];
+    double o[U - D];
+#pragma unroll
+    for (int r = U - D - 1; r >= 0; --r) {
+      double wv[D];
+#pragma unroll
+      for (int m = 0; m < D; ++m) wv[m] = u[r + 1 + m];
+      o[r] = eval(u[r], wv);
+      em.add(o[r]);
     }
 #pragma unroll
-    for (int r = 0; r < 6; ++r) tail[r] = u[r + 2];  // w_{n-6..n-1}
-    // outputs j = n-7, n-8 (windows w_{j..j+6} inside this block)
+    for (int r = 0; r < U - D; ++r) yb[k + r + sigma] = o[r];
 #pragma unroll
-    for (int r = 1; r >= 0; --r) {
-      double o = c[0] * u[r];
-#pragma unroll
-      for (int m = 1; m < 7; ++m) o = fma(c[m], u[r + m], o);
-      em.add(o);
-      at(k + r) = o;
-    }
-#pragma unroll
-    for (int m = 0; m < 6; ++m) win[m] = u[m];  // w_{n-8} .. w_{n-3}
+    for (int m = 0; m < D; ++m) win[m] = u[m];  // w_{n-8} .. w_{n-8+D-1}
   }
   for (int k = n - 2 * U; k >= 0; k -= U) {
     double u[U], o[U];
 #pragma unroll
-    for (int r = 0; r < U; ++r) u[r] = at(k + r);
+    for (int r = 0; r < U; ++r) u[r] = yb[k + r];
 #pragma unroll
     for (int r = U - 1; r >= 0; --r) {
-      q1 = fma(z1, q1, u[r]);
-      q2 = fma(z1, q2, q1);
-      const double w = q2;  // w_{k+r}; window w_{k+r+1 ..} in win
-      double acc = c[0] * w;
+      const double w = chain(u[r]);  // w_{k+r}; window w_{k+r+1 ..} in win
+      o[r] = eval(w, win);
 #pragma unroll
-      for (int m = 1; m < 7; ++m) acc = fma(c[m], win[m - 1], acc);
-#pragma unroll
-      for (int m = 5; m > 0; --m) win[m] = win[m - 1];
+      for (int m = D - 1; m > 0; --m) win[m] = win[m - 1];
       win[0] = w;
-      o[r] = acc;
-      em.add(acc);
+      em.add(o[r]);
     }
 #pragma unroll
-    for (int r = 0; r < U; ++r) at(k + r) = o[r];
+    for (int r = 0; r < U; ++r) yb[k + r + sigma] = o[r];
   }
-  // win = w_0 .. w_5: the wrapped outputs j = n-6 .. n-1
+  // win = w_0 .. w_{D-1}: the wrapped outputs j = n-D .. n-1
 #pragma unroll
-  for (int r = 0; r < 6; ++r) {
-    double o = c[0] * tail[r];
+  for (int r = 0; r < D; ++r) {
+    double wv[D];
 #pragma unroll
-    for (int m = 1; m < 7; ++m) {
-      const int t = r + m;  // window index: t < 6 -> tail[t], else w_{t-6} = win[t-6]
-      o = fma(c[m], t < 6 ? tail[t] : win[t - 6], o);
+    for (int m = 0; m < D; ++m) {
+      const int t = r + 1 + m;  // window index: t < D -> tail[t], else w_{t-D} = win[t-D]
+      wv[m] = t < D ? tail[t] : win[t - D];
     }
+    const double o = eval(tail[r], wv);
     em.add(o);
-    at(n - 6 + r) = o;
+    const int slot = n - D + r + sigma;
+    yb[slot >= n ? slot - n : slot] = o;
   }
   if (s) y[0] = y[n];
   return em.bad();
@@ -576,9 +605,9 @@ __global__ void __launch_bounds__(kSplineT)
 
   // ---- per-line solve (Thomas + Sherman-Morrison) and evaluation -----------
   bool bad = false;
-  // contiguous double sweep: evaluated inside the solve (iir2_eval_fused);
-  // uniform over the warp (template flags and kernel arguments only)
-  const bool fused_eval = CONTIG && PCR && DBL && a.iir && n >= 64 && n % 8 == 0;
+  // contiguous recursive-filter sweeps: evaluated inside the solve
+  // (iir_eval_fused); uniform over the warp (template flags and arguments)
+  const bool fused_eval = CONTIG && PCR && a.iir && n >= 64 && n % 8 == 0;
   if (t < lines) {
     const double* mult = a.fac;
     const double* denom = a.fac + n;
@@ -596,16 +625,25 @@ __global__ void __launch_bounds__(kSplineT)
       const double* pk = a.fac + 4 * n + 7;
       if (a.iir) {
         const double z1 = pk[kPcrLevels + 2];  // z1^1 of the power table
-        if constexpr (DBL) {
-          if (fused_eval) {
-            // solve + evaluation in one sweep pair over the row (see iir2_eval_fused)
-            double w4[4], c[7];
-            int j0;
-            spline_eval_weights(a, L0 + t, n, -6.0 * z1, w4, j0);
+        if (fused_eval) {
+          // solve + evaluation in one pass pair over the row (iir_eval_fused);
+          // j0s = the row's (even) rotation for the bulk-store write-out
+          double w4[4];
+          int j0;
+          spline_eval_weights(a, L0 + t, n, -6.0 * z1, w4, j0);
+          if constexpr (DBL) {
+            double c[7];
             spline_weights2(w4, c);
-            j0s[t] = (2 * j0) % n;
-            bad |= iir2_eval_fused(y, n, z1, c, (t >> 3) & 1);
-          } else if (n >= 64) {
+            const int jr = (2 * j0) % n;  // even: n is even
+            j0s[t] = jr;
+            bad |= iir_eval_fused<true>(y, n, z1, c, (t >> 3) & 1, 0);
+          } else {
+            const int sigma = j0 & 1;
+            j0s[t] = (j0 + sigma) % n;
+            bad |= iir_eval_fused<false>(y, n, z1, w4, (t >> 3) & 1, sigma);
+          }
+        } else if constexpr (DBL) {
+          if (n >= 64) {
             iir_solve2(y, YS, n, z1);
           } else {
             iir_solve(y, YS, n, z1);
@@ -1123,7 +1161,13 @@ static int launch_spline(SplineTileArgs a, bool contig, bool exact, cudaStream_t
   // beats the warp-per-line rows kernel (1.30 ms, shuffle-latency bound);
   // VPB_SPLINE_DBL_ROWS=1 selects the rows kernel
   static const bool dbl_rows = getenv("VPB_SPLINE_DBL_ROWS") != nullptr;
-  const bool rows_ok = contig && pcr && !no_rows && !(a.dbl && !dbl_rows) && a.n % 32 == 0 &&
+  // single contiguous sweeps: the tile kernel with the fused evaluation and
+  // bulk-store write-out (n >= 64, n % 8 == 0) beats the warp-per-line rows
+  // kernel; VPB_SPLINE_ROWS=1 selects the rows kernel for them
+  static const bool force_rows = getenv("VPB_SPLINE_ROWS") != nullptr;
+  const bool tile_fused = a.iir && a.n >= 64 && a.n % 8 == 0 && !force_rows;
+  const bool rows_ok = contig && pcr && !no_rows && !(a.dbl && !dbl_rows) && !tile_fused &&
+                       a.n % 32 == 0 &&
                        (npt == 1 || npt == 2 || npt == 4 || npt == 8) &&
                        (reinterpret_cast<uintptr_t>(a.src) & 15) == 0;
   if (rows_ok) {

@@ -9,6 +9,16 @@ NVLink share can be estimated.  This is a projection, not a multi-GPU
 measurement.
 
     python scripts/emulate_shards.py --config cfg2 --worlds 1 2 4 8 --steps 5
+    python scripts/emulate_shards.py --config cfg5 --worlds 2 4 8 --vshard
+
+--vshard evaluates VELOCITY-direction sharding (the paper's own choice,
+PAPER.md:609-613): rank r holds the v2 slab f[V_r][v1][x2][x1],
+so every x pass (x1, x2 and the merged composed pass) is local and runs on
+whole (x1, x2) planes, and only the v2 sweep of the v pass needs halo cells
+(E-shifts of at most one v2 cell here: one cell on each side).  One rank's
+compute is emulated as advance() on the slab grid (nv2 / W + 2 halo cells
+of v2, periodic instead of halo-fed v2: the same kernels and bytes); the
+density becomes a partial sum per rank plus an allreduce of n1 n2 doubles.
 """
 
 from __future__ import annotations
@@ -29,6 +39,7 @@ def main() -> None:
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--worlds", type=int, nargs="+", default=[1, 2, 4, 8])
     ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--vshard", action="store_true", help="v2-slab sharding (see doc)")
     args = ap.parse_args()
     import gc
 
@@ -43,6 +54,31 @@ def main() -> None:
     grid = vpb.make_grid(problem, "dg", dofs, dg_order=order)
     N = grid.total_dof
     for w in args.worlds:
+        if args.vshard:
+            cells_v2 = grid.axes[3].count // w + 2  # the slab plus one halo cell per side
+            slab = vpb.make_grid(problem, "dg", (grid.dof(0), grid.dof(1), grid.dof(2),
+                                                 cells_v2 * order), dg_order=order)
+            f = vpb.initialize(problem, slab)
+            f = vpb.advance(f, tau, 2, consume=True)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            f = vpb.advance(f, tau, args.steps, consume=True)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / args.steps
+            halo = 2 * order * grid.dof(0) * grid.dof(1) * grid.dof(2) * 8
+            print(json.dumps({"config": args.config, "world": w, "layout": f"v2 x{w}",
+                              "per_rank_compute_ms_per_step": ms,
+                              "projected_dof_per_s_compute_only": N / (ms * 1e-3),
+                              "v2_cells_per_rank_incl_halo": cells_v2,
+                              "halo_bytes_per_rank_per_step": int(halo),
+                              "rho_allreduce_bytes": 8 * grid.dof(0) * grid.dof(1)}), flush=True)
+            del f
+            driver._state_cached.cache_clear()
+            gc.collect()
+            torch.cuda.empty_cache()
+            continue
         if w == 1:
             f = vpb.initialize(problem, grid)
             f = vpb.advance(f, tau, 2, consume=True)
