@@ -370,7 +370,14 @@ def run_sharded(args, cfg_name: str, cfg: dict, d, world: int, rank: int, local:
     grid = vpb.make_grid(problem, cfg["method"], cfg["dofs"], dg_order=cfg["order"])
     N = grid.total_dof
     tau = cfg["tau"]
-    if cfg["method"] == "dg":
+    if cfg["method"] == "dg" and args.layout == "v":
+        # velocity sharding (the paper's decomposition): v2 slabs, local x
+        # passes, one v2 halo exchange per step (dist.VShardedSolver)
+        solver = dist.VShardedSolver(grid, dist.TorchComm(), [rank], world)
+        local_f = lambda: solver.local(solver.f[rank], rank)  # noqa: E731
+        layout = (f"v2-shard x{world} (local x passes; NCCL v2 halos of {solver.H} cells "
+                  "per side, zero-copy; rho partials all-gathered)")
+    elif cfg["method"] == "dg":
         # x1 shards when the merged stencil pass applies (its halo fits a
         # shard), else the process grid (x1 x x2 at 8 GPUs)
         solver = dist.ShardedSolver(grid, dist.Decomposition(grid, world, 1), dist.TorchComm(),
@@ -460,7 +467,10 @@ def run_sharded(args, cfg_name: str, cfg: dict, d, world: int, rank: int, local:
         s0.record(stream)
         for _ in range(k_e2e):
             local_f().copy_(host, non_blocking=True)
-            solver.step(tau)
+            if hasattr(solver, "advance"):
+                solver.advance(tau, 1)
+            else:
+                solver.step(tau)
             host.copy_(local_f(), non_blocking=True)
         s1.record(stream)
         torch.cuda.synchronize()
@@ -750,6 +760,9 @@ def main() -> None:
                     help="time per-step calls replayed from CUDA graphs (driver.StepGraph)")
     ap.add_argument("--per-step", action="store_true",
                     help="time one strang_step call per step instead of advance()")
+    ap.add_argument("--layout", default="v", choices=["v", "x"],
+                    help="N > 1, dG: v2 slabs (VShardedSolver, default) or x1 / x1 x x2 "
+                         "shards (ShardedSolver)")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent replicas instead of the sharded field")
     ap.add_argument("--ref-budget", type=float, default=240.0,

@@ -261,6 +261,19 @@ int vpb_dg_sweep_xstencil_rows(const double* src, double* dst, const int64_t dim
                                const double* wcell2_host, double volume, double* work,
                                double* rc_out, double* stats, int32_t phase, void* stream);
 
+/* Fused v1 v2 pass of one v2 shard of a velocity-sharded field
+ * (dist.VShardedSolver): `src` holds src_v2_cells v2 cells -- the shard's
+ * dims[3]/order cells starting at cell v2_offset, neighbour halo cells
+ * before and after (contiguous rows: v2 is the outermost axis) -- and `dst`
+ * the shard's cells.  Replaces _advect_velocity (driver.py:231-242) on the
+ * shard; halo_flag is raised if a shift needs a cell beyond the halos. */
+int vpb_dg_sweep_vplane_v2halo(const double* src, double* dst, const int64_t dims[4],
+                               int32_t order, int32_t src_v2_cells, int32_t v2_offset,
+                               const double* a1, const double* b1, const int64_t* q1,
+                               const double* alpha1, const double* a2, const double* b2,
+                               const int64_t* q2, const double* alpha2, int32_t* flag1,
+                               int32_t* flag2, int32_t* halo_flag, void* stream);
+
 /* One spline sweep along `axis`; shift of line = values[table row]*scale. */
 int vpb_spline_sweep_axis(int32_t axis, const double* src, double* dst, const int64_t dims[4],
                           const double* values, double scale, double h, int32_t* flag,

@@ -689,7 +689,15 @@ __global__ void __launch_bounds__(32 * kVCells)
 constexpr int kVSpan = 3;    // window = kVCells + kVSpan cells (q1 spread <= 2)
 constexpr int kVStages = 4;
 
-template <int P>
+// VH (v2-sharded fields, dist.VShardedSolver): src holds C2 source v2 cells,
+// the shard's own cells at [v2off, v2off + C2out) with halo cells of the
+// neighbouring ranks before and after them (contiguous rows: v2 is the
+// outermost axis), and dst holds the C2out output cells.  The stream is not
+// periodic: source cells k = 0 .. C2-1, the pair (k-1, k) produces output
+// cell k - v2off + q2(x), stored when inside [0, C2out).  A lane whose
+// shift would need a source cell outside the halos raises vh_flag (the
+// host's halo width bounds |E tau / h_v|; the solver raises on the flag).
+template <int P, bool VH = false>
 __global__ void __launch_bounds__(32 * kVCells)
     dg_vplane_tma_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t nx,
                          int C1, int C2, const double* __restrict__ a1,
@@ -697,7 +705,8 @@ __global__ void __launch_bounds__(32 * kVCells)
                          const double* __restrict__ al1, const double* __restrict__ a2,
                          const double* __restrict__ b2, const int64_t* __restrict__ q2,
                          const double* __restrict__ al2, int32_t* __restrict__ flag1,
-                         int32_t* __restrict__ flag2, const __grid_constant__ CUtensorMap tmap) {
+                         int32_t* __restrict__ flag2, const __grid_constant__ CUtensorMap tmap,
+                         int v2off = 0, int C2out = 0, int32_t* __restrict__ vh_flag = nullptr) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int W = kVCells + kVSpan;       // window cells
   constexpr int WP = W * P;                 // window v1 dofs
@@ -716,7 +725,11 @@ __global__ void __launch_bounds__(32 * kVCells)
   const bool active = c1 < C1;
 
   const int qm1 = (int)wrap_mod(q1[x], C1);
-  const int qm2 = (int)wrap_mod(q2[x], C2);
+  const int qm2 = VH ? (int)q2[x] : (int)wrap_mod(q2[x], C2);
+  // VH: the lane's outputs 0 .. C2out-1 need source cells v2off - q2 - 1 ..
+  // v2off - q2 + C2out - 1 of the stream
+  const bool vh_bad = VH && (v2off - qm2 - 1 < 0 || v2off - qm2 + C2out - 1 > C2 - 1);
+  const int klast = VH ? C2 - 1 : C2;  // last source step (periodic: C2 wraps to cell 0)
   // block-wide window of source v1 cells (q1 in [qmin, qmax], taken mod C1
   // relative to the warp-0 lane-0 value so the spread is the true spread)
   if (threadIdx.x == 0) {
@@ -774,8 +787,8 @@ __global__ void __launch_bounds__(32 * kVCells)
   const double* up_base = src + (int64_t)up1 * P * nx + x;
   bool bad1 = false, bad2 = false;
 
-  auto issue = [&](int k) {  // source v2 cell k (0..C2) into slot k % kVStages
-    const int s = k == C2 ? 0 : k;
+  auto issue = [&](int k) {  // source v2 cell k (0..klast) into slot k % kVStages
+    const int s = (!VH && k == C2) ? 0 : k;
     const int sl = k % kVStages;
     double* dstp = ring + sl * stage;
     mbar_arrive_expect_tx(bars + sl, (uint32_t)(wcells * P * P * 32) * 8u);
@@ -792,7 +805,7 @@ __global__ void __launch_bounds__(32 * kVCells)
   }
   __syncthreads();
   if (use_tma && threadIdx.x == 0)
-    for (int k = 0; k < kVStages && k <= C2; ++k) issue(k);
+    for (int k = 0; k < kVStages && k <= klast; ++k) issue(k);
 
   // GEN: per-lane alpha == 0 exact-shift branches; otherwise the common
   // all-lanes-interpolate body without them.
@@ -810,7 +823,7 @@ __global__ void __launch_bounds__(32 * kVCells)
           ul[m2][m] = t[((wlo * P + m2) * P + m) * 32];
         }
     } else {
-      const int s = k == C2 ? 0 : k;
+      const int s = (!VH && k == C2) ? 0 : k;
 #pragma unroll
       for (int m2 = 0; m2 < P; ++m2) {
         const int64_t r = ((int64_t)s * P + m2) * row_stride;
@@ -842,7 +855,7 @@ __global__ void __launch_bounds__(32 * kVCells)
   };
   auto release = [&](int k) {  // every thread is done with slot k % kVStages
     __syncthreads();
-    if (use_tma && threadIdx.x == 0 && k + kVStages <= C2) issue(k + kVStages);
+    if (use_tma && threadIdx.x == 0 && k + kVStages <= klast) issue(k + kVStages);
   };
 
   // Non-finite values: only the outputs are tested in the common path; an
@@ -853,7 +866,9 @@ __global__ void __launch_bounds__(32 * kVCells)
     constexpr bool GEN = decltype(genc)::value;
     double g[P][P];
     v1_cell(k, g, genc);
-    double* out = dst + ((int64_t)c2 * P) * row_stride + (int64_t)c1 * P * nx + x;
+    // VH: pairs outside the shard's output cells only advance the chain
+    const bool store = !VH || (c2 >= 0 && c2 < C2out);
+    double* out = dst + ((int64_t)(store ? c2 : 0) * P) * row_stride + (int64_t)c1 * P * nx + x;
     ExpMax eo;
 #pragma unroll
     for (int j2 = 0; j2 < P; ++j2)
@@ -871,8 +886,10 @@ __global__ void __launch_bounds__(32 * kVCells)
           for (int m = 1; m < P; ++m) acc_b = step_madd(acc_b, B2[j2][m], g[m][j]);
           o = dadd(acc_a, acc_b);
         }
-        eo.add(o);
-        __stcs(out + j2 * row_stride + j * nx, o);
+        if (store) {
+          eo.add(o);
+          __stcs(out + j2 * row_stride + j * nx, o);
+        }
       }
     if (eo.bad()) {
       bad2 = true;
@@ -901,12 +918,13 @@ __global__ void __launch_bounds__(32 * kVCells)
       v1_cell(0, gp, std::false_type{});
   }
   release(0);
-  int c2 = qm2;  // output cell of source cell s: s + q2 (mod C2); s = 1 first
-  for (int k = 1; k <= C2; ++k) {
+  // output cell of source cell s: s + q2 (mod C2), s = 1 first; VH: s - v2off + q2
+  int c2 = VH ? qm2 - v2off : qm2;
+  for (int k = 1; k <= klast; ++k) {
     const int sl = k % kVStages;
     if (sl == 0) phase ^= 1u;
     if (use_tma) mbar_wait(bars + sl, phase);
-    if (++c2 == C2) c2 = 0;
+    if (++c2 == C2 && !VH) c2 = 0;
     if (active) {
       if (gen)
         step(k, gp, c2, std::true_type{});
@@ -917,6 +935,7 @@ __global__ void __launch_bounds__(32 * kVCells)
   }
   report_flag(bad1, flag1);
   report_flag(bad2, flag2);
+  if (VH) report_flag(active && vh_bad, vh_flag);
 }
 
 template <int P>
@@ -955,9 +974,71 @@ static int launch_vplane(const double* src, double* dst, const int64_t dims[4], 
   return launched("dg_vplane_kernel");
 }
 
+// v2-sharded shard: src = [v2 halo | shard cells | v2 halo] (C2src cells),
+// dst = the shard's C2out cells.  TMA ring only (the halo stream has no
+// direct-load kernel); needs nx % 32 == 0 and at least kVCells + kVSpan v1 cells.
+template <int P>
+static int launch_vplane_vh(const double* src, double* dst, const int64_t dims[4], int C2src,
+                            int v2off, const double* a1, const double* b1, const int64_t* q1,
+                            const double* al1, const double* a2, const double* b2,
+                            const int64_t* q2, const double* al2, int32_t* f1, int32_t* f2,
+                            int32_t* vh_flag, cudaStream_t st) {
+  const int64_t nx = dims[0] * dims[1];
+  const int C1 = (int)(dims[2] / P);
+  const int C2out = (int)(dims[3] / P);
+  if (nx == 0 || C1 == 0 || C2out == 0) return VPB_OK;
+  VPB_REQUIRE(nx % 32 == 0 && C1 >= kVCells + kVSpan,
+              "v2-halo v pass needs nx %% 32 == 0 and >= %d v1 cells", kVCells + kVSpan);
+  VPB_REQUIRE((reinterpret_cast<uintptr_t>(src) & 15) == 0, "field buffers must be 16-byte aligned");
+  const uint64_t nv1 = (uint64_t)C1 * P, nv2 = (uint64_t)C2src * P;
+  CUtensorMap tmap;
+  if (!encode_tmap_3d(&tmap, src, (uint64_t)nx, nv1, nv2, (uint64_t)nx * 8,
+                      (uint64_t)nx * nv1 * 8, 32, P, P)) {
+    set_error("cannot encode the v-plane tensor map");
+    return VPB_ERR_UNSUPPORTED;
+  }
+  const size_t smem = (size_t)kVStages * P * (kVCells + kVSpan) * P * 32 * 8 + kVStages * 8;
+  VPB_REQUIRE(smem <= 200 * 1024, "v-plane ring does not fit shared memory");
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(dg_vplane_tma_kernel<P, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  dim3 grid((unsigned)((C1 + kVCells - 1) / kVCells), (unsigned)((nx + 31) / 32));
+  dg_vplane_tma_kernel<P, true><<<grid, 32 * kVCells, smem, st>>>(
+      src, dst, nx, C1, C2src, a1, b1, q1, al1, a2, b2, q2, al2, f1, f2, tmap, v2off, C2out,
+      vh_flag);
+  return launched("dg_vplane_tma_kernel");
+}
+
 }  // namespace vpb
 
 using namespace vpb;
+
+// Fused v1 v2 pass of one v2 shard (dist.VShardedSolver): `src` holds
+// src_v2_cells source v2 cells (the shard's dims[3] / order cells start at
+// cell v2_offset, halo cells of the neighbouring shards before and after),
+// `dst` the shard's own cells; the v2 tables index the shard's x columns as
+// usual.  halo_flag is raised when a shift needs a cell beyond the halos.
+extern "C" int vpb_dg_sweep_vplane_v2halo(const double* src, double* dst, const int64_t dims[4],
+                                          int32_t order, int32_t src_v2_cells, int32_t v2_offset,
+                                          const double* a1, const double* b1, const int64_t* q1,
+                                          const double* alpha1, const double* a2, const double* b2,
+                                          const int64_t* q2, const double* alpha2, int32_t* flag1,
+                                          int32_t* flag2, int32_t* halo_flag, void* stream) {
+  VPB_REQUIRE(src != dst, "src and dst must be distinct buffers");
+  VPB_REQUIRE(order >= 1 && order <= kMaxOrder, "order %d outside 1..9", order);
+  VPB_REQUIRE(dims[2] % order == 0 && dims[3] % order == 0, "v axes not whole cells");
+  VPB_REQUIRE(v2_offset >= 0 && v2_offset + dims[3] / order <= src_v2_cells,
+              "shard cells outside the source stream");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = VPB_OK;
+  VPB_XPLANE_SWITCH(order, rc = launch_vplane_vh<PP>(src, dst, dims, src_v2_cells, v2_offset, a1,
+                                                     b1, q1, alpha1, a2, b2, q2, alpha2, flag1,
+                                                     flag2, halo_flag, st));
+  return rc;
+}
 
 extern "C" int vpb_dg_sweep_vplane(const double* src, double* dst, const int64_t dims[4],
                                    int32_t order, const double* a1, const double* b1,

@@ -334,6 +334,52 @@ class CudaOps:
                                                      self._device.stream()),
                 "vpb_dg_sweep_xstencil_rows")
 
+    # -- velocity-sharded field (VShardedSolver) ------------------------------------
+    def xpass_work(self, dims, order, qmul) -> int:
+        fn = (self.lib.vpb_dg_xplane_density_work_len if qmul == 1
+              else self.lib.vpb_dg_xcomp_density_work_len)
+        return int(fn(self._lib.dims(dims), order))
+
+    def xpass_rows(self, src, dst, dims, order, t1, t2, r0, qmul, f1, f2, dens=None):
+        """x half step (qmul 1: vpb_dg_sweep_xplane[_density]) or the merged
+        closing + opening pair (qmul 2: vpb_dg_sweep_xcomp_density) of a v2
+        slab whose first dof row is global row r0 (x2 tables offset by r0);
+        dens = (wv1, wv2 of the slab, mid, wc1, wc2, volume, work, rc, stats)."""
+        L = self._lib
+        st = self._device.stream()
+        nv2 = dims[3]
+        a2, b2, q2, al2 = (t2.a[r0:r0 + nv2], t2.b[r0:r0 + nv2], t2.q[r0:r0 + nv2],
+                           t2.alpha[r0:r0 + nv2])
+        tail = ()
+        if dens is not None:
+            wv1, wv2, mid, wc1, wc2, volume, work, rc, stats = dens
+            tail = (wv1.data_ptr(), wv2.data_ptr(), mid.ctypes.data, wc1.ctypes.data,
+                    wc2.ctypes.data, volume, work.data_ptr(), rc.data_ptr(), stats.data_ptr())
+        if qmul == 2:
+            k2 = t2.composed()[r0:r0 + nv2]
+            L.check(self.lib.vpb_dg_sweep_xcomp_density(
+                src.data_ptr(), dst.data_ptr(), L.dims(dims), order, t1.composed().data_ptr(),
+                t1.q.data_ptr(), t1.alpha.data_ptr(), k2.data_ptr(), q2.data_ptr(),
+                al2.data_ptr(), f1.data_ptr(), *tail, st), "vpb_dg_sweep_xcomp_density")
+            return
+        head = (src.data_ptr(), dst.data_ptr(), L.dims(dims), order, t1.a.data_ptr(),
+                t1.b.data_ptr(), t1.q.data_ptr(), t1.alpha.data_ptr(), a2.data_ptr(),
+                b2.data_ptr(), q2.data_ptr(), al2.data_ptr(), f1.data_ptr(), f2.data_ptr())
+        if dens is None:
+            L.check(self.lib.vpb_dg_sweep_xplane(*head, st), "vpb_dg_sweep_xplane")
+        else:
+            L.check(self.lib.vpb_dg_sweep_xplane_density(*head, *tail, st),
+                    "vpb_dg_sweep_xplane_density")
+
+    def vplane_v2halo(self, src_ext, dst, dims, order, c2e, off, t1, t2, f1, f2, hflag):
+        L = self._lib
+        L.check(self.lib.vpb_dg_sweep_vplane_v2halo(
+            src_ext.data_ptr(), dst.data_ptr(), L.dims(dims), order, int(c2e), int(off),
+            t1.a.data_ptr(), t1.b.data_ptr(), t1.q.data_ptr(), t1.alpha.data_ptr(),
+            t2.a.data_ptr(), t2.b.data_ptr(), t2.q.data_ptr(), t2.alpha.data_ptr(),
+            f1.data_ptr(), f2.data_ptr(), hflag.data_ptr(), self._device.stream()),
+            "vpb_dg_sweep_vplane_v2halo")
+
     def pack(self, axis, f, dims, order, cell0, width, buf):
         L = self._lib
         L.check(self.lib.vpb_halo_pack(axis, f.data_ptr(), L.dims(dims), order, cell0, width,
@@ -1160,6 +1206,303 @@ class SplineShardedSolver:
                                self.v2sq[v0:v1].contiguous(), out, work)
             sums[r] = out
         tot = self.comm.allreduce(sums, "sum").cpu().numpy()
+        ee_t = torch.zeros(1, dtype=torch.float64, device=self.device)
+        self.ops.electric_energy(self.e, self.n1 * self.n2, self.wx_full, ee_t)
+        ee = float(ee_t.cpu()[0])
+        mass, l1, l2sq, kin = (float(x) for x in tot[:4])
+        return {"time": float(time), "electric_energy": ee, "mass": mass, "l1_norm": l1,
+                "l2_norm": math.sqrt(max(l2sq, 0.0)), "kinetic_energy": kin,
+                "total_energy": kin + ee}
+
+
+# ---------------------------------------------------------------------------
+# Velocity-sharded dG solver (the paper's decomposition)
+# ---------------------------------------------------------------------------
+KIND_VL, KIND_VR = 3, 4  # v2 halo messages: receiver's left / right halo
+
+
+class VShardedSolver:
+    """Strang steps of a 2x2v dG field split along v2 over W ranks.
+
+    The paper parallelises over velocity; SURVEY §8f.3
+    asks for that alternative to the x sharding of :class:`ShardedSolver`.
+    Rank r owns the v2 cells V_r = [c0, c1) as a contiguous slab of the
+    canonical buffer, stored between H halo cells of each neighbour
+    (v2 is the outermost axis, so every halo is one contiguous block of
+    rows and travels zero-copy: NCCL sends straight from the field).
+
+    * x half steps (and the merged closing + opening pair, "fast"
+      arithmetic) are LOCAL: whole (x1, x2) planes, the single-GPU kernels
+      on the slab with the x2 tables offset to the slab's rows; their
+      density epilogue gives the slab's partial cell-centre density.
+    * density: the partials are all-gathered and summed in rank order on
+      every rank (deterministic), every rank solves the Poisson problem.
+    * v pass: one halo exchange of H v2 cells per side, then the fused
+      v1 v2 kernel streams [halo | slab | halo] non-periodically
+      (``vpb_dg_sweep_vplane_v2halo``).  H bounds the E shift:
+      |E2 tau / h_v2| < H - 1; the kernel raises a flag beyond that and the
+      solver raises ``RuntimeError``.
+
+    Per step and rank: 2 x H x P rows of n1 n2 nv1 doubles of halo (vs the x
+    sharding's x1 halos of the doubled reach on every plane) and a
+    C1 C2-double allgather.
+    """
+
+    def __init__(self, grid: GridSpec, comm, ranks, world: int, ops=None, device=None,
+                 halo_cells: int = 2):
+        if grid.method != DG or grid.ndim != 4:
+            raise NotImplementedError("the velocity-sharded step covers the 2x2v SLDG path")
+        p = grid.order
+        n1, n2, nv1, nv2 = grid.dims4
+        C2v = nv2 // p
+        self.H = int(halo_cells)
+        self.cr = [split_cells(C2v, world, r) for r in range(world)]
+        if min(c1 - c0 for c0, c1 in self.cr) < self.H:
+            raise ValueError(f"{C2v} v2 cells over {world} ranks leave a shard narrower than "
+                             f"the {self.H}-cell halo")
+        self.grid = grid
+        self.comm = comm
+        self.world = world
+        self.ops = ops or CudaOps()
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.order = p
+        self.n1, self.n2, self.nv1, self.nv2 = n1, n2, nv1, nv2
+        self.row = n1 * n2 * nv1  # doubles per v2 dof row
+        self.ranks = list(ranks)
+        dev = self.device
+        self.f, self.buf, self.flags = {}, {}, {}
+        for r in self.ranks:
+            c0, c1 = self.cr[r]
+            n = (c1 - c0 + 2 * self.H) * p * self.row
+            self.f[r] = torch.empty(n, dtype=torch.float64, device=dev)
+            self.buf[r] = torch.empty(n, dtype=torch.float64, device=dev)
+        w = [torch.as_tensor(grid.axis_weights(a), dtype=torch.float64).to(dev) for a in range(4)]
+        self.wv1, self.wv2 = w[2], w[3]
+        self.wx_full = (w[1][:, None] * w[0][None, :]).reshape(-1).contiguous()
+        self.vpoints = [torch.as_tensor(grid.axis_points(a), dtype=torch.float64).to(dev)
+                        for a in (2, 3)]
+        self.v1sq = self.vpoints[0] ** 2
+        self.v2sq = self.vpoints[1] ** 2
+        self.rho = torch.empty(n1 * n2, dtype=torch.float64, device=dev)
+        self.e = torch.empty(2 * n1 * n2, dtype=torch.float64, device=dev)
+        self.solve_flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.names = ["x1 half (open)", "x2 half (open)", "field solve", "v1 full", "v2 full",
+                      "x1 half (close)", "x2 half (close)"]
+        self._xtab = {}
+        self._dens = None
+        self._halo_bytes = 0
+
+    # -- geometry ----------------------------------------------------------------
+    def dims(self, r: int):
+        c0, c1 = self.cr[r]
+        return (self.n1, self.n2, self.nv1, (c1 - c0) * self.order)
+
+    def local(self, t: torch.Tensor, r: int) -> torch.Tensor:
+        """The shard's own rows of an extended buffer."""
+        c0, c1 = self.cr[r]
+        a = self.H * self.order * self.row
+        return t[a:a + (c1 - c0) * self.order * self.row]
+
+    # -- data movement helpers (tests / I/O) -------------------------------------
+    def initialize(self, problem) -> None:
+        from . import _device, _lib
+        from .driver import separable_factors
+
+        g1, g2, space = separable_factors(problem, self.grid)
+        lib = _lib.load()
+        dg1 = torch.as_tensor(np.asarray(g1), dtype=torch.float64).to(self.device)
+        sp = torch.as_tensor(np.asarray(space).reshape(-1), dtype=torch.float64).to(self.device)
+        p = self.order
+        for r in self.ranks:
+            c0, c1 = self.cr[r]
+            dg2 = torch.as_tensor(np.asarray(g2)[c0 * p:c1 * p], dtype=torch.float64).to(self.device)
+            _lib.check(lib.vpb_fill_separable(self.local(self.f[r], r).data_ptr(),
+                                              _lib.dims(self.dims(r)), dg1.data_ptr(),
+                                              dg2.data_ptr(), sp.data_ptr(), _device.stream()),
+                       "vpb_fill_separable")
+
+    def scatter(self, logical: np.ndarray) -> None:
+        p = self.order
+        for r in self.ranks:
+            c0, c1 = self.cr[r]
+            box = np.ascontiguousarray(logical[:, :, :, c0 * p:c1 * p].transpose(3, 2, 1, 0))
+            self.local(self.f[r], r).copy_(torch.from_numpy(box.reshape(-1)).to(self.device))
+
+    def local_logical(self, r: int) -> np.ndarray:
+        d = self.dims(r)
+        return (self.local(self.f[r], r).view(d[3], d[2], d[1], d[0]).permute(3, 2, 1, 0)
+                .cpu().numpy())
+
+    def gather(self) -> np.ndarray:
+        out = np.empty(self.grid.dofs)
+        p = self.order
+        for r in self.ranks:
+            c0, c1 = self.cr[r]
+            out[:, :, :, c0 * p:c1 * p] = self.local_logical(r)
+        return out
+
+    # -- pieces of the step --------------------------------------------------------
+    def x_tables(self, tau: float):
+        key = float(tau)
+        if key not in self._xtab:
+            g = self.grid
+            self._xtab = {key: [self.ops.tables(self.vpoints[d], 0.5 * tau, g.axes[d].h,
+                                                g.dg_degree) for d in range(2)]}
+        return self._xtab[key]
+
+    def _density_consts(self):
+        if self._dens is None:
+            from .grid import gauss_nodes
+            from .poisson import _lagrange_row
+
+            p = self.order
+            nodes, _ = gauss_nodes(p)
+            mid = np.ascontiguousarray(_lagrange_row(nodes, 0.5))
+            cells = [np.ascontiguousarray(np.asarray(self.grid.axis_weights(a))[:p])
+                     for a in (0, 1)]
+            ax = self.grid.axes
+            volume = (ax[0].upper - ax[0].lower) * (ax[1].upper - ax[1].lower)
+            self._dens = (mid, cells[0], cells[1], float(volume))
+        return self._dens
+
+    def _x_pass(self, tau, qmul, fl, stats_row, rc_parts, mark):
+        """One local x pass on every shard (qmul 1: a half step; 2: the merged
+        pair); with rc_parts the density epilogue fills the partials."""
+        t1, t2 = self.x_tables(tau)
+        p = self.order
+        mid, wc1, wc2, volume = self._density_consts()
+        mark(("sweep_x12x12" if qmul == 2 else "sweep_x12") + ("_rho" if rc_parts is not None
+                                                               else ""))
+        for r in self.ranks:
+            c0, _ = self.cr[r]
+            d = self.dims(r)
+            dens = None
+            if rc_parts is not None:
+                work = torch.empty(self.ops.xpass_work(d, p, qmul), dtype=torch.float64,
+                                   device=self.device)
+                rc = torch.empty((self.n1 // p) * (self.n2 // p), dtype=torch.float64,
+                                 device=self.device)
+                wv2 = self.wv2[c0 * p:c0 * p + d[3]].contiguous()
+                dens = (self.wv1, wv2, mid, wc1, wc2, volume, work, rc, stats_row[r])
+                rc_parts[r] = rc
+            f1, f2 = fl[r]
+            self.ops.xpass_rows(self.local(self.f[r], r), self.local(self.buf[r], r), d, p, t1,
+                                t2, c0 * p, qmul, f1, f2, dens)
+            self.f[r], self.buf[r] = self.buf[r], self.f[r]
+
+    def _sum_parts(self, parts: dict) -> torch.Tensor:
+        """Rank-order sum of per-rank partials, identical on every rank."""
+        full = self.comm.allgather(parts)
+        out = full[0].clone()
+        for t in full[1:]:
+            out += t
+        return out
+
+    def _exchange_halos(self, mark) -> None:
+        mark("halo_v2")
+        H, p = self.H, self.order
+        hrows = H * p * self.row
+        msgs = {}
+        for r in self.ranks:
+            c0, c1 = self.cr[r]
+            nl = (c1 - c0) * p * self.row
+            f = self.f[r]
+            left, right = (r - 1) % self.world, (r + 1) % self.world
+            first = f[hrows:2 * hrows]              # my first H cells -> left's right halo
+            last = f[nl:nl + hrows]                 # my last H cells -> right's left halo
+            msgs[r] = [(KIND_VR, left, first, right, f[hrows + nl:2 * hrows + nl]),
+                       (KIND_VL, right, last, left, f[0:hrows])]
+        self.comm.exchange(msgs)
+        self._halo_bytes += 8 * 2 * hrows * len(self.ranks)
+
+    def _v_pass(self, tau, fl, hflag, mark) -> None:
+        g = self.grid
+        mark("tables_v12")
+        nx = self.n1 * self.n2
+        tv = [self.ops.tables(self.e[d * nx:(d + 1) * nx], tau, g.axes[2 + d].h, g.dg_degree)
+              for d in range(2)]
+        self._exchange_halos(mark)
+        mark("sweep_v12")
+        p = self.order
+        for r in self.ranks:
+            c0, c1 = self.cr[r]
+            f1, f2 = fl[r]
+            self.ops.vplane_v2halo(self.f[r], self.local(self.buf[r], r), self.dims(r), p,
+                                   c1 - c0 + 2 * self.H, self.H, tv[0], tv[1], f1, f2, hflag)
+            self.f[r], self.buf[r] = self.buf[r], self.f[r]
+
+    def advance(self, tau: float, nsteps: int, first_step: int | None = None,
+                timer=None) -> None:
+        """``nsteps`` Strang steps (driver.py:245-265 each) with the merged x
+        passes of the "fast" arithmetic between them (driver.advance)."""
+        from .driver import SubstepError
+        from .poisson import _warn_if_not_neutral
+
+        if nsteps <= 0:
+            return
+        mark = timer or (lambda label: None)
+        dev = self.device
+        flags = {r: torch.zeros((nsteps, 8), dtype=torch.int32, device=dev) for r in self.ranks}
+        stats = {r: torch.zeros((nsteps, 4), dtype=torch.float64, device=dev)
+                 for r in self.ranks}
+        solve_flags = torch.zeros((nsteps, 1), dtype=torch.int32, device=dev)
+        hflag = torch.zeros(1, dtype=torch.int32, device=dev)
+
+        def fl(m, k):
+            return {r: (flags[r][m][k:k + 1], flags[r][m][k + 1:k + 2]) for r in self.ranks}
+
+        rc_parts = {}
+        self._x_pass(tau, 1, fl(0, 0), {r: stats[r][0] for r in self.ranks}, rc_parts, mark)
+        for m in range(nsteps):
+            mark("rho_allgather")
+            rc = self._sum_parts(rc_parts)
+            mark("field_solve")
+            self.ops.field_solve_centred(self.grid, rc, self.e, solve_flags[m])
+            self._v_pass(tau, fl(m, 3), hflag, mark)
+            if m + 1 < nsteps:  # closing of step m + opening of step m+1, one pass
+                rc_parts = {}
+                self._x_pass(tau, 2, fl(m, 5), {r: stats[r][m + 1] for r in self.ranks},
+                             rc_parts, mark)
+            else:
+                self._x_pass(tau, 1, fl(m, 5), None, None, mark)
+        mark("flags")
+        for r in self.ranks:
+            flags[r][:, 2:3] = torch.maximum(flags[r][:, 2:3], solve_flags)
+        fh = self.comm.allreduce(flags, "max").cpu().numpy()
+        sh = self._sum_parts(stats).cpu().numpy()
+        hmax = self.comm.allreduce({r: hflag for r in self.ranks}, "max").cpu().numpy()
+        mark(None)
+        if hmax.any():
+            raise RuntimeError(f"an E shift exceeded the {self.H}-cell v2 halo; "
+                               "construct VShardedSolver with a wider halo_cells")
+        for m in range(nsteps):
+            _warn_if_not_neutral(float(sh[m, 0]))
+            for k, name in enumerate(self.names):
+                if fh[m, k]:
+                    raise SubstepError(name, None if first_step is None
+                                       else (first_step + m) * tau)
+
+    def diagnostics(self, time: float = 0.0) -> dict:
+        """Global conserved quantities (driver.py:279-316)."""
+        p = self.order
+        parts, sums = {}, {}
+        for r in self.ranks:
+            c0, _ = self.cr[r]
+            d = self.dims(r)
+            wv2 = self.wv2[c0 * p:c0 * p + d[3]].contiguous()
+            v2sq = self.v2sq[c0 * p:c0 * p + d[3]].contiguous()
+            rl = torch.empty(self.n1 * self.n2, dtype=torch.float64, device=self.device)
+            work = torch.empty(self.ops.density_work(d), dtype=torch.float64, device=self.device)
+            f = self.local(self.f[r], r)
+            self.ops.density(f, d, self.wv1, wv2, rl, work)
+            parts[r] = rl
+            out = torch.zeros(8, dtype=torch.float64, device=self.device)
+            dwork = torch.empty(self.ops.diag_work(d), dtype=torch.float64, device=self.device)
+            self.ops.diag_sums(f, d, self.wx_full, self.wv1, wv2, self.v1sq, v2sq, out, dwork)
+            sums[r] = out
+        self.rho.copy_(self._sum_parts(parts))
+        self.ops.field_solve(self.grid, self.rho, self.e, None, self.solve_flag)
+        tot = self._sum_parts(sums).cpu().numpy()
         ee_t = torch.zeros(1, dtype=torch.float64, device=self.device)
         self.ops.electric_energy(self.e, self.n1 * self.n2, self.wx_full, ee_t)
         ee = float(ee_t.cpu()[0])

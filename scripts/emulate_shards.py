@@ -11,14 +11,10 @@ measurement.
     python scripts/emulate_shards.py --config cfg2 --worlds 1 2 4 8 --steps 5
     python scripts/emulate_shards.py --config cfg5 --worlds 2 4 8 --vshard
 
---vshard evaluates VELOCITY-direction sharding (the paper's own choice,
-PAPER.md:609-613): rank r holds the v2 slab f[V_r][v1][x2][x1],
-so every x pass (x1, x2 and the merged composed pass) is local and runs on
-whole (x1, x2) planes, and only the v2 sweep of the v pass needs halo cells
-(E-shifts of at most one v2 cell here: one cell on each side).  One rank's
-compute is emulated as advance() on the slab grid (nv2 / W + 2 halo cells
-of v2, periodic instead of halo-fed v2: the same kernels and bytes); the
-density becomes a partial sum per rank plus an allreduce of n1 n2 doubles.
+--vshard runs VShardedSolver (velocity-direction sharding, the paper's own
+choice) the same way: every shard's x passes
+(local, whole (x1, x2) planes), v2 halo copies and halo-fed v pass back to
+back on one GPU, total / W per rank.
 """
 
 from __future__ import annotations
@@ -55,26 +51,27 @@ def main() -> None:
     N = grid.total_dof
     for w in args.worlds:
         if args.vshard:
-            cells_v2 = grid.axes[3].count // w + 2  # the slab plus one halo cell per side
-            slab = vpb.make_grid(problem, "dg", (grid.dof(0), grid.dof(1), grid.dof(2),
-                                                 cells_v2 * order), dg_order=order)
-            f = vpb.initialize(problem, slab)
-            f = vpb.advance(f, tau, 2, consume=True)
+            solver = dist.VShardedSolver(grid, dist.VirtualComm(w), range(w), w)
+            solver.initialize(problem)
+            solver.advance(tau, 2)
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            solver._halo_bytes = 0
             e0.record()
-            f = vpb.advance(f, tau, args.steps, consume=True)
+            solver.advance(tau, args.steps)
             e1.record()
             torch.cuda.synchronize()
-            ms = e0.elapsed_time(e1) / args.steps
-            halo = 2 * order * grid.dof(0) * grid.dof(1) * grid.dof(2) * 8
+            per_rank = e0.elapsed_time(e1) / args.steps / w
             print(json.dumps({"config": args.config, "world": w, "layout": f"v2 x{w}",
-                              "per_rank_compute_ms_per_step": ms,
-                              "projected_dof_per_s_compute_only": N / (ms * 1e-3),
-                              "v2_cells_per_rank_incl_halo": cells_v2,
-                              "halo_bytes_per_rank_per_step": int(halo),
-                              "rho_allreduce_bytes": 8 * grid.dof(0) * grid.dof(1)}), flush=True)
-            del f
+                              "per_rank_compute_ms_per_step": per_rank,
+                              "projected_dof_per_s_compute_only": N / (per_rank * 1e-3),
+                              "v2_cells_per_rank": solver.cr[0][1] - solver.cr[0][0],
+                              "halo_cells_per_side": solver.H,
+                              "halo_bytes_per_rank_per_step": int(solver._halo_bytes
+                                                                  / args.steps / w),
+                              "rho_allgather_bytes": 8 * (grid.axes[0].count
+                                                          * grid.axes[1].count)}), flush=True)
+            del solver
             driver._state_cached.cache_clear()
             gc.collect()
             torch.cuda.empty_cache()

@@ -103,6 +103,47 @@ class NumpyOps:
         sl[axis] = slice(wl * order, wl * order + dims[axis])
         self._store(dst, dims, out[tuple(sl)], flag)
 
+    # -- velocity-sharded field (VShardedSolver) -------------------------------
+    def xpass_work(self, dims, order, qmul):
+        return 1
+
+    def xpass_rows(self, src, dst, dims, order, t1, t2, r0, qmul, f1, f2, dens=None):
+        """x half step (qmul 1) or the two consecutive half steps (qmul 2) of
+        a v2 slab (x2 table rows from r0), periodic x, sweep by sweep; density
+        partial of the result as the kernels' epilogue defines it."""
+        nv2 = dims[3]
+        t2s = _Tab(t2.a[r0:r0 + nv2], t2.b[r0:r0 + nv2], t2.q[r0:r0 + nv2],
+                   t2.alpha[r0:r0 + nv2])
+        arr = _box(src, dims)
+        for _ in range(qmul):
+            arr = self._sweep_lines(arr, 0, dims, order, t1)
+            arr = self._sweep_lines(arr, 1, dims, order, t2s)
+        self._store(dst, dims, arr, f1)
+        if dens is not None:
+            wv1, wv2, mid, wc1, wc2, volume, work, rc_out, stats = dens
+            p = order
+            n1, n2, nv1, _ = dims
+            o = arr.reshape(n1 // p, p, n2 // p, p, nv1, nv2)
+            wa, wb = wv1.numpy(), wv2.numpy()
+            rc = np.einsum("aibjvw,i,j,v,w->ba", o, mid, mid, wa, wb, optimize=False)
+            rc_out.copy_(torch.from_numpy(np.ascontiguousarray(rc).reshape(-1)))
+            mean = np.einsum("aibjvw,i,j,v,w->", o, wc1, wc2, wa, wb, optimize=False)
+            stats[0] = float(mean) / volume
+
+    def vplane_v2halo(self, src_ext, dst, dims, order, c2e, off, t1, t2, f1, f2, hflag):
+        """v1 then v2 sweep of [halo | slab | halo]: swept periodically over
+        the extended rows (whose wrap-around only reaches discarded cells when
+        the halos are wide enough), the slab's cells kept."""
+        n1, n2, nv1, nv2 = dims
+        ed = (n1, n2, nv1, c2e * order)
+        ext = _box(src_ext, ed)
+        q = np.asarray(t2.q)
+        if q.size and (off - q.max() - 1 < 0 or off - q.min() + nv2 // order - 1 > c2e - 1):
+            hflag.fill_(1)
+        ext = self._sweep_lines(ext, 2, ed, order, t1)
+        ext = self._sweep_lines(ext, 3, ed, order, t2)
+        self._store(dst, dims, ext[:, :, :, off * order:off * order + nv2], f2)
+
     # -- three-cell x-plane stencil passes (ShardedSolver.advance) ------------
     def stencil_tables(self, tab, single: bool):
         a, b = tab.a, tab.b
