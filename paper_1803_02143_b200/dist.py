@@ -1239,17 +1239,22 @@ class VShardedSolver:
       every rank (deterministic), every rank solves the Poisson problem.
     * v pass: one halo exchange of H v2 cells per side, then the fused
       v1 v2 kernel streams [halo | slab | halo] non-periodically
-      (``vpb_dg_sweep_vplane_v2halo``).  H bounds the E shift:
-      |E2 tau / h_v2| < H - 1; the kernel raises a flag beyond that and the
-      solver raises ``RuntimeError``.
+      (``vpb_dg_sweep_vplane_v2halo``).  H bounds the E shift: the v2 cell
+      offset q2 = floor(E2 tau / h_v2) must lie in [-H, H-1] (H = 1: a
+      shift of less than one cell either way, true for the BASELINE
+      configurations); the kernel raises a flag beyond that and the solver
+      raises ``RuntimeError``.
+    * overlap: the x pass that precedes a v pass runs its two H-cell
+      boundary blocks of v2 rows first, posts the halo exchange of their
+      output, and runs the interior rows while it is in flight.
 
     Per step and rank: 2 x H x P rows of n1 n2 nv1 doubles of halo (vs the x
     sharding's x1 halos of the doubled reach on every plane) and a
-    C1 C2-double allgather.
+    C1 C2-double allgather of the density partials.
     """
 
     def __init__(self, grid: GridSpec, comm, ranks, world: int, ops=None, device=None,
-                 halo_cells: int = 2):
+                 halo_cells: int = 1):
         if grid.method != DG or grid.ndim != 4:
             raise NotImplementedError("the velocity-sharded step covers the 2x2v SLDG path")
         p = grid.order
@@ -1367,28 +1372,72 @@ class VShardedSolver:
 
     def _x_pass(self, tau, qmul, fl, stats_row, rc_parts, mark):
         """One local x pass on every shard (qmul 1: a half step; 2: the merged
-        pair); with rc_parts the density epilogue fills the partials."""
+        pair); with rc_parts the density epilogue fills the partials and the
+        pass feeds a v pass: its H-cell boundary blocks of v2 rows run first,
+        the v2 halo exchange of their output is posted, and the interior rows
+        run while it is in flight (comm/compute overlap).
+        Returns the pending exchange requests (wait before the v pass)."""
         t1, t2 = self.x_tables(tau)
-        p = self.order
+        p, H = self.order, self.H
         mid, wc1, wc2, volume = self._density_consts()
         mark(("sweep_x12x12" if qmul == 2 else "sweep_x12") + ("_rho" if rc_parts is not None
                                                                else ""))
-        for r in self.ranks:
+        feeds_v = rc_parts is not None
+
+        def run(r, a, b, with_dens, parts):
+            """x pass on the shard's v2 cells [a, b) (local numbering)."""
             c0, _ = self.cr[r]
-            d = self.dims(r)
+            d = (self.n1, self.n2, self.nv1, (b - a) * p)
+            off = a * p * self.row
+            src = self.local(self.f[r], r)[off:off + d[3] * self.row]
+            dst = self.local(self.buf[r], r)[off:off + d[3] * self.row]
             dens = None
-            if rc_parts is not None:
+            if with_dens:
                 work = torch.empty(self.ops.xpass_work(d, p, qmul), dtype=torch.float64,
                                    device=self.device)
                 rc = torch.empty((self.n1 // p) * (self.n2 // p), dtype=torch.float64,
                                  device=self.device)
-                wv2 = self.wv2[c0 * p:c0 * p + d[3]].contiguous()
-                dens = (self.wv1, wv2, mid, wc1, wc2, volume, work, rc, stats_row[r])
-                rc_parts[r] = rc
+                st = torch.zeros(4, dtype=torch.float64, device=self.device)
+                wv2 = self.wv2[(c0 + a) * p:(c0 + b) * p].contiguous()
+                dens = (self.wv1, wv2, mid, wc1, wc2, volume, work, rc, st)
+                parts.append((rc, st))
             f1, f2 = fl[r]
-            self.ops.xpass_rows(self.local(self.f[r], r), self.local(self.buf[r], r), d, p, t1,
-                                t2, c0 * p, qmul, f1, f2, dens)
+            self.ops.xpass_rows(src, dst, d, p, t1, t2, (c0 + a) * p, qmul, f1, f2, dens)
+
+        parts = {r: [] for r in self.ranks}
+        # split every shard (decided on the global decomposition, so every
+        # rank sums its density blocks in the same pattern) when all have an
+        # interior beyond the two boundary blocks
+        split = feeds_v and all(c1 - c0 >= 2 * H + 1 for c0, c1 in self.cr)
+        blocks = {}
+        for r in self.ranks:
+            c0, c1 = self.cr[r]
+            nl = c1 - c0
+            blocks[r] = [(0, H), (nl - H, nl), (H, nl - H)] if split else [(0, nl)]
+        for r in self.ranks:
+            for a, b in (blocks[r][:2] if split else blocks[r]):
+                run(r, a, b, feeds_v, parts[r])
+        reqs = []
+        if feeds_v:
+            # the boundary cells of the new state are in buf: send them now
+            # (NCCL runs on its own stream; the pass's timer label spans it)
+            reqs = self._post_halos(self.buf)
+        if split:
+            for r in self.ranks:
+                a, b = blocks[r][2]
+                run(r, a, b, True, parts[r])
+        if feeds_v:
+            for r in self.ranks:  # fixed order: left block, right block, interior
+                rc = parts[r][0][0].clone()
+                mean = parts[r][0][1][0].clone()
+                for rc_k, st_k in parts[r][1:]:
+                    rc += rc_k
+                    mean += st_k[0]
+                rc_parts[r] = rc
+                stats_row[r][0] = mean
+        for r in self.ranks:
             self.f[r], self.buf[r] = self.buf[r], self.f[r]
+        return reqs
 
     def _sum_parts(self, parts: dict) -> torch.Tensor:
         """Rank-order sum of per-rank partials, identical on every rank."""
@@ -1398,30 +1447,38 @@ class VShardedSolver:
             out += t
         return out
 
-    def _exchange_halos(self, mark) -> None:
-        mark("halo_v2")
+    def _post_halos(self, bufs: dict) -> list:
+        """Post the v2 halo exchange of the extended buffers ``bufs``: my
+        first H cells go to the left neighbour's right halo, my last H cells
+        to the right neighbour's left halo; contiguous rows, sent and
+        received in place (no packing)."""
         H, p = self.H, self.order
         hrows = H * p * self.row
         msgs = {}
         for r in self.ranks:
             c0, c1 = self.cr[r]
             nl = (c1 - c0) * p * self.row
-            f = self.f[r]
+            f = bufs[r]
             left, right = (r - 1) % self.world, (r + 1) % self.world
             first = f[hrows:2 * hrows]              # my first H cells -> left's right halo
             last = f[nl:nl + hrows]                 # my last H cells -> right's left halo
             msgs[r] = [(KIND_VR, left, first, right, f[hrows + nl:2 * hrows + nl]),
                        (KIND_VL, right, last, left, f[0:hrows])]
-        self.comm.exchange(msgs)
         self._halo_bytes += 8 * 2 * hrows * len(self.ranks)
+        return self.comm.exchange_async(msgs)
 
-    def _v_pass(self, tau, fl, hflag, mark) -> None:
+    def _v_pass(self, tau, fl, hflag, mark, reqs=None) -> None:
+        """Fused v pass of every shard; ``reqs``: the pending halo exchange of
+        the preceding x pass (None: exchange here)."""
         g = self.grid
         mark("tables_v12")
         nx = self.n1 * self.n2
         tv = [self.ops.tables(self.e[d * nx:(d + 1) * nx], tau, g.axes[2 + d].h, g.dg_degree)
               for d in range(2)]
-        self._exchange_halos(mark)
+        if reqs is None:
+            mark("halo_v2")
+            reqs = self._post_halos(self.f)
+        self.comm.wait(reqs)
         mark("sweep_v12")
         p = self.order
         for r in self.ranks:
@@ -1452,17 +1509,18 @@ class VShardedSolver:
             return {r: (flags[r][m][k:k + 1], flags[r][m][k + 1:k + 2]) for r in self.ranks}
 
         rc_parts = {}
-        self._x_pass(tau, 1, fl(0, 0), {r: stats[r][0] for r in self.ranks}, rc_parts, mark)
+        reqs = self._x_pass(tau, 1, fl(0, 0), {r: stats[r][0] for r in self.ranks}, rc_parts,
+                            mark)
         for m in range(nsteps):
             mark("rho_allgather")
             rc = self._sum_parts(rc_parts)
             mark("field_solve")
             self.ops.field_solve_centred(self.grid, rc, self.e, solve_flags[m])
-            self._v_pass(tau, fl(m, 3), hflag, mark)
+            self._v_pass(tau, fl(m, 3), hflag, mark, reqs)
             if m + 1 < nsteps:  # closing of step m + opening of step m+1, one pass
                 rc_parts = {}
-                self._x_pass(tau, 2, fl(m, 5), {r: stats[r][m + 1] for r in self.ranks},
-                             rc_parts, mark)
+                reqs = self._x_pass(tau, 2, fl(m, 5), {r: stats[r][m + 1] for r in self.ranks},
+                                    rc_parts, mark)
             else:
                 self._x_pass(tau, 1, fl(m, 5), None, None, mark)
         mark("flags")
