@@ -216,3 +216,44 @@ def test_fullsize_advance_vs_reference(slvp, tag, prob, method, dofs, order, tau
         assert abs(rr.mass - rec0.mass) <= MASS_TOL * rec0.mass, (tag, m)
         del g
         torch.cuda.empty_cache()
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(not __import__("os").environ.get("VPB_TEST_CFG5"),
+                    reason="config 5 (6.9e9 dofs, ~2 min of reference time on 16 cores and "
+                           "~120 GB of host RAM): opt in with VPB_TEST_CFG5=1")
+def test_fullsize_config5_one_step_vs_reference(slvp):
+    """BASELINE config 5 (288^4, degree 2, dt=0.05): one step of the headline
+    advance() against the reference's strang_step on the host, compared in
+    v2 chunks on the host (55 GB per copy)."""
+    tau = 0.05
+    grid_r, fr = refstep.make_field(slvp, "landau4d", "dg", 288, 3)
+    fr = slvp.strang_step(fr, tau, workers=refstep.host_threads(), consume=True)
+    rr = slvp.diagnostics(fr, tau)
+    f0 = _vpb_initial("landau4d", "dg", 288, 3)
+    m0 = vpb.diagnostics(f0, 0.0).mass
+    g, rec = vpb.advance(f0, tau, 1, consume=True, record_time=tau)
+    ref = fr.array
+    nv2 = ref.shape[3]
+    num = den = 0.0
+    worst_fl = 0.0
+    for a in range(0, nv2, 24):
+        b = min(nv2, a + 24)
+        got = g.array[:, :, :, a:b].cpu().numpy()
+        r = np.asarray(ref[:, :, :, a:b])
+        num = max(num, float(np.max(np.abs(got - r))))
+        den = max(den, float(np.max(np.abs(r))))
+        del got, r
+    for a in range(0, nv2, 24):  # floored pointwise error, needs the global peak
+        b = min(nv2, a + 24)
+        got = g.array[:, :, :, a:b].cpu().numpy()
+        r = np.asarray(ref[:, :, :, a:b])
+        worst_fl = max(worst_fl, float(np.max(np.abs(got - r) / np.maximum(np.abs(r), FLOOR * den))))
+        del got, r
+    err = num / den
+    print(f"cfg5 step 1: max-rel {err:.2e} floored {worst_fl:.2e} EE {rec.electric_energy:.15g} "
+          f"ref {rr.electric_energy:.15g}")
+    assert err <= F_TOL
+    assert worst_fl <= FLOOR_TOL
+    assert abs(rec.electric_energy - rr.electric_energy) <= EE_TOL * rr.electric_energy
+    assert abs(rec.mass - m0) <= MASS_TOL * m0
