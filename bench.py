@@ -373,10 +373,13 @@ def run_sharded(args, cfg_name: str, cfg: dict, d, world: int, rank: int, local:
     if cfg["method"] == "dg" and args.layout == "v":
         # velocity sharding (the paper's decomposition): v2 slabs, local x
         # passes, one v2 halo exchange per step (dist.VShardedSolver)
-        solver = dist.VShardedSolver(grid, dist.TorchComm(), [rank], world)
+        solver = dist.VShardedSolver(grid, dist.TorchComm(), [rank], world,
+                                     peer_halos=args.peer_halos)
         local_f = lambda: solver.local(solver.f[rank], rank)  # noqa: E731
-        layout = (f"v2-shard x{world} (local x passes; NCCL v2 halos of {solver.H} cells "
-                  "per side, zero-copy; rho partials all-gathered)")
+        layout = (f"v2-shard x{world} (local x passes; v2 halos of {solver.H} cells per side "
+                  + ("read in place from the neighbours' buffers over NVLink (CUDA IPC)"
+                     if args.peer_halos else "by zero-copy NCCL send/recv")
+                  + "; rho partials all-gathered)")
     elif cfg["method"] == "dg":
         # x1 shards when the merged stencil pass applies (its halo fits a
         # shard), else the process grid (x1 x x2 at 8 GPUs)
@@ -763,6 +766,9 @@ def main() -> None:
     ap.add_argument("--layout", default="v", choices=["v", "x"],
                     help="N > 1, dG: v2 slabs (VShardedSolver, default) or x1 / x1 x x2 "
                          "shards (ShardedSolver)")
+    ap.add_argument("--peer-halos", action="store_true",
+                    help="--layout v: the v pass reads the neighbours' boundary rows in place "
+                         "(CUDA IPC peer memory) instead of NCCL halo rows")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent replicas instead of the sharded field")
     ap.add_argument("--ref-budget", type=float, default=240.0,

@@ -274,6 +274,20 @@ int vpb_dg_sweep_vplane_v2halo(const double* src, double* dst, const int64_t dim
                                const int64_t* q2, const double* alpha2, int32_t* flag1,
                                int32_t* flag2, int32_t* halo_flag, void* stream);
 
+/* The same pass with the halo regions read in place from the neighbouring
+ * shards' own buffers (peer memory over NVLink, CUDA IPC-mapped; the halo
+ * exchange fused into the pass): left halo = cells [l_cell0, l_cell0 + H)
+ * of src_l, own cells from cell c_cell0 of src, right halo = cells
+ * [r_cell0, r_cell0 + H) of src_r (each buffer src_*_cells v2 cells). */
+int vpb_dg_sweep_vplane_v2peer(const double* src_l, int32_t src_l_cells, int32_t l_cell0,
+                               const double* src, int32_t src_cells, int32_t c_cell0,
+                               const double* src_r, int32_t src_r_cells, int32_t r_cell0,
+                               int32_t halo_cells, double* dst, const int64_t dims[4],
+                               int32_t order, const double* a1, const double* b1,
+                               const int64_t* q1, const double* alpha1, const double* a2,
+                               const double* b2, const int64_t* q2, const double* alpha2,
+                               int32_t* flag1, int32_t* flag2, int32_t* halo_flag, void* stream);
+
 /* One spline sweep along `axis`; shift of line = values[table row]*scale. */
 int vpb_spline_sweep_axis(int32_t axis, const double* src, double* dst, const int64_t dims[4],
                           const double* values, double scale, double h, int32_t* flag,

@@ -109,6 +109,10 @@ SIGNATURES = {
                                    + [c_int32, c_void_p]),
     "vpb_dg_sweep_vplane_v2halo": (c_int, [c_void_p, c_void_p, POINTER(c_int64), c_int32,
                                            c_int32, c_int32] + [c_void_p] * 12),
+    "vpb_dg_sweep_vplane_v2peer": (c_int, [c_void_p, c_int32, c_int32, c_void_p, c_int32,
+                                           c_int32, c_void_p, c_int32, c_int32, c_int32,
+                                           c_void_p, POINTER(c_int64), c_int32]
+                                   + [c_void_p] * 12),
     "vpb_slab_copy": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64, c_void_p]),
     "vpb_spline_sweep_axis": (c_int, [c_int32, c_void_p, c_void_p, POINTER(c_int64), c_void_p,
                                       c_double, c_double, c_void_p, c_void_p]),

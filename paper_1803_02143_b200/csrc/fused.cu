@@ -689,14 +689,25 @@ __global__ void __launch_bounds__(32 * kVCells)
 constexpr int kVSpan = 3;    // window = kVCells + kVSpan cells (q1 spread <= 2)
 constexpr int kVStages = 4;
 
-// VH (v2-sharded fields, dist.VShardedSolver): src holds C2 source v2 cells,
-// the shard's own cells at [v2off, v2off + C2out) with halo cells of the
-// neighbouring ranks before and after them (contiguous rows: v2 is the
-// outermost axis), and dst holds the C2out output cells.  The stream is not
-// periodic: source cells k = 0 .. C2-1, the pair (k-1, k) produces output
-// cell k - v2off + q2(x), stored when inside [0, C2out).  A lane whose
-// shift would need a source cell outside the halos raises vh_flag (the
-// host's halo width bounds |E tau / h_v|; the solver raises on the flag).
+// VH (v2-sharded fields, dist.VShardedSolver): the source stream has C2
+// v2 cells, the shard's own cells at [v2off, v2off + C2out) with v2off halo
+// cells of each neighbouring rank before and after them, and dst holds the
+// C2out output cells.  The three regions may live in three buffers: `VHalo`
+// gives, per region, the buffer (its own tensor map for the TMA ring and
+// its base pointer for direct loads) and the buffer cell of the region's
+// first stream cell -- the halos are either rows of this shard's extended
+// buffer filled by NCCL, or the neighbours' own boundary rows read in place
+// over NVLink (IPC-mapped peer memory: the exchange fused into the pass).
+// The stream is not periodic: source cells k = 0 .. C2-1, the pair (k-1, k)
+// produces output cell k - v2off + q2(x), stored when inside [0, C2out).  A
+// lane whose shift would need a source cell outside the halos raises
+// vh_flag (the host's halo width bounds |E tau / h_v|; the solver raises).
+struct VHalo {
+  const double* src_l;  // left halo region: buffer and the cell of stream cell 0
+  const double* src_r;  // right halo region: buffer and the cell of stream cell v2off + C2out
+  int cl0, cc0, cr0;    // own region: `src` at cell cc0 for stream cell v2off
+};
+
 template <int P, bool VH = false>
 __global__ void __launch_bounds__(32 * kVCells)
     dg_vplane_tma_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t nx,
@@ -706,7 +717,10 @@ __global__ void __launch_bounds__(32 * kVCells)
                          const double* __restrict__ b2, const int64_t* __restrict__ q2,
                          const double* __restrict__ al2, int32_t* __restrict__ flag1,
                          int32_t* __restrict__ flag2, const __grid_constant__ CUtensorMap tmap,
-                         int v2off = 0, int C2out = 0, int32_t* __restrict__ vh_flag = nullptr) {
+                         int v2off = 0, int C2out = 0, int32_t* __restrict__ vh_flag = nullptr,
+                         const __grid_constant__ CUtensorMap tmap_l = CUtensorMap{},
+                         const __grid_constant__ CUtensorMap tmap_r = CUtensorMap{},
+                         const VHalo vhs = VHalo{}) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int W = kVCells + kVSpan;       // window cells
   constexpr int WP = W * P;                 // window v1 dofs
@@ -787,14 +801,37 @@ __global__ void __launch_bounds__(32 * kVCells)
   const double* up_base = src + (int64_t)up1 * P * nx + x;
   bool bad1 = false, bad2 = false;
 
+  // VH: stream cell k -> (region tensor map / base pointer, buffer cell)
+  auto region = [&](int k, const CUtensorMap*& map, const double*& base, int& bc) {
+    if (!VH) {
+      map = &tmap;
+      base = src;
+      bc = k == C2 ? 0 : k;
+    } else if (k < v2off) {
+      map = &tmap_l;
+      base = vhs.src_l;
+      bc = vhs.cl0 + k;
+    } else if (k < v2off + C2out) {
+      map = &tmap;
+      base = src;
+      bc = vhs.cc0 + k - v2off;
+    } else {
+      map = &tmap_r;
+      base = vhs.src_r;
+      bc = vhs.cr0 + k - v2off - C2out;
+    }
+  };
   auto issue = [&](int k) {  // source v2 cell k (0..klast) into slot k % kVStages
-    const int s = (!VH && k == C2) ? 0 : k;
+    const CUtensorMap* map;
+    const double* base;
+    int s;
+    region(k, map, base, s);
     const int sl = k % kVStages;
     double* dstp = ring + sl * stage;
     mbar_arrive_expect_tx(bars + sl, (uint32_t)(wcells * P * P * 32) * 8u);
     int cell = wstart;
     for (int w = 0; w < wcells; ++w) {  // one {32 x, P dofs, P rows} box per needed cell
-      tma_load_3d(dstp + w * (P * P * 32), &tmap, (int)x0, cell * P, s * P, bars + sl);
+      tma_load_3d(dstp + w * (P * P * 32), map, (int)x0, cell * P, s * P, bars + sl);
       if (++cell == C1) cell = 0;
     }
   };
@@ -823,10 +860,14 @@ __global__ void __launch_bounds__(32 * kVCells)
           ul[m2][m] = t[((wlo * P + m2) * P + m) * 32];
         }
     } else {
-      const int s = (!VH && k == C2) ? 0 : k;
+      const CUtensorMap* map;
+      const double* base;
+      int s;
+      region(k, map, base, s);
+      const int64_t rb = (base - src);  // same x / v1 layout in every region's buffer
 #pragma unroll
       for (int m2 = 0; m2 < P; ++m2) {
-        const int64_t r = ((int64_t)s * P + m2) * row_stride;
+        const int64_t r = rb + ((int64_t)s * P + m2) * row_stride;
 #pragma unroll
         for (int m = 0; m < P; ++m) {
           uu[m2][m] = __ldcs(up_base + r + m * nx);
@@ -974,27 +1015,41 @@ static int launch_vplane(const double* src, double* dst, const int64_t dims[4], 
   return launched("dg_vplane_kernel");
 }
 
-// v2-sharded shard: src = [v2 halo | shard cells | v2 halo] (C2src cells),
-// dst = the shard's C2out cells.  TMA ring only (the halo stream has no
-// direct-load kernel); needs nx % 32 == 0 and at least kVCells + kVSpan v1 cells.
+// v2-sharded shard: the stream [left halo (H cells) | own cells | right
+// halo (H cells)], each region in its own buffer (bl / bc / br with nl_cells
+// / nc_cells / nr_cells v2 cells; the region starts at buffer cell l0 / c0 /
+// r0), dst = the shard's own cells.  TMA ring only (the halo stream has no
+// separate direct-load kernel); needs nx % 32 == 0 and at least kVCells +
+// kVSpan v1 cells.
 template <int P>
-static int launch_vplane_vh(const double* src, double* dst, const int64_t dims[4], int C2src,
-                            int v2off, const double* a1, const double* b1, const int64_t* q1,
-                            const double* al1, const double* a2, const double* b2,
-                            const int64_t* q2, const double* al2, int32_t* f1, int32_t* f2,
-                            int32_t* vh_flag, cudaStream_t st) {
+static int launch_vplane_vh(const double* bl, int nl_cells, int l0, const double* bc,
+                            int nc_cells, int c0, const double* br, int nr_cells, int r0,
+                            double* dst, const int64_t dims[4], int H, const double* a1,
+                            const double* b1, const int64_t* q1, const double* al1,
+                            const double* a2, const double* b2, const int64_t* q2,
+                            const double* al2, int32_t* f1, int32_t* f2, int32_t* vh_flag,
+                            cudaStream_t st) {
   const int64_t nx = dims[0] * dims[1];
   const int C1 = (int)(dims[2] / P);
   const int C2out = (int)(dims[3] / P);
   if (nx == 0 || C1 == 0 || C2out == 0) return VPB_OK;
   VPB_REQUIRE(nx % 32 == 0 && C1 >= kVCells + kVSpan,
               "v2-halo v pass needs nx %% 32 == 0 and >= %d v1 cells", kVCells + kVSpan);
-  VPB_REQUIRE((reinterpret_cast<uintptr_t>(src) & 15) == 0, "field buffers must be 16-byte aligned");
-  const uint64_t nv1 = (uint64_t)C1 * P, nv2 = (uint64_t)C2src * P;
-  CUtensorMap tmap;
-  if (!encode_tmap_3d(&tmap, src, (uint64_t)nx, nv1, nv2, (uint64_t)nx * 8,
+  VPB_REQUIRE(H >= 1 && l0 >= 0 && l0 + H <= nl_cells && c0 >= 0 && c0 + C2out <= nc_cells &&
+                  r0 >= 0 && r0 + H <= nr_cells,
+              "v2 halo regions outside their buffers");
+  for (const double* b : {bl, bc, br})
+    VPB_REQUIRE(b && (reinterpret_cast<uintptr_t>(b) & 15) == 0,
+                "field buffers must be 16-byte aligned");
+  const uint64_t nv1 = (uint64_t)C1 * P;
+  CUtensorMap tl, tc, tr;
+  if (!encode_tmap_3d(&tl, bl, (uint64_t)nx, nv1, (uint64_t)nl_cells * P, (uint64_t)nx * 8,
+                      (uint64_t)nx * nv1 * 8, 32, P, P) ||
+      !encode_tmap_3d(&tc, bc, (uint64_t)nx, nv1, (uint64_t)nc_cells * P, (uint64_t)nx * 8,
+                      (uint64_t)nx * nv1 * 8, 32, P, P) ||
+      !encode_tmap_3d(&tr, br, (uint64_t)nx, nv1, (uint64_t)nr_cells * P, (uint64_t)nx * 8,
                       (uint64_t)nx * nv1 * 8, 32, P, P)) {
-    set_error("cannot encode the v-plane tensor map");
+    set_error("cannot encode the v-plane tensor maps");
     return VPB_ERR_UNSUPPORTED;
   }
   const size_t smem = (size_t)kVStages * P * (kVCells + kVSpan) * P * 32 * 8 + kVStages * 8;
@@ -1005,10 +1060,11 @@ static int launch_vplane_vh(const double* src, double* dst, const int64_t dims[4
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
+  const VHalo vhs{bl, br, l0, c0, r0};
   dim3 grid((unsigned)((C1 + kVCells - 1) / kVCells), (unsigned)((nx + 31) / 32));
   dg_vplane_tma_kernel<P, true><<<grid, 32 * kVCells, smem, st>>>(
-      src, dst, nx, C1, C2src, a1, b1, q1, al1, a2, b2, q2, al2, f1, f2, tmap, v2off, C2out,
-      vh_flag);
+      bc, dst, nx, C1, C2out + 2 * H, a1, b1, q1, al1, a2, b2, q2, al2, f1, f2, tc, H, C2out,
+      vh_flag, tl, tr, vhs);
   return launched("dg_vplane_tma_kernel");
 }
 
@@ -1030,13 +1086,43 @@ extern "C" int vpb_dg_sweep_vplane_v2halo(const double* src, double* dst, const 
   VPB_REQUIRE(src != dst, "src and dst must be distinct buffers");
   VPB_REQUIRE(order >= 1 && order <= kMaxOrder, "order %d outside 1..9", order);
   VPB_REQUIRE(dims[2] % order == 0 && dims[3] % order == 0, "v axes not whole cells");
-  VPB_REQUIRE(v2_offset >= 0 && v2_offset + dims[3] / order <= src_v2_cells,
-              "shard cells outside the source stream");
+  const int nc = (int)(dims[3] / order);
+  VPB_REQUIRE(v2_offset >= 1 && v2_offset + nc + v2_offset <= src_v2_cells,
+              "shard cells and halos outside the source stream");
   cudaStream_t st = (cudaStream_t)stream;
   int rc = VPB_OK;
-  VPB_XPLANE_SWITCH(order, rc = launch_vplane_vh<PP>(src, dst, dims, src_v2_cells, v2_offset, a1,
+  const int H = v2_offset;
+  VPB_XPLANE_SWITCH(order, rc = launch_vplane_vh<PP>(src, src_v2_cells, 0, src, src_v2_cells, H,
+                                                     src, src_v2_cells, H + nc, dst, dims, H, a1,
                                                      b1, q1, alpha1, a2, b2, q2, alpha2, flag1,
                                                      flag2, halo_flag, st));
+  return rc;
+}
+
+// The same pass with the halo regions read IN PLACE from the neighbouring
+// shards' buffers (peer memory over NVLink, CUDA IPC-mapped): the left halo
+// is cells [l_cell0, l_cell0 + H) of src_l (src_l_cells cells), the own
+// cells start at cell c_cell0 of src, the right halo is cells [r_cell0,
+// r_cell0 + H) of src_r.  No exchange, no halo rows: the collective is fused
+// into the pass (the host orders it after the neighbours' x pass).
+extern "C" int vpb_dg_sweep_vplane_v2peer(const double* src_l, int32_t src_l_cells, int32_t l_cell0,
+                                          const double* src, int32_t src_cells, int32_t c_cell0,
+                                          const double* src_r, int32_t src_r_cells, int32_t r_cell0,
+                                          int32_t halo_cells, double* dst, const int64_t dims[4],
+                                          int32_t order, const double* a1, const double* b1,
+                                          const int64_t* q1, const double* alpha1, const double* a2,
+                                          const double* b2, const int64_t* q2, const double* alpha2,
+                                          int32_t* flag1, int32_t* flag2, int32_t* halo_flag,
+                                          void* stream) {
+  VPB_REQUIRE(src != dst, "src and dst must be distinct buffers");
+  VPB_REQUIRE(order >= 1 && order <= kMaxOrder, "order %d outside 1..9", order);
+  VPB_REQUIRE(dims[2] % order == 0 && dims[3] % order == 0, "v axes not whole cells");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = VPB_OK;
+  VPB_XPLANE_SWITCH(order, rc = launch_vplane_vh<PP>(src_l, src_l_cells, l_cell0, src, src_cells,
+                                                     c_cell0, src_r, src_r_cells, r_cell0, dst,
+                                                     dims, halo_cells, a1, b1, q1, alpha1, a2, b2,
+                                                     q2, alpha2, flag1, flag2, halo_flag, st));
   return rc;
 }
 

@@ -171,6 +171,19 @@ class TorchComm:
         for req in reqs:
             req.wait()
 
+    def allgather_object(self, obj) -> list:
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+    def barrier_device(self) -> None:
+        """Order every rank's stream after every other rank's queued work
+        (a one-element all-reduce on the stream; no host synchronisation)."""
+        t = torch.zeros(1, dtype=torch.int32,
+                        device=torch.device("cuda", torch.cuda.current_device())
+                        if torch.cuda.is_available() else "cpu")
+        self.dist.all_reduce(t, group=self.group)
+
     def allgather(self, local: dict) -> list:
         (t,) = local.values()
         out = [torch.empty_like(t) for _ in range(self.world)]
@@ -210,6 +223,9 @@ class VirtualComm:
     @staticmethod
     def wait(reqs: list) -> None:
         return None
+
+    def barrier_device(self) -> None:
+        return None  # one process, one stream: already ordered
 
     def allgather(self, local: dict) -> list:
         return [local[r] for r in range(self.world)]
@@ -379,6 +395,17 @@ class CudaOps:
             t2.a.data_ptr(), t2.b.data_ptr(), t2.q.data_ptr(), t2.alpha.data_ptr(),
             f1.data_ptr(), f2.data_ptr(), hflag.data_ptr(), self._device.stream()),
             "vpb_dg_sweep_vplane_v2halo")
+
+    def vplane_v2peer(self, src_l, l_cells, l0, src, c_cells, c0, src_r, r_cells, r0, H, dst,
+                      dims, order, t1, t2, f1, f2, hflag):
+        L = self._lib
+        L.check(self.lib.vpb_dg_sweep_vplane_v2peer(
+            src_l.data_ptr(), int(l_cells), int(l0), src.data_ptr(), int(c_cells), int(c0),
+            src_r.data_ptr(), int(r_cells), int(r0), int(H), dst.data_ptr(), L.dims(dims), order,
+            t1.a.data_ptr(), t1.b.data_ptr(), t1.q.data_ptr(), t1.alpha.data_ptr(),
+            t2.a.data_ptr(), t2.b.data_ptr(), t2.q.data_ptr(), t2.alpha.data_ptr(),
+            f1.data_ptr(), f2.data_ptr(), hflag.data_ptr(), self._device.stream()),
+            "vpb_dg_sweep_vplane_v2peer")
 
     def pack(self, axis, f, dims, order, cell0, width, buf):
         L = self._lib
@@ -1254,7 +1281,7 @@ class VShardedSolver:
     """
 
     def __init__(self, grid: GridSpec, comm, ranks, world: int, ops=None, device=None,
-                 halo_cells: int = 1):
+                 halo_cells: int = 1, peer_halos: bool = False):
         if grid.method != DG or grid.ndim != 4:
             raise NotImplementedError("the velocity-sharded step covers the 2x2v SLDG path")
         p = grid.order
@@ -1296,6 +1323,36 @@ class VShardedSolver:
         self._xtab = {}
         self._dens = None
         self._halo_bytes = 0
+        # peer_halos: the v pass reads the neighbours' boundary rows in place
+        # (vpb_dg_sweep_vplane_v2peer) instead of receiving them into halo rows
+        self.peer_halos = bool(peer_halos)
+        self._nswap = 0  # passes so far: every shard's f is its buffer pair[_nswap % 2]
+        self._peer_pair = {}
+        if self.peer_halos:
+            self._map_peers()
+
+    def _map_peers(self) -> None:
+        """Buffer pairs of the v2 neighbours: this process's own tensors when
+        they are local (VirtualComm), else CUDA IPC mappings of the remote
+        ones (peer memory over NVLink), exchanged once with the communicator."""
+        need = set()
+        for r in self.ranks:
+            need.update({(r - 1) % self.world, (r + 1) % self.world})
+        remote = sorted(need - set(self.ranks))
+        for nb in need & set(self.ranks):
+            self._peer_pair[nb] = (self.f[nb], self.buf[nb])
+        if remote:
+            from torch.multiprocessing.reductions import rebuild_cuda_tensor, reduce_tensor
+
+            (r,) = self.ranks
+            mine = tuple(reduce_tensor(t)[1] for t in (self.f[r], self.buf[r]))
+            allargs = self.comm.allgather_object(mine)
+            for nb in remote:
+                self._peer_pair[nb] = tuple(rebuild_cuda_tensor(*a) for a in allargs[nb])
+
+    def _peer_f(self, nb: int) -> torch.Tensor:
+        """Neighbour nb's current f (its buffers swap in lockstep with ours)."""
+        return self._peer_pair[nb][self._nswap % 2]
 
     # -- geometry ----------------------------------------------------------------
     def dims(self, r: int):
@@ -1408,7 +1465,8 @@ class VShardedSolver:
         # split every shard (decided on the global decomposition, so every
         # rank sums its density blocks in the same pattern) when all have an
         # interior beyond the two boundary blocks
-        split = feeds_v and all(c1 - c0 >= 2 * H + 1 for c0, c1 in self.cr)
+        split = (feeds_v and not self.peer_halos
+                 and all(c1 - c0 >= 2 * H + 1 for c0, c1 in self.cr))
         blocks = {}
         for r in self.ranks:
             c0, c1 = self.cr[r]
@@ -1418,7 +1476,7 @@ class VShardedSolver:
             for a, b in (blocks[r][:2] if split else blocks[r]):
                 run(r, a, b, feeds_v, parts[r])
         reqs = []
-        if feeds_v:
+        if feeds_v and not self.peer_halos:
             # the boundary cells of the new state are in buf: send them now
             # (NCCL runs on its own stream; the pass's timer label spans it)
             reqs = self._post_halos(self.buf)
@@ -1437,6 +1495,7 @@ class VShardedSolver:
                 stats_row[r][0] = mean
         for r in self.ranks:
             self.f[r], self.buf[r] = self.buf[r], self.f[r]
+        self._nswap += 1
         return reqs
 
     def _sum_parts(self, parts: dict) -> torch.Tensor:
@@ -1475,18 +1534,40 @@ class VShardedSolver:
         nx = self.n1 * self.n2
         tv = [self.ops.tables(self.e[d * nx:(d + 1) * nx], tau, g.axes[2 + d].h, g.dg_degree)
               for d in range(2)]
+        p, H = self.order, self.H
+        if self.peer_halos:
+            # the neighbours' x passes are complete: the rho gather that the
+            # field solve waited for ordered every rank after them
+            mark("sweep_v12")
+            for r in self.ranks:
+                c0, c1 = self.cr[r]
+                left, right = (r - 1) % self.world, (r + 1) % self.world
+                nl_l = self.cr[left][1] - self.cr[left][0]
+                nl_r = self.cr[right][1] - self.cr[right][0]
+                f1, f2 = fl[r]
+                self.ops.vplane_v2peer(self._peer_f(left), nl_l + 2 * H, nl_l, self.f[r],
+                                       c1 - c0 + 2 * H, H, self._peer_f(right), nl_r + 2 * H, H,
+                                       H, self.local(self.buf[r], r), self.dims(r), p, tv[0],
+                                       tv[1], f1, f2, hflag)
+            self._halo_bytes += sum(8 * 2 * H * p * self.row for _ in self.ranks)
+            for r in self.ranks:
+                self.f[r], self.buf[r] = self.buf[r], self.f[r]
+            self._nswap += 1
+            # a neighbour's next x pass overwrites the buffer just read here
+            self.comm.barrier_device()
+            return
         if reqs is None:
             mark("halo_v2")
             reqs = self._post_halos(self.f)
         self.comm.wait(reqs)
         mark("sweep_v12")
-        p = self.order
         for r in self.ranks:
             c0, c1 = self.cr[r]
             f1, f2 = fl[r]
             self.ops.vplane_v2halo(self.f[r], self.local(self.buf[r], r), self.dims(r), p,
-                                   c1 - c0 + 2 * self.H, self.H, tv[0], tv[1], f1, f2, hflag)
+                                   c1 - c0 + 2 * H, H, tv[0], tv[1], f1, f2, hflag)
             self.f[r], self.buf[r] = self.buf[r], self.f[r]
+        self._nswap += 1
 
     def advance(self, tau: float, nsteps: int, first_step: int | None = None,
                 timer=None) -> None:

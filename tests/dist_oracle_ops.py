@@ -144,6 +144,18 @@ class NumpyOps:
         ext = self._sweep_lines(ext, 3, ed, order, t2)
         self._store(dst, dims, ext[:, :, :, off * order:off * order + nv2], f2)
 
+    def vplane_v2peer(self, src_l, l_cells, l0, src, c_cells, c0, src_r, r_cells, r0, H, dst,
+                      dims, order, t1, t2, f1, f2, hflag):
+        """The halo regions read from the neighbours' buffers: assemble the
+        stream [left H cells | own cells | right H cells] and run the
+        extended-buffer pass."""
+        n1, n2, nv1, nv2 = dims
+        row = n1 * n2 * nv1 * order  # doubles per v2 cell
+        nc = nv2 // order
+        ext = torch.cat([src_l[l0 * row:(l0 + H) * row], src[c0 * row:(c0 + nc) * row],
+                         src_r[r0 * row:(r0 + H) * row]])
+        self.vplane_v2halo(ext, dst, dims, order, nc + 2 * H, H, t1, t2, f1, f2, hflag)
+
     # -- three-cell x-plane stencil passes (ShardedSolver.advance) ------------
     def stencil_tables(self, tab, single: bool):
         a, b = tab.a, tab.b

@@ -365,6 +365,26 @@ def test_virtual_vsharded_advance_matches_oracle_steps(world):
         assert got[k] == pytest.approx(ref[k], rel=1e-12), k
 
 
+@pytest.mark.parametrize("world", [2, 3])
+def test_virtual_vsharded_peer_halos_match_exchanged_halos(world):
+    """peer_halos: the v pass reads the neighbours' boundary rows in place
+    (the NVLink peer-memory variant) -- the same result as the NCCL-filled
+    halo rows (bitwise when the exchanged variant does not split its x pass
+    into boundary and interior blocks, else up to the density partials'
+    summation order)."""
+    grid, og = vgrids()
+    out = []
+    for peer in (False, True):
+        solver = dist.VShardedSolver(grid, dist.VirtualComm(world), range(world), world,
+                                     ops=NumpyOps(), device=torch.device("cpu"), peer_halos=peer)
+        solver.scatter(core.initialize(PROB, og))
+        solver.advance(TAU, 3)
+        out.append(solver.gather())
+    if world == 3:  # shards of 3, 3, 2 cells: no boundary/interior split
+        assert np.array_equal(out[0], out[1])
+    assert max_rel(out[1], out[0]) <= 1e-14
+
+
 def test_vsharded_rejects_shards_narrower_than_the_halo():
     grid, _ = vgrids()
     with pytest.raises(ValueError, match="narrower than"):

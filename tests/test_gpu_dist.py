@@ -121,6 +121,52 @@ def test_vsharded_advance_matches_single_gpu_advance(world, tau):
         assert got[k] == pytest.approx(getattr(rec, k), rel=1e-12), k
 
 
+@pytest.mark.parametrize("world", [2, 3])
+def test_vsharded_peer_halos_match_exchanged_halos(world):
+    """peer_halos=True: the v pass reads the neighbours' boundary rows in
+    place through per-region tensor maps (vpb_dg_sweep_vplane_v2peer; on a
+    multi-GPU box the neighbours' buffers are CUDA IPC mappings over NVLink)
+    -- against the exchanged-halo solver and the single-GPU advance()."""
+    prob = vpb.problem_spec("landau4d")
+    grid = vpb.make_grid(prob, "dg", DOFS, dg_order=3)
+    out = []
+    for peer in (False, True):
+        solver = dist.VShardedSolver(grid, dist.VirtualComm(world), range(world), world,
+                                     peer_halos=peer)
+        solver.initialize(prob)
+        solver.advance(TAU, 4)
+        out.append(solver.gather())
+    f = vpb.advance(vpb.initialize(prob, grid), TAU, 4)
+    assert max_rel(out[1], f.numpy()) <= 1e-13
+    assert max_rel(out[1], out[0]) <= 1e-14
+
+
+def _ipc_child(args, q):
+    import torch as _t
+    from torch.multiprocessing.reductions import rebuild_cuda_tensor
+
+    t = rebuild_cuda_tensor(*args)
+    q.put((float(t.sum()), float(t[7])))
+
+
+def test_cuda_ipc_mapping_used_for_peer_halos():
+    """The plumbing VShardedSolver._map_peers uses on a multi-GPU box (each
+    rank maps its neighbours' buffers with torch's CUDA IPC reductions): a
+    second process maps this process's buffer and reads it."""
+    import torch.multiprocessing as tmp
+    from torch.multiprocessing.reductions import reduce_tensor
+
+    t = torch.arange(1000, dtype=torch.float64, device="cuda")
+    args = reduce_tensor(t)[1]
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    proc = ctx.Process(target=_ipc_child, args=(args, q))
+    proc.start()
+    got = q.get(timeout=120)
+    proc.join(timeout=60)
+    assert got == (float(t.sum()), 7.0)
+
+
 def test_vsharded_v2halo_pass_bitwise_equal_to_fused_v_pass():
     """The halo-fed v pass of each slab is bitwise the single-GPU fused v
     pass restricted to the slab (same operations, same order)."""
