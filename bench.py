@@ -241,6 +241,26 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # distributed plumbing
 # ---------------------------------------------------------------------------
+# The JSON line goes to the process's original stdout; everything else that
+# writes to file descriptor 1 (NCCL's version banner, library chatter) is
+# sent to stderr, so stdout carries exactly one JSON line.
+_JSON_OUT = None
+
+
+def protect_stdout() -> None:
+    global _JSON_OUT
+    if _JSON_OUT is None:
+        sys.stdout.flush()
+        _JSON_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def emit_line(line: dict) -> None:
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -248,16 +268,22 @@ def dist_env():
     return world, rank, local
 
 
-def maybe_init(world: int, local: int, backend: str):
+def maybe_init(world: int, local: int, backend: str, force: bool = False):
+    """Process group for N > 1 (torchrun); ``force`` also creates it for a
+    single rank (``--sharded``: the multi-GPU code path, NCCL included, on a
+    one-GPU box)."""
     import torch
     import torch.distributed as dist
 
-    if world > 1 and not dist.is_initialized():
+    if (world > 1 or force) and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", str(world))
         if backend == "nccl":
             torch.cuda.set_device(local)
         dist.init_process_group(backend)
-    return dist if world > 1 else None
+    return dist if (world > 1 or force) else None
 
 
 def barrier(d, device=None):
@@ -351,7 +377,7 @@ def run_reference_arm(args, cfg_name: str, cfg: dict) -> None:
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "host_threads": r["threads"],
     }
-    print(json.dumps(line), flush=True)
+    emit_line(line)
 
 
 # ---------------------------------------------------------------------------
@@ -485,7 +511,7 @@ def run_sharded(args, cfg_name: str, cfg: dict, d, world: int, rank: int, local:
                "path": "per-rank pinned host slab -> H2D -> sharded step -> D2H"}
     step_gbs_local = 6 * BYTES_PER_DOF_SWEEP * n_local / (ms_per_step * 1e-3) / 1e9
     if rank == 0:
-        print(json.dumps({
+        emit_line({
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
@@ -511,7 +537,7 @@ def run_sharded(args, cfg_name: str, cfg: dict, d, world: int, rank: int, local:
                                     if cfg["method"] == "dg" else None},
             "e2e": e2e, "cpu_baseline": None, "clocks": clocks.summary(),
             "gpu_launches": int(gpu_launches),
-        }), flush=True)
+        })
     if d is not None:
         d.destroy_process_group()
 
@@ -520,9 +546,9 @@ def run_vpb(args, cfg_name: str, cfg: dict) -> None:
     import torch
 
     world, rank, local = dist_env()
-    d = maybe_init(world, local, "nccl")
+    d = maybe_init(world, local, "nccl", force=args.sharded)
     torch.cuda.set_device(local)
-    if world > 1 and not args.replicas:
+    if (world > 1 or args.sharded) and not args.replicas:
         return run_sharded(args, cfg_name, cfg, d, world, rank, local)
     import paper_1803_02143_b200 as vpb
     from paper_1803_02143_b200 import driver
@@ -740,7 +766,7 @@ def run_vpb(args, cfg_name: str, cfg: dict) -> None:
                          "graph": "strang_step per step replayed from CUDA graphs"}[mode],
             "per_call": per_call,
         }
-        print(json.dumps(line), flush=True)
+        emit_line(line)
     if d is not None:
         d.destroy_process_group()
 
@@ -769,6 +795,9 @@ def main() -> None:
     ap.add_argument("--peer-halos", action="store_true",
                     help="--layout v: the v pass reads the neighbours' boundary rows in place "
                          "(CUDA IPC peer memory) instead of NCCL halo rows")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the sharded multi-GPU solver (torch.distributed, NCCL) even at "
+                         "N = 1: exercises the N > 1 code path on a one-GPU box")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent replicas instead of the sharded field")
     ap.add_argument("--ref-budget", type=float, default=240.0,
@@ -776,6 +805,7 @@ def main() -> None:
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per launch of the dominant kernel (from profiles/)")
     args = ap.parse_args()
+    protect_stdout()
     if args.warmup < 3 and args.impl == "vpb":
         print("note: warmup raised to 3 (timing rules)", file=sys.stderr)
         args.warmup = 3

@@ -317,18 +317,32 @@ __global__ void __launch_bounds__(32 * kRedWarps)
     for (int k = 0; k < kRedWarps; ++k) t += ws[k][lane];
     rc[e] = t;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    double m = 0.0;
-    for (int64_t b = 0; b < nblocks; ++b) m += mean_part[b];
-    if (stats != nullptr) stats[0] = m / volume;
-    if (diag_out != nullptr) diag_out[0] = m;  // mass
-  }
-  if (blockIdx.x == 0 && threadIdx.x >= 32 && threadIdx.x < 35 && diag_out != nullptr &&
-      mom_part != nullptr) {
-    const int k = threadIdx.x - 32;  // l1, l2^2, kinetic
-    double m = 0.0;
-    for (int64_t b = 0; b < nblocks; ++b) m += mom_part[b * 3 + k];
-    diag_out[1 + k] = m;
+  // the scalar partials (density mean; l1, l2^2, kinetic) of block 0: one
+  // warp each, lane-strided partial sums then a fixed butterfly (the same
+  // order every run)
+  if (blockIdx.x == 0 && w < 4) {
+    const double* src = nullptr;
+    int64_t stride = 1;
+    if (w == 0) {
+      src = mean_part;
+    } else if (diag_out != nullptr && mom_part != nullptr) {
+      src = mom_part + (w - 1);
+      stride = 3;
+    }
+    if (src != nullptr) {
+      double m = 0.0;
+      for (int64_t b = lane; b < nblocks; b += 32) m += src[b * stride];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
+      if (lane == 0) {
+        if (w == 0) {
+          if (stats != nullptr) stats[0] = m / volume;
+          if (diag_out != nullptr) diag_out[0] = m;  // mass
+        } else {
+          diag_out[w] = m;  // l1, l2^2, kinetic
+        }
+      }
+    }
   }
 }
 

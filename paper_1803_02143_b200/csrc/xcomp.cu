@@ -24,9 +24,10 @@
 // Streaming along x2 (per plane, source order from s0 = -2(q2+1) mod C2):
 // C2+2 source cells t = 0, 1, ..., C2+1 arrive in chunks of G cells through an
 // mbarrier ring of 1-D bulk copies; thread c = x1 cell c applies the composed
-// x1 stencil to source cell t (3 x1 cells of each of its P rows), keeps the
-// last two results in registers, and from t = 2 on emits output x2 cell t-2
-// (streaming stores), optionally with the density epilogue of xplane.cuh.
+// x1 stencil to source cell t (3 x1 cells of each of its P rows), folds the
+// result into the running x2 sums of output cells t-2, t-1 and t (registers),
+// and from t = 2 on emits output x2 cell t-2 (streaming stores), optionally
+// with the density epilogue of xplane.cuh.
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -116,7 +117,7 @@ __device__ __forceinline__ double lds_keep(const double* p) {
   asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"((unsigned)__cvta_generic_to_shared(p)));
   return v;
 }
-template <int P, bool DENS, bool HALO = false, bool T2S = false>
+template <int P, bool DENS, bool HALO = false, bool T2S = false, bool BST = false>
 __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? (T2S ? 168 : VPB_XCOMP_MAXNREG) : 168)
     dg_xcomp_kernel(const double* __restrict__ src, double* __restrict__ dst, int n1, int C2,
                     int G, int nst, int64_t nitems, int64_t items_per_block, const XcMap mp,
@@ -136,7 +137,12 @@ __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? (T2S ? 168 : VPB_XCO
   const int hls = HALO ? G * P * sx.wl * P : 0, hrs = HALO ? G * P * sx.wr * P : 0;
   double* hlb = inb + nst * slot;
   double* hrb = hlb + nst * hls;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(hrb + nst * hrs);
+  // BST: output cells are staged in shared memory ([2][G cells], one buffer
+  // per ring chunk parity) and leave by one bulk copy per chunk (the chunk's
+  // output cells are consecutive x2 cells of one plane: contiguous in HBM)
+  double* obuf = hrb + nst * hrs;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(obuf + (BST ? 2 * slot : 0));
+  int ob = 0;  // BST: staging buffer of the current chunk
 
   const int tid = threadIdx.x;
   const int it_begin = (int)(blockIdx.x * items_per_block);
@@ -247,7 +253,12 @@ __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? (T2S ? 168 : VPB_XCO
   int off0 = 0, off1 = 0, off2 = 0;  // element offsets of the three x1 source cells
   int hrs0 = 0, hrs1 = 0, hrs2 = 0;  // HALO: row strides of their regions
 
-  double w0[P][P], w1[P][P];         // x1 results of source cells t-2, t-1
+  // running x2 partial sums: a1 = output t-2 after the AA and AB+BA terms of
+  // source cells t-2, t-1; a2 = output t-1 after the AA term of cell t-1.
+  // Each output's fma chain runs in the same order as a one-shot sum over
+  // (t-2, t-1, t) -- bitwise the same -- but every x1 result is consumed
+  // when it is formed, so no register window shifts between cells.
+  double a1[P][P], a2[P][P];
   bool bad = false;
   int st = 0;
   uint32_t phase = 0;
@@ -356,54 +367,20 @@ __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? (T2S ? 168 : VPB_XCO
               }
             }
           }
-          if (t >= 2) {
-            double o[P][P];
-            if constexpr (E2) {
-#pragma unroll
-              for (int j2 = 0; j2 < P; ++j2)
-#pragma unroll
-                for (int jj = 0; jj < P; ++jj) o[j2][jj] = g[j2][jj];
-            } else {
-              // each table coefficient is loaded once and applied to the P
-              // x1 nodes (same per-output operation order as a jj-outer loop)
-#pragma unroll
-              for (int j2 = 0; j2 < P; ++j2) {
-                double acc[P];
-                {
-                  const double c = VPB_T2(0, j2, 0);
-#pragma unroll
-                  for (int jj = 0; jj < P; ++jj) acc[jj] = c * w0[0][jj];
-                }
-#pragma unroll
-                for (int m = 1; m < P; ++m) {
-                  const double c = VPB_T2(0, j2, m);
-#pragma unroll
-                  for (int jj = 0; jj < P; ++jj) acc[jj] = fma(c, w0[m][jj], acc[jj]);
-                }
-#pragma unroll
-                for (int m = 0; m < P; ++m) {
-                  const double c = VPB_T2(1, j2, m);
-#pragma unroll
-                  for (int jj = 0; jj < P; ++jj) acc[jj] = fma(c, w1[m][jj], acc[jj]);
-                }
-#pragma unroll
-                for (int m = 0; m < P; ++m) {
-                  const double c = VPB_T2(2, j2, m);
-#pragma unroll
-                  for (int jj = 0; jj < P; ++jj) acc[jj] = fma(c, g[m][jj], acc[jj]);
-                }
-#pragma unroll
-                for (int jj = 0; jj < P; ++jj) o[j2][jj] = acc[jj];
-              }
-            }
+          // output x2 cell t-2 (streaming stores, optional density epilogue)
+          auto emit = [&](const double (&o)[P][P]) {
             ExpMax eo;
             const int oc = r.oa + t - 2;
-            double* ot = outp + (int64_t)oc * cell + tid * P;
+            double* ot = BST ? obuf + ob * slot + (t - t0) * cell + tid * P
+                             : outp + (int64_t)oc * cell + tid * P;
 #pragma unroll
             for (int j2 = 0; j2 < P; ++j2) {
 #pragma unroll
               for (int jj = 0; jj < P; ++jj) eo.add(o[j2][jj]);
-              if constexpr (P % 2 == 0) {
+              if constexpr (BST) {
+#pragma unroll
+                for (int jj = 0; jj < P; ++jj) ot[j2 * n1 + jj] = o[j2][jj];
+              } else if constexpr (P % 2 == 0) {
 #pragma unroll
                 for (int jj = 0; jj < P; jj += 2)
                   __stcs(reinterpret_cast<double2*>(ot + j2 * n1 + jj),
@@ -432,14 +409,49 @@ __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? (T2S ? 168 : VPB_XCO
               red_add_hint(mypart + oc * C1 + tid, dmul(wplane, rcv), pol_keep);
               meanacc = fma(wplane, mv, meanacc);
             }
-          }
+          };
+          if constexpr (E2) {
+            if (t >= 2) emit(g);
+          } else {
+            // each table coefficient is loaded once and applied to the P x1
+            // nodes (same per-output operation order as a jj-outer loop)
+            if (t >= 2) {
 #pragma unroll
-          for (int m2 = 0; m2 < P; ++m2)
+              for (int j2 = 0; j2 < P; ++j2)
 #pragma unroll
-            for (int jj = 0; jj < P; ++jj) {
-              w0[m2][jj] = w1[m2][jj];
-              w1[m2][jj] = g[m2][jj];
+                for (int m = 0; m < P; ++m) {
+                  const double c = VPB_T2(2, j2, m);
+#pragma unroll
+                  for (int jj = 0; jj < P; ++jj) a1[j2][jj] = fma(c, g[m][jj], a1[j2][jj]);
+                }
+              emit(a1);
             }
+            if (t >= 1) {
+#pragma unroll
+              for (int j2 = 0; j2 < P; ++j2)
+#pragma unroll
+                for (int m = 0; m < P; ++m) {
+                  const double c = VPB_T2(1, j2, m);
+#pragma unroll
+                  for (int jj = 0; jj < P; ++jj)
+                    a1[j2][jj] = fma(c, g[m][jj], m == 0 ? a2[j2][jj] : a1[j2][jj]);
+                }
+            }
+#pragma unroll
+            for (int j2 = 0; j2 < P; ++j2) {
+              {
+                const double c = VPB_T2(0, j2, 0);
+#pragma unroll
+                for (int jj = 0; jj < P; ++jj) a2[j2][jj] = c * g[0][jj];
+              }
+#pragma unroll
+              for (int m = 1; m < P; ++m) {
+                const double c = VPB_T2(0, j2, m);
+#pragma unroll
+                for (int jj = 0; jj < P; ++jj) a2[j2][jj] = fma(c, g[m][jj], a2[j2][jj]);
+              }
+            }
+          }
         }
       };
       if (active) {
@@ -450,13 +462,35 @@ __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? (T2S ? 168 : VPB_XCO
         else if (!ex2) run(T{}, F{});
         else run(T{}, T{});
       }
+      if constexpr (BST) {
+        fence_proxy_async_smem();            // staged outputs -> async proxy
+        if (tid == 0) bulk_wait_read<0>();   // chunk k-1's store released the other buffer
+      }
       __syncthreads();  // every thread is done with ring slot st
+      if constexpr (BST) {
+        // outputs of this chunk: source cells t >= 2, i.e. output cells
+        // oa + max(t0, 2) - 2 .. oa + t0 + ns - 3
+        const int tb = max(t0, 2), nout = t0 + ns - tb;
+        if (tid == 0 && nout > 0) {
+          const double* sb = obuf + ob * slot + (tb - t0) * cell;
+          double* gd = outp + (int64_t)(r.oa + tb - 2) * cell;
+          if (DENS)
+            bulk_s2g_hint(gd, sb, (uint32_t)nout * cell * 8u, pol_stream);
+          else
+            bulk_s2g(gd, sb, (uint32_t)nout * cell * 8u);
+          bulk_commit();
+        }
+        ob ^= 1;
+      }
       if (tid == 0 && p_it < it_end) issue_next();
       if (++st == nst) {
         st = 0;
         phase ^= 1u;
       }
     }
+  }
+  if constexpr (BST) {
+    if (tid == 0) bulk_wait<0>();  // staged stores complete before the CTA retires
   }
   report_flag(bad, flag);
   if (DENS) {
@@ -478,6 +512,7 @@ __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? (T2S ? 168 : VPB_XCO
 
 struct XcLaunch {
   int threads, G, nst;
+  bool bst;  // output cells leave through shared memory by bulk copies
   size_t smem;
   int64_t ppb, blocks, max_blocks;
 };
@@ -496,17 +531,29 @@ static bool xcomp_t2s(const int64_t dims[4]) {
   }
 }
 
-template <int P, bool DENS, bool HALO, bool T2S>
+template <int P, bool DENS, bool HALO, bool T2S, bool BST>
 static void xcomp_occupancy(int threads, size_t smem, int* occ) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(dg_xcomp_kernel<P, DENS, HALO, T2S>,
+    cudaFuncSetAttribute(dg_xcomp_kernel<P, DENS, HALO, T2S, BST>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr = true;
   }
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, dg_xcomp_kernel<P, DENS, HALO, T2S>, threads,
-                                                smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, dg_xcomp_kernel<P, DENS, HALO, T2S, BST>,
+                                                threads, smem);
 }
+
+// Launch an instance: T2S per xcomp_t2s, BST (halo-free passes only) per the plan.
+#define VPB_XCOMP_DISPATCH(T2S_, BST_, ...)                                           \
+  do {                                                                                \
+    if (T2S_) {                                                                       \
+      if (BST_) { constexpr bool T2 = (P == 3), BS = !HALO; __VA_ARGS__; }            \
+      else { constexpr bool T2 = (P == 3), BS = false; __VA_ARGS__; }                 \
+    } else {                                                                          \
+      if (BST_) { constexpr bool T2 = false, BS = !HALO; __VA_ARGS__; }               \
+      else { constexpr bool T2 = false, BS = false; __VA_ARGS__; }                    \
+    }                                                                                 \
+  } while (0)
 
 template <int P, bool DENS, bool HALO = false>
 static int plan_xcomp(const int64_t dims[4], int64_t nitems, XcLaunch* L, int hcells = 0) {
@@ -542,11 +589,17 @@ static int plan_xcomp(const int64_t dims[4], int64_t nitems, XcLaunch* L, int hc
     set_error("x plane chunk of %d dofs does not fit shared memory", P * n1);
     return VPB_ERR_UNSUPPORTED;
   }
+  // BST: two chunks of output cells staged in shared memory (coalesced bulk
+  // stores instead of 24-byte-strided lane stores), when they fit the same
+  // budget without shrinking the chunk; VPB_XCOMP_BST=0/1 forces it off / on
+  static const int env_bst = getenv("VPB_XCOMP_BST") ? atoi(getenv("VPB_XCOMP_BST")) : -1;
+  const size_t obytes = 2 * (size_t)G * cell_bytes;
+  L->bst = !HALO && env_bst != 0 &&
+           (env_bst == 1 ? L->smem + obytes <= 220 * 1024 : L->smem + obytes <= (size_t)env_smem);
+  if (L->bst) L->smem += obytes;
   int occ = 0;
-  if (xcomp_t2s<P>(dims))
-    xcomp_occupancy<P, DENS, HALO, (P == 3)>(L->threads, L->smem, &occ);
-  else
-    xcomp_occupancy<P, DENS, HALO, false>(L->threads, L->smem, &occ);
+  VPB_XCOMP_DISPATCH(xcomp_t2s<P>(dims), L->bst,
+                     (xcomp_occupancy<P, DENS, HALO, T2, BS>(L->threads, L->smem, &occ)));
   if (occ < 1) occ = 1;
   L->max_blocks = (int64_t)occ * xplane_sm_count();
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(nitems, L->max_blocks));
@@ -565,14 +618,11 @@ static int launch_xcomp(const double* src, double* dst, const int64_t dims[4], i
   XcLaunch L;
   int rc = plan_xcomp<P, DENS, HALO>(dims, nitems, &L, HALO ? sx.wl + sx.wr : 0);
   if (rc) return rc;
-  if (xcomp_t2s<P>(dims))
-    dg_xcomp_kernel<P, DENS, HALO, (P == 3)><<<(unsigned)L.blocks, L.threads, L.smem, st>>>(
-        src, dst, (int)dims[0], (int)(dims[1] / P), L.G, L.nst, nitems, L.ppb, mp, k1, q1, al1,
-        k2, q2, al2, flag, dn, dacc, sx);
-  else
-    dg_xcomp_kernel<P, DENS, HALO, false><<<(unsigned)L.blocks, L.threads, L.smem, st>>>(
-        src, dst, (int)dims[0], (int)(dims[1] / P), L.G, L.nst, nitems, L.ppb, mp, k1, q1, al1,
-        k2, q2, al2, flag, dn, dacc, sx);
+  VPB_XCOMP_DISPATCH(xcomp_t2s<P>(dims), L.bst,
+                     (dg_xcomp_kernel<P, DENS, HALO, T2, BS>
+                      <<<(unsigned)L.blocks, L.threads, L.smem, st>>>(
+                          src, dst, (int)dims[0], (int)(dims[1] / P), L.G, L.nst, nitems, L.ppb,
+                          mp, k1, q1, al1, k2, q2, al2, flag, dn, dacc, sx)));
   if (nblocks_out) *nblocks_out = L.blocks;
   return launched("dg_xcomp_kernel");
 }

@@ -1,0 +1,6 @@
+set -x
+o=gpurun_out/r02b; mkdir -p $o
+nvidia-smi > $o/smi.txt 2>&1
+python -c "import __graft_entry__ as g; g.smoke()" > $o/smoke.log 2>&1; echo smoke rc=$? >> $o/smoke.log
+timeout 2400 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $o/pytest_gpu.log 2>&1; echo rc=$? >> $o/pytest_gpu.log
+python bench.py --steps 20 --warmup 5 > $o/bench_cfg2_20.json 2> $o/bench_cfg2_20.err
