@@ -565,7 +565,8 @@ def run_vpb(args, cfg_name: str, cfg: dict) -> None:
     from paper_1803_02143_b200 import _lib
 
     lib = _lib.load()
-    mode = "graph" if args.graph else ("per-step" if args.per_step else "merged")
+    mode = (("graph" if args.per_step else "advance-graph") if args.graph
+            else ("per-step" if args.per_step else "merged"))
     dev = torch.device("cuda", local)
     nslot = st.flags.numel()
 
@@ -585,7 +586,7 @@ def run_vpb(args, cfg_name: str, cfg: dict) -> None:
                 driver.enqueue_step(field, tau, st, timer=timer)
                 driver.check_step(st, None)
 
-    run_steps(args.warmup, how="merged" if mode == "merged" else "per-step")
+    run_steps(args.warmup, how="merged" if mode in ("merged", "advance-graph") else "per-step")
 
     # --- timed region: K steps, events per kernel group
     labels: list = []
@@ -599,27 +600,34 @@ def run_vpb(args, cfg_name: str, cfg: dict) -> None:
 
     graph = None
     n_launch0 = lib.vpb_launch_count()
-    if mode == "graph":
+    if mode in ("graph", "advance-graph"):
         # the per-kernel breakdown comes from an eager pass of K steps; the
-        # headline timing replays the whole step from CUDA graphs
+        # headline timing replays the steps from CUDA graphs (per step, or the
+        # whole K-step advance() block)
         e0 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        run_steps(args.steps, timer=mark, how="per-step")
+        run_steps(args.steps, timer=mark, how="per-step" if mode == "graph" else "merged")
         e1 = torch.cuda.Event(enable_timing=True)
         e1.record(stream)
         torch.cuda.synchronize()
         eager_ms = e0.elapsed_time(e1)
         eager_launches = lib.vpb_launch_count() - n_launch0
-        graph = driver.StepGraph(field, tau)
-        for _ in range(args.warmup):
-            graph.step()
+        if mode == "graph":
+            graph = driver.StepGraph(field, tau)
+            for _ in range(args.warmup):
+                graph.step()
+        else:
+            graph = driver.AdvanceGraph(field, tau, args.steps)
+            graph.advance()
     barrier(d, local)
     torch.cuda.synchronize()
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
     clocks.begin()
     start.record(stream)
-    if graph is not None:
+    if mode == "advance-graph":
+        graph.advance()
+    elif graph is not None:
         for _ in range(args.steps):
             graph.step()
     else:
@@ -763,7 +771,9 @@ def run_vpb(args, cfg_name: str, cfg: dict) -> None:
                                    "steps share one HBM pass ('fast': composed 3-cell "
                                    "stencils; 'exact': the four sweeps bitwise)",
                          "per-step": "strang_step(consume=True) per step",
-                         "graph": "strang_step per step replayed from CUDA graphs"}[mode],
+                         "graph": "strang_step per step replayed from CUDA graphs",
+                         "advance-graph": "advance(field, tau, K) replayed from a CUDA graph "
+                                          "(driver.AdvanceGraph)"}[mode],
             "per_call": per_call,
         }
         emit_line(line)
@@ -786,7 +796,8 @@ def main() -> None:
     ap.add_argument("--e2e-blocks", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--graph", action="store_true",
-                    help="time per-step calls replayed from CUDA graphs (driver.StepGraph)")
+                    help="replay the K timed steps from a CUDA graph (driver.AdvanceGraph; "
+                         "with --per-step: per-step strang_step graphs, driver.StepGraph)")
     ap.add_argument("--per-step", action="store_true",
                     help="time one strang_step call per step instead of advance()")
     ap.add_argument("--layout", default="v", choices=["v", "x"],

@@ -258,6 +258,10 @@ __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? (T2S ? 168 : VPB_XCO
   // Each output's fma chain runs in the same order as a one-shot sum over
   // (t-2, t-1, t) -- bitwise the same -- but every x1 result is consumed
   // when it is formed, so no register window shifts between cells.
+  // (P <= 2: a1 / a2 are the x1 results of cells t-2 / t-1 instead; measured
+  // in the bench loop, the running sums win at P = 3 (config 2: 4.02 -> 3.83
+  // ms) and lose at P = 2 (config 3: 0.766 -> 0.788 ms))
+  constexpr bool kRunningSums = P >= 3;
   double a1[P][P], a2[P][P];
   bool bad = false;
   int st = 0;
@@ -412,6 +416,50 @@ __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? (T2S ? 168 : VPB_XCO
           };
           if constexpr (E2) {
             if (t >= 2) emit(g);
+          } else if constexpr (!kRunningSums) {
+            // P <= 2: a1 / a2 hold the x1 results of source cells t-2 / t-1
+            // (a few register moves per cell; the AA and AB+BA products of an
+            // output do not wait for cell t)
+            if (t >= 2) {
+              double o[P][P];
+#pragma unroll
+              for (int j2 = 0; j2 < P; ++j2) {
+                double acc[P];
+                {
+                  const double c = VPB_T2(0, j2, 0);
+#pragma unroll
+                  for (int jj = 0; jj < P; ++jj) acc[jj] = c * a1[0][jj];
+                }
+#pragma unroll
+                for (int m = 1; m < P; ++m) {
+                  const double c = VPB_T2(0, j2, m);
+#pragma unroll
+                  for (int jj = 0; jj < P; ++jj) acc[jj] = fma(c, a1[m][jj], acc[jj]);
+                }
+#pragma unroll
+                for (int m = 0; m < P; ++m) {
+                  const double c = VPB_T2(1, j2, m);
+#pragma unroll
+                  for (int jj = 0; jj < P; ++jj) acc[jj] = fma(c, a2[m][jj], acc[jj]);
+                }
+#pragma unroll
+                for (int m = 0; m < P; ++m) {
+                  const double c = VPB_T2(2, j2, m);
+#pragma unroll
+                  for (int jj = 0; jj < P; ++jj) acc[jj] = fma(c, g[m][jj], acc[jj]);
+                }
+#pragma unroll
+                for (int jj = 0; jj < P; ++jj) o[j2][jj] = acc[jj];
+              }
+              emit(o);
+            }
+#pragma unroll
+            for (int m2 = 0; m2 < P; ++m2)
+#pragma unroll
+              for (int jj = 0; jj < P; ++jj) {
+                a1[m2][jj] = a2[m2][jj];
+                a2[m2][jj] = g[m2][jj];
+              }
           } else {
             // each table coefficient is loaded once and applied to the P x1
             // nodes (same per-output operation order as a jj-outer loop)

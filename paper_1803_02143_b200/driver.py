@@ -678,6 +678,64 @@ class StepGraph:
         return self.field
 
 
+class AdvanceGraph:
+    """Blocks of ``nsteps`` merged Strang steps (:func:`advance` with
+    ``consume=True``) replayed from CUDA graphs -- the reference's ``run``
+    loop between two records (driver.py:371-377) repeats the same block, and
+    on small, L2-resident grids the host-side launch cost of the block's
+    kernels exceeds their device time.
+
+    The block is captured once per buffer parity (like :class:`StepGraph`);
+    :meth:`advance` replays it and then performs the same non-finite checks
+    and neutrality warnings as :func:`advance`.  Results are bitwise those of
+    ``advance(field, tau, nsteps, consume=True)``.
+    """
+
+    def __init__(self, field: DistributionField, tau: float, nsteps: int):
+        if nsteps <= 0:
+            raise ValueError("nsteps must be positive")
+        self.field = field
+        self.tau = float(tau)
+        self.nsteps = int(nsteps)
+        self.st = step_state(field.grid)
+        dev = _device.device()
+        self.flags = torch.zeros((nsteps, self.st.flags.numel()), dtype=torch.int32, device=dev)
+        self.stats = torch.zeros((nsteps, self.st.stats.numel()), dtype=torch.float64,
+                                 device=dev)
+        # eager warm-up block: caches x tables, allocates the scratch of every
+        # pass, sets kernel attributes (nothing may allocate during capture)
+        enqueue_steps(field, tau, nsteps, self.st, self.flags, self.stats)
+        check_steps(self.st, self.flags, self.stats, None, tau)
+        self.graphs = []
+        self.bufs = []
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        for _ in range(2):
+            self.bufs.append((field._phys, self.st.buf))
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                enqueue_steps(field, tau, nsteps, self.st, self.flags, self.stats)
+            self.graphs.append(g)
+            if field._phys is self.bufs[0][0]:
+                break  # even number of swaps per block: one graph suffices
+        torch.cuda.current_stream().wait_stream(side)
+        field._phys, self.st.buf = self.bufs[0]  # capture executed nothing
+        self.parity = 0
+
+    def replay(self) -> None:
+        """Queue one block (no host synchronisation, no checks)."""
+        self.graphs[self.parity].replay()
+        nxt = (self.parity + 1) % len(self.graphs)
+        self.field._phys, self.st.buf = self.bufs[nxt]
+        self.parity = nxt
+
+    def advance(self, first_step: int | None = None) -> DistributionField:
+        """One block of ``nsteps`` steps; raises / warns like :func:`advance`."""
+        self.replay()
+        check_steps(self.st, self.flags, self.stats, first_step, self.tau)
+        return self.field
+
+
 def strang_step(field: DistributionField, tau: float, workers: int = 1, consume: bool = False,
                 time_label: float | None = None) -> DistributionField:
     """Advance by one Strang step of size tau (driver.py:245-265).

@@ -357,6 +357,27 @@ def test_step_graph_replays_bitwise_equal_to_eager_steps(prob, method, dofs, ord
         g.step()
 
 
+@pytest.mark.parametrize("prob,method,dofs,order,k", [
+    ("landau4d", "dg", 24, 3, 3), ("landau4d", "dg", 24, 3, 2), ("landau4d", "spline", 16, 0, 3),
+    ("landau2d", "dg", 32, 4, 3), ("twostream4d_baseline", "dg", 16, 2, 4)])
+def test_advance_graph_replays_bitwise_equal_to_advance(prob, method, dofs, order, k):
+    """driver.AdvanceGraph: K-step blocks of advance() from CUDA graphs
+    (both buffer parities when a block swaps an odd number of times)."""
+    problem = vpb.problem_spec(prob)
+    grid = vpb.make_grid(problem, method, dofs, dg_order=order)
+    f_eager = vpb.initialize(problem, grid)
+    f_graph = vpb.initialize(problem, grid)
+    f_eager = vpb.advance(f_eager, 0.1, k, consume=True)  # the constructor's eager block
+    g = vpb.AdvanceGraph(f_graph, 0.1, k)
+    for b in range(3):
+        f_eager = vpb.advance(f_eager, 0.1, k, consume=True)
+        assert g.advance() is f_graph
+        assert np.array_equal(f_graph.numpy(), f_eager.numpy()), b
+    f_graph.data[7] = math.nan
+    with pytest.raises(vpb.SubstepError):
+        g.advance(first_step=4 * k)
+
+
 def test_fused_v_reports_nonfinite_field_in_v1():
     prob = vpb.problem_spec("landau4d")
     grid = vpb.make_grid(prob, "dg", 12, dg_order=3)
