@@ -68,7 +68,10 @@ def check_family(n, src_data, launch):
 
 
 GRIDS = [("landau4d", "dg", (24, 18, 12, 12), 3), ("landau4d", "dg", (16, 12, 10, 8), 2),
-         ("landau4d", "dg", (20, 16, 12, 12), 4)]
+         ("landau4d", "dg", (20, 16, 12, 12), 4),
+         # composed x pass with output staging (BST) over many ring chunks per
+         # plane: 4 cells per chunk (96 x1 dofs) and config 2's 2 cells (192)
+         ("landau4d", "dg", (96, 96, 6, 6), 3), ("landau4d", "dg", (192, 48, 6, 6), 3)]
 
 
 def _field(prob, method, dofs, order, tau=0.7, steps=1):
