@@ -3,7 +3,7 @@
 # (the other objects come from the in-tree build); load it with VPB_LIB=...
 # usage: build_variant.sh NAME "fused fused2 xcomp" -DFOO=1 ...
 set -e
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 name=$1; shift
 srcs=$1; shift
 python -c "import paper_1803_02143_b200._build as b; b.build()"
