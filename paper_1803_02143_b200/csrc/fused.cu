@@ -584,7 +584,10 @@ namespace vpb {
 // Grid: x-fastest is the v1-cell group so the blocks sharing source cells
 // (neighbouring c1) run together and hit L1/L2.
 // ---------------------------------------------------------------------------
-constexpr int kVCells = 4;  // v1 cells (warps) per CTA
+#ifndef VPB_VCELLS
+#define VPB_VCELLS 4
+#endif
+constexpr int kVCells = VPB_VCELLS;  // v1 cells (warps) per CTA
 
 template <int P>
 __global__ void __launch_bounds__(32 * kVCells)
@@ -701,7 +704,10 @@ __global__ void __launch_bounds__(32 * kVCells)
 // keeps every warp access conflict-free whatever the per-lane q1.  Blocks
 // whose q1 spread exceeds the window fall back to direct global loads.
 constexpr int kVSpan = 3;    // window = kVCells + kVSpan cells (q1 spread <= 2)
-constexpr int kVStages = 4;
+#ifndef VPB_VSTAGES
+#define VPB_VSTAGES 4
+#endif
+constexpr int kVStages = VPB_VSTAGES;
 
 // VH (v2-sharded fields, dist.VShardedSolver): the source stream has C2
 // v2 cells, the shard's own cells at [v2off, v2off + C2out) with v2off halo
