@@ -261,6 +261,25 @@ int vpb_dg_sweep_xstencil_rows(const double* src, double* dst, const int64_t dim
                                const double* wcell2_host, double volume, double* work,
                                double* rc_out, double* stats, int32_t phase, void* stream);
 
+/* The stencil pass on an x1 x x2 sharded field (the 4 x 2 process grid of
+ * dist.ShardedSolver): x1 halos hl / hr as for vpb_dg_sweep_xstencil, and the
+ * plane is not periodic in x2 either -- source x2 cells -wl2..-1 and
+ * C2..C2+wr2-1 come from x2l / x2r, three parts each in the shard's own
+ * layouts: [0] the x1 dofs [plane][w2 cells][P rows][n1] (vpb_halo_pack axis
+ * 1 of the neighbour), [1] / [2] the left / right x1 halo cells of those rows
+ * [plane][w2 cells][P rows][wl*P] / [wr*P] (the corners, taken from the
+ * neighbour's x1 halo buffers).  wv1 == NULL: no density epilogue; else as
+ * vpb_dg_sweep_xstencil_density (work: vpb_dg_xstencil_density_work_len). */
+int vpb_dg_sweep_xstencil2(const double* src, double* dst, const int64_t dims[4], int32_t order,
+                           const double* k1, const int64_t* q1, const double* alpha1,
+                           const double* k2, const int64_t* q2, const double* alpha2,
+                           int32_t qmul, const double* hl, int32_t wl, const double* hr,
+                           int32_t wr, int32_t wl2, const double* const x2l[3], int32_t wr2,
+                           const double* const x2r[3], int32_t* flag, const double* wv1,
+                           const double* wv2, const double* mid_host,
+                           const double* wcell1_host, const double* wcell2_host, double volume,
+                           double* work, double* rc_out, double* stats, void* stream);
+
 /* Fused v1 v2 pass of one v2 shard of a velocity-sharded field
  * (dist.VShardedSolver): `src` holds src_v2_cells v2 cells -- the shard's
  * dims[3]/order cells starting at cell v2_offset, neighbour halo cells

@@ -91,11 +91,21 @@ struct XcMap {
 // pass; 1: a single sweep with tables {0, A, B}).  HALO (x1-sharded field):
 // the row is the shard's cells 0..C1-1, not periodic; cells -wl..-1 come from
 // hl and C1..C1+wr-1 from hr, laid out [plane][x2 row][w*P] (vpb_halo_pack).
+// x2-sharded fields (x2 != 0, x1 x x2 process grids): the plane's x2 rows
+// are not periodic either; source x2 cells -wl2..-1 and C2..C2+wr2-1 come
+// from the x2 halo buffers x2l / x2r, each three parts in the layouts of the
+// shard's own data: [0] the x1 dofs [plane][w2 cells][P rows][n1]
+// (vpb_halo_pack axis 1), [1] / [2] their left / right x1 halo cells
+// [plane][w2 cells][P rows][wl*P] / [wr*P] (the x1 halo rows of the
+// neighbour's boundary cells: the corners).
 struct XcStencil {
   int qmul;
   const double* hl;
   const double* hr;
   int wl, wr;
+  int x2 = 0, wl2 = 0, wr2 = 0;
+  const double* x2l[3] = {nullptr, nullptr, nullptr};
+  const double* x2r[3] = {nullptr, nullptr, nullptr};
 };
 
 // Register budget.  A sub-partition holds 16K registers: at 224 per thread
@@ -168,7 +178,8 @@ __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? (T2S ? 168 : VPB_XCO
   auto iv2_of = [&](int l) { return (int)mp.iv2_0 + l / nv1l; };
   // first source cell of an item: -(qmul q2 + 2) + oa (mod C2)
   auto s0_of = [&](const Item& r) {
-    return (int)wrap_mod(-((int64_t)sx.qmul * q2[iv2_of(r.l)] + 2) + r.oa, C2);
+    const int64_t s = -((int64_t)sx.qmul * q2[iv2_of(r.l)] + 2) + r.oa;
+    return HALO && sx.x2 ? (int)s : (int)wrap_mod(s, C2);  // x2-sharded: halo cells
   };
   // producer (thread 0)
   int p_it = it_begin;
@@ -178,6 +189,55 @@ __global__ void __launch_bounds__(128) __maxnreg__(P >= 3 ? (T2S ? 168 : VPB_XCO
     const int t0 = p_k * G;
     const int ns = min(G, p_r.L - t0);
     int sb = p_s0 + t0;
+    if constexpr (HALO) {
+      if (sx.x2) {
+        // x2-sharded: the chunk's cells [sb, sb + ns) lie in [-wl2, C2 + wr2)
+        // (host-sized halos); runs by region, each region in the shard's
+        // own layouts (rows, x1 halo rows)
+        const int hcl = P * sx.wl * P, hcr = P * sx.wr * P;
+        mbar_arrive_expect_tx(bars + p_st, (uint32_t)ns * (cell + hcl + hcr) * 8u);
+        int c = sb, k = 0;
+        while (k < ns) {
+          const double *own, *xl, *xr;
+          int run;
+          if (c < 0) {
+            const int64_t b = (int64_t)p_r.l * sx.wl2 + (c + sx.wl2);
+            own = sx.x2l[0] + b * cell;
+            xl = sx.x2l[1] + b * hcl;
+            xr = sx.x2l[2] + b * hcr;
+            run = min(ns - k, -c);
+          } else if (c < C2) {
+            const int64_t b = (int64_t)p_r.l * C2 + c;
+            own = src + (int64_t)p_r.l * plane_elems + (int64_t)c * cell;
+            xl = sx.hl + b * hcl;
+            xr = sx.hr + b * hcr;
+            run = min(ns - k, C2 - c);
+          } else {
+            const int64_t b = (int64_t)p_r.l * sx.wr2 + (c - C2);
+            own = sx.x2r[0] + b * cell;
+            xl = sx.x2r[1] + b * hcl;
+            xr = sx.x2r[2] + b * hcr;
+            run = ns - k;
+          }
+          bulk_g2s(inb + p_st * slot + k * cell, own, (uint32_t)run * cell * 8u, bars + p_st);
+          if (hcl)
+            bulk_g2s(hlb + p_st * hls + k * hcl, xl, (uint32_t)run * hcl * 8u, bars + p_st);
+          if (hcr)
+            bulk_g2s(hrb + p_st * hrs + k * hcr, xr, (uint32_t)run * hcr * 8u, bars + p_st);
+          k += run;
+          c += run;
+        }
+        if (++p_st == nst) p_st = 0;
+        if (++p_k == p_r.nch) {
+          p_k = 0;
+          if (++p_it < it_end) {
+            p_r = item_of(p_it);
+            p_s0 = s0_of(p_r);
+          }
+        }
+        return;
+      }
+    }
     while (sb >= C2) sb -= C2;
     const double* base = src + (int64_t)p_r.l * plane_elems;
     double* d = inb + p_st * slot;
@@ -838,6 +898,62 @@ extern "C" int vpb_dg_sweep_xstencil_density(
   int64_t used = 0;
   cudaStream_t st = (cudaStream_t)stream;
   const XcStencil sx{qmul, hl, hr, wl, wr};
+  VPB_XPLANE_SWITCH(order, rc = (launch_xcomp<PP, true, true>(
+                               src, dst, dims, dims[2] * dims[3], xcomp_whole_field(dims, PP), k1,
+                               q1, alpha1, k2, q2, alpha2, flag, dn, 0, st, &used, sx)));
+  if (rc) return rc;
+  VPB_REQUIRE(used == nblk, "x-plane launch plan changed (%lld vs %lld CTAs)", (long long)used,
+              (long long)nblk);
+  return launch_xdens_reduce(work, nblk, cc, volume, rc_out, stats, st);
+}
+
+// The stencil pass on an x1 x x2 sharded field: x1 halos as above and x2
+// halos (x2l / x2r, three parts each, see XcStencil) of wl2 / wr2 cells; the
+// plane is not periodic in x2.  wv1 == nullptr: no density epilogue.
+extern "C" int vpb_dg_sweep_xstencil2(
+    const double* src, double* dst, const int64_t dims[4], int32_t order, const double* k1,
+    const int64_t* q1, const double* alpha1, const double* k2, const int64_t* q2,
+    const double* alpha2, int32_t qmul, const double* hl, int32_t wl, const double* hr,
+    int32_t wr, int32_t wl2, const double* const x2l[3], int32_t wr2,
+    const double* const x2r[3], int32_t* flag, const double* wv1, const double* wv2,
+    const double* mid_host, const double* wcell1_host, const double* wcell2_host, double volume,
+    double* work, double* rc_out, double* stats, void* stream) {
+  int rc = xstencil_args(src, dst, dims, order, qmul, hl, wl, hr, wr);
+  if (rc) return rc;
+  VPB_REQUIRE(k1 && q1 && alpha1 && k2 && q2 && alpha2, "null pointer");
+  VPB_REQUIRE(wl2 >= 0 && wr2 >= 0 && wl2 <= dims[1] / order && wr2 <= dims[1] / order,
+              "x2 halo wider than the shard");
+  XcStencil sx{qmul, hl, hr, wl, wr};
+  sx.x2 = 1;
+  sx.wl2 = wl2;
+  sx.wr2 = wr2;
+  for (int k = 0; k < 3; ++k) {
+    sx.x2l[k] = wl2 ? x2l[k] : nullptr;
+    sx.x2r[k] = wr2 ? x2r[k] : nullptr;
+    const bool need_l = wl2 && (k == 0 || (k == 1 ? wl : wr));
+    const bool need_r = wr2 && (k == 0 || (k == 1 ? wl : wr));
+    VPB_REQUIRE(!need_l || (x2l[k] && (reinterpret_cast<uintptr_t>(x2l[k]) & 15) == 0),
+                "x2 left halo part %d missing or not 16-byte aligned", k);
+    VPB_REQUIRE(!need_r || (x2r[k] && (reinterpret_cast<uintptr_t>(x2r[k]) & 15) == 0),
+                "x2 right halo part %d missing or not 16-byte aligned", k);
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (wv1 == nullptr) {
+    const XDensity none{nullptr, nullptr, nullptr, nullptr, {}, {}};
+    VPB_XPLANE_SWITCH(order, rc = (launch_xcomp<PP, false, true>(
+                                 src, dst, dims, dims[2] * dims[3], xcomp_whole_field(dims, PP),
+                                 k1, q1, alpha1, k2, q2, alpha2, flag, none, 0, st, nullptr, sx)));
+    return rc;
+  }
+  VPB_REQUIRE(rc_out != nullptr && stats != nullptr, "null pointer");
+  const int64_t cc = (dims[0] / order) * (dims[1] / order);
+  const int64_t len = vpb_dg_xstencil_density_work_len(dims, order, wl, wr);
+  VPB_REQUIRE(len > 0, "cannot plan the x-plane launch");
+  const int64_t nblk = len / (cc + 1);
+  XDensity dn;
+  rc = xdensity_setup(&dn, order, wv1, wv2, mid_host, wcell1_host, wcell2_host, work, nblk, cc);
+  if (rc) return rc;
+  int64_t used = 0;
   VPB_XPLANE_SWITCH(order, rc = (launch_xcomp<PP, true, true>(
                                src, dst, dims, dims[2] * dims[3], xcomp_whole_field(dims, PP), k1,
                                q1, alpha1, k2, q2, alpha2, flag, dn, 0, st, &used, sx)));

@@ -126,6 +126,10 @@ def halo_widths(q: np.ndarray) -> tuple[int, int]:
 # sender's last cells, sent to its right neighbour); "R" its RIGHT halo.
 KIND_L, KIND_R = 0, 1
 KIND_A2A = 2  # all-to-all reshard chunks (one per peer pair)
+# x2 halos of the x1 x x2 stencil pass: receiver's left / right x2 halo, parts
+# 0 (x1 dofs), 1 (their left x1 halo cells), 2 (their right x1 halo cells)
+KIND_X2L = (10, 11, 12)
+KIND_X2R = (13, 14, 15)
 
 
 class TorchComm:
@@ -329,6 +333,29 @@ class CudaOps:
             *head, wv1.data_ptr(), wv2.data_ptr(), mid.ctypes.data, wc1.ctypes.data,
             wc2.ctypes.data, volume, work.data_ptr(), rc_out.data_ptr(), stats.data_ptr(),
             self._device.stream()), "vpb_dg_sweep_xstencil_density")
+
+    def xstencil2(self, src, dst, dims, order, k1, t1, k2, t2, qmul, hl, wl, hr, wr, wl2, x2l,
+                  wr2, x2r, flag, dens=None):
+        """The stencil pass of an x1 x x2 shard (vpb_dg_sweep_xstencil2): x2l /
+        x2r = (x1 dofs, left x1 halo, right x1 halo) of the x2 halo cells."""
+        import ctypes
+
+        L = self._lib
+        ptrs = lambda parts, w: (ctypes.c_void_p * 3)(*[  # noqa: E731
+            t.data_ptr() if (w and t is not None and t.numel()) else None for t in parts])
+        if dens is not None:
+            wv1, wv2, mid, wc1, wc2, volume, work, rc_out, stats = dens
+            tail = (wv1.data_ptr(), wv2.data_ptr(), mid.ctypes.data, wc1.ctypes.data,
+                    wc2.ctypes.data, volume, work.data_ptr(), rc_out.data_ptr(),
+                    stats.data_ptr())
+        else:
+            tail = (None,) * 5 + (0.0,) + (None,) * 3
+        L.check(self.lib.vpb_dg_sweep_xstencil2(
+            src.data_ptr(), dst.data_ptr(), L.dims(dims), order, k1.data_ptr(), t1.q.data_ptr(),
+            t1.alpha.data_ptr(), k2.data_ptr(), t2.q.data_ptr(), t2.alpha.data_ptr(), qmul,
+            hl.data_ptr() if wl else None, wl, hr.data_ptr() if wr else None, wr,
+            wl2, ptrs(x2l, wl2), wr2, ptrs(x2r, wr2), flag.data_ptr(), *tail,
+            self._device.stream()), "vpb_dg_sweep_xstencil2")
 
     def xstencil_rows(self, src, dst, dims, order, v2_0, v2_rows, k1, t1, k2, t2, qmul, hl, wl,
                       hr, wr, flag, dens=None, phase=3):
@@ -692,8 +719,9 @@ class ShardedSolver:
         xcomp.cu: at most 128 local x1 cells), and -- given tau -- the
         single half step's x1 halo fitting every shard.  Otherwise advance()
         runs step() (the halo sweeps) in a loop."""
-        if not (self.dec.sharded(0) and not self.dec.sharded(1)
-                and hasattr(self.ops, "xstencil") and self.grid.ndim == 4):
+        if not (self.dec.sharded(0) and hasattr(self.ops, "xstencil") and self.grid.ndim == 4):
+            return False
+        if self.dec.sharded(1) and not hasattr(self.ops, "xstencil2"):
             return False
         p = self.order
         for r in range(self.dec.world):
@@ -707,7 +735,19 @@ class ShardedSolver:
                             for (c0, c1) in [self.dec.cells(r, 0)])
             if max(wl, wr) > cells_min:
                 return False
+            if self.dec.sharded(1) and max(self._x2_widths(tau, 1)) > self._x2_cells_min():
+                return False
         return True
+
+    def _x2_cells_min(self) -> int:
+        return min(c1 - c0 for r in range(self.dec.world) for (c0, c1) in [self.dec.cells(r, 1)])
+
+    def _x2_widths(self, tau: float, qmul: int) -> tuple[int, int]:
+        """x2 halo cells of a stencil pass on an x2-sharded field: source x2
+        cells c - Q - 2 .. c - Q, Q = qmul q2, over every v2 row."""
+        t2, _ = self.x_tables(1, tau)
+        q = qmul * np.asarray(self.ops.tables_q(t2))
+        return (max(0, int(q.max()) + 2) if q.size else 0, max(0, -int(q.min())) if q.size else 0)
 
     def _stencil_setup(self, tau: float):
         """Tables of the three-cell x passes and their x1 halo widths."""
@@ -734,6 +774,8 @@ class ShardedSolver:
         _, _, wl, wr = tabs[2]
         cells_min = min(c1 - c0 for r in range(self.dec.world)
                         for (c0, c1) in [self.dec.cells(r, 0)])
+        if self.dec.sharded(1) and max(self._x2_widths(tau, 2)) > self._x2_cells_min():
+            return False
         return max(wl, wr) <= cells_min
 
     def _density_consts(self):
@@ -787,6 +829,10 @@ class ShardedSolver:
         self._halo_bytes = getattr(self, "_halo_bytes", 0) + sum(
             8 * (m[0][2].numel() * (wl > 0) + m[1][2].numel() * (wr > 0)) for m in msgs.values())
         mid, wc1, wc2, volume = self._density_consts()
+        if self.dec.sharded(1):
+            self._x2_stencil_pass(tau, qmul, msgs, bufs, k1, t1, k2, t2, wl, wr, flag_slot,
+                                  with_density, flags_row, stats_row, rc_parts, mark)
+            return
         blocks = self._row_blocks()
         if blocks is not None:
             self._pipelined_pass(msgs, bufs, blocks, k1, t1, k2, t2, qmul, wl, wr, flag_slot,
@@ -808,6 +854,71 @@ class ShardedSolver:
                 rc_parts[r] = rc
             self.ops.xstencil(sh.f, sh.buf, sh.dims, p, k1, t1, k2, t2, qmul, recv_l, wl,
                               recv_r, wr, fl, dens)
+            sh.swap()
+
+    def _x2_stencil_pass(self, tau, qmul, msgs, bufs, k1, t1, k2, t2, wl, wr, flag_slot,
+                         with_density, flags_row, stats_row, rc_parts, mark):
+        """The stencil pass of an x1 x x2 decomposition (the 4 x 2 grid at 8
+        GPUs): the x1 halo exchange, then the x2 halo exchange of the
+        boundary cells' x1 dofs and of their x1 halo rows (the corners, from
+        the x1 halos just received), then vpb_dg_sweep_xstencil2 per shard."""
+        p = self.order
+        wl2, wr2 = self._x2_widths(tau, qmul)
+        self.comm.exchange(msgs)
+        mark("halo_x2")
+        msgs2, bufs2 = {}, {}
+        for r, sh in self.shards.items():
+            left2, right2 = self.dec.neighbours(r, 1)
+            d = sh.dims
+            n1, nx2 = d[0], d[1]
+            c2l = nx2 // p
+            planes = d[2] * d[3]
+            recv_l, recv_r = bufs[r]
+            send = {}
+            recv = {}
+            # my last wl2 cells -> right2's left halo; my first wr2 cells -> left2's right halo
+            for side, w, cell0 in (("L", wl2, c2l - wl2), ("R", wr2, 0)):
+                parts_s, parts_r = [], []
+                for k, (h, hw) in enumerate(((None, n1), (recv_l, wl * p), (recv_r, wr * p))):
+                    n = planes * w * p * hw if (w and hw) else 0
+                    sb = torch.empty(n, dtype=sh.f.dtype, device=sh.f.device)
+                    rb = torch.empty(n, dtype=sh.f.dtype, device=sh.f.device)
+                    if n:
+                        if k == 0:
+                            self.ops.pack(1, sh.f, d, p, cell0, w, sb)
+                        else:  # rows of the boundary cells in the x1 halo buffer
+                            run = w * p * hw
+                            self.ops.slab_copy(h[cell0 * p * hw:], c2l * p * hw, sb, run,
+                                               planes, run)
+                    parts_s.append(sb)
+                    parts_r.append(rb)
+                send[side], recv[side] = parts_s, parts_r
+            items = []
+            for k in range(3):
+                items.append((KIND_X2L[k], right2, send["L"][k], left2, recv["L"][k]))
+                items.append((KIND_X2R[k], left2, send["R"][k], right2, recv["R"][k]))
+            msgs2[r] = items
+            bufs2[r] = (recv["L"], recv["R"])
+        self._halo_bytes = getattr(self, "_halo_bytes", 0) + sum(
+            8 * it[2].numel() for m in msgs2.values() for it in m)
+        self.comm.exchange(msgs2)
+        mark(("sweep_x12x12" if qmul == 2 else "sweep_x12") + ("_rho" if with_density else ""))
+        mid, wc1, wc2, volume = self._density_consts()
+        for r, sh in self.shards.items():
+            recv_l, recv_r = bufs[r]
+            x2l, x2r = bufs2[r]
+            fl = flags_row[r][flag_slot:flag_slot + 1]
+            dens = None
+            if with_density:
+                d = sh.dims
+                work = torch.empty(self.ops.xstencil_work(d, p, wl, wr), dtype=torch.float64,
+                                   device=sh.f.device)
+                rc = torch.empty((d[1] // p) * (d[0] // p), dtype=torch.float64,
+                                 device=sh.f.device)
+                dens = (self.wv1, self.wv2, mid, wc1, wc2, volume, work, rc, stats_row[r])
+                rc_parts[r] = rc
+            self.ops.xstencil2(sh.f, sh.buf, sh.dims, p, k1, t1, k2, t2, qmul, recv_l, wl,
+                               recv_r, wr, wl2, x2l, wr2, x2r, fl, dens)
             sh.swap()
 
     def _row_blocks(self):
@@ -866,11 +977,11 @@ class ShardedSolver:
             sh.swap()
 
     def _gather_rc(self, rc_parts: dict) -> torch.Tensor:
-        """Shard cell-centre density slabs [C2][C1 local] -> full [C2][C1]."""
+        """Shard cell-centre density slabs [C2 local][C1 local] -> full [C2][C1]."""
         p = self.order
         C1, C2 = self.n1 // p, self.n2 // p
-        m = max((b0 - a0) * C2 for r in range(self.dec.world)
-                for (a0, b0) in [self.dec.cells(r, 0)])
+        m = max((b0 - a0) * (b1 - a1) for r in range(self.dec.world)
+                for (a0, b0), (a1, b1) in [(self.dec.cells(r, 0), self.dec.cells(r, 1))])
         locs = {}
         for r, rc in rc_parts.items():
             pad = torch.zeros(m, dtype=torch.float64, device=rc.device)
@@ -880,7 +991,8 @@ class ShardedSolver:
         full = torch.empty((C2, C1), dtype=torch.float64, device=self.device)
         for r, part in enumerate(parts):
             a0, b0 = self.dec.cells(r, 0)
-            full[:, a0:b0] = part[: (b0 - a0) * C2].view(C2, b0 - a0)
+            a1, b1 = self.dec.cells(r, 1)
+            full[a1:b1, a0:b0] = part[: (b0 - a0) * (b1 - a1)].view(b1 - a1, b0 - a0)
         return full.view(-1)
 
     def advance(self, tau: float, nsteps: int, first_step: int | None = None,

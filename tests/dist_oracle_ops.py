@@ -205,6 +205,59 @@ class NumpyOps:
             mean = np.einsum("aibjvw,i,j,v,w->", o, wc1, wc2, wa, wb, optimize=False)
             stats[0] = float(mean) / volume
 
+    def xstencil2(self, src, dst, dims, order, k1, t1, k2, t2, qmul, hl, wl, hr, wr, wl2, x2l,
+                  wr2, x2r, flag, dens=None):
+        """x1 x x2 shard: the extended box [x2 halo | rows | x2 halo] x [x1
+        halo | x1 | x1 halo] (corners from the x2 halos' x1 parts), x1
+        stencil on every row of it, then the x2 stencil without wrap."""
+        p = order
+        n1, n2, nv1, nv2 = dims
+        c1n, c2n = n1 // p, n2 // p
+
+        def row_block(own, l, r, rows):
+            parts = []
+            if wl:
+                parts.append(_box(l, (wl * p, rows, nv1, nv2)))
+            parts.append(_box(own, (n1, rows, nv1, nv2)))
+            if wr:
+                parts.append(_box(r, (wr * p, rows, nv1, nv2)))
+            return np.concatenate(parts, axis=0)
+
+        blocks = []
+        if wl2:
+            blocks.append(row_block(x2l[0], x2l[1], x2l[2], wl2 * p))
+        blocks.append(row_block(src, hl, hr, n2))
+        if wr2:
+            blocks.append(row_block(x2r[0], x2r[1], x2r[2], wr2 * p))
+        ext = np.concatenate(blocks, axis=1)  # (x1 ext, x2 ext, v1, v2)
+        c2e = wl2 + c2n + wr2
+        ext = ext.reshape(wl + c1n + wr, p, c2e * p, nv1, nv2)
+        g = np.zeros((c1n, p, c2e * p, nv1, nv2))
+        for iv1 in range(nv1):
+            qq = qmul * int(t1.q[iv1])
+            for k in range(3):
+                j = np.arange(c1n) - qq - 2 + k + wl
+                g[:, :, :, iv1, :] += np.einsum("jm,cmxv->cjxv", k1[iv1, k],
+                                                ext[:, :, :, iv1, :][j], optimize=False)
+        g2 = g.reshape(c1n, p, c2e, p, nv1, nv2)
+        o = np.zeros((c1n, p, c2n, p, nv1, nv2))
+        for iv2 in range(nv2):
+            qq = qmul * int(t2.q[iv2])
+            for k in range(3):
+                j = np.arange(c2n) - qq - 2 + k + wl2
+                assert j.min() >= 0 and j.max() < c2e, "x2 halo too narrow"
+                o[..., iv2] += np.einsum("jm,aibmv->aibjv", k2[iv2, k],
+                                         g2[..., iv2][:, :, j], optimize=False)
+        out = o.reshape(n1, n2, nv1, nv2)
+        self._store(dst, dims, out, flag)
+        if dens is not None:
+            wv1, wv2, mid, wc1, wc2, volume, work, rc_out, stats = dens
+            wa, wb = wv1.numpy(), wv2.numpy()
+            rc = np.einsum("aibjvw,i,j,v,w->ba", o, mid, mid, wa, wb, optimize=False)
+            rc_out.copy_(torch.from_numpy(np.ascontiguousarray(rc).reshape(-1)))
+            mean = np.einsum("aibjvw,i,j,v,w->", o, wc1, wc2, wa, wb, optimize=False)
+            stats[0] = float(mean) / volume
+
     def xstencil_rows(self, src, dst, dims, order, v2_0, v2_rows, k1, t1, k2, t2, qmul, hl, wl,
                       hr, wr, flag, dens=None, phase=3):
         """One block of v2 rows of the pipelined pass: the whole-shard pass

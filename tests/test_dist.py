@@ -121,6 +121,32 @@ def test_virtual_sharded_advance_matches_oracle_steps(p1, tau):
     assert max_rel(solver.gather(), f) <= 1e-13
 
 
+@pytest.mark.parametrize("p1,p2,tau", [(2, 2, TAU), (4, 2, TAU), (2, 3, 0.25)])
+def test_virtual_sharded_advance_x1x2_matches_oracle_steps(p1, p2, tau):
+    """x1 x x2 process grids (the 4 x 2 layout at 8 GPUs): advance() runs the
+    stencil passes with x1 halos, then x2 halos carrying the corner cells
+    (vpb_dg_sweep_xstencil2; oracle restatement), against oracle steps."""
+    calls = []
+
+    class Counting(NumpyOps):
+        def xstencil2(self, *a, **k):
+            calls.append(a[8])  # qmul
+            return super().xstencil2(*a, **k)
+
+    grid, og = grids()
+    dec = dist.Decomposition(grid, p1, p2)
+    solver = dist.ShardedSolver(grid, dec, dist.VirtualComm(dec.world), range(dec.world),
+                                ops=Counting(), device=torch.device("cpu"))
+    assert solver._stencil_ready(tau)
+    solver.scatter(core.initialize(PROB, og))
+    solver.advance(tau, 3)
+    assert calls, "the x1 x x2 stencil path did not run"
+    f = core.initialize(PROB, og)
+    for _ in range(3):
+        f = core.strang_step(f, og, tau)
+    assert max_rel(solver.gather(), f) <= 1e-13
+
+
 @pytest.mark.parametrize("blocks", [2, 3, 100])
 def test_pipelined_halo_blocks_match_one_exchange(blocks):
     """advance() with the halo exchange and stencil pass pipelined in blocks
@@ -200,6 +226,42 @@ def test_two_rank_gloo_sharded_advance_equals_in_process(tmp_path):
     solver.scatter(core.initialize(PROB, og))
     solver.advance(TAU, 3)
     for r in range(2):
+        assert np.array_equal(np.load(tmp_path / f"a{r}.npy"), solver.local_logical(r))
+
+
+def _advance2d_worker(rank, world, port, p1, p2, outdir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as tdist
+
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        grid, og = grids()
+        dec = dist.Decomposition(grid, p1, p2)
+        solver = dist.ShardedSolver(grid, dec, dist.TorchComm(), [rank], ops=NumpyOps(),
+                                    device=torch.device("cpu"))
+        assert solver._stencil_ready(TAU)
+        solver.scatter(core.initialize(PROB, og))
+        solver.advance(TAU, 3)
+        np.save(os.path.join(outdir, f"a{rank}.npy"), solver.local_logical(rank))
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_four_rank_gloo_x1x2_advance_equals_in_process(tmp_path):
+    """2 x 2 process grid over gloo: the x1 then x2 halo exchanges of the
+    stencil passes (6 x2 messages per rank, corners included) through
+    TorchComm == the in-process VirtualComm run."""
+    port = _free_port()
+    mp.start_processes(_advance2d_worker, args=(4, port, 2, 2, str(tmp_path)), nprocs=4,
+                       join=True, start_method="spawn")
+    grid, og = grids()
+    dec = dist.Decomposition(grid, 2, 2)
+    solver = dist.ShardedSolver(grid, dec, dist.VirtualComm(4), range(4), ops=NumpyOps(),
+                                device=torch.device("cpu"))
+    solver.scatter(core.initialize(PROB, og))
+    solver.advance(TAU, 3)
+    for r in range(4):
         assert np.array_equal(np.load(tmp_path / f"a{r}.npy"), solver.local_logical(r))
 
 

@@ -73,6 +73,28 @@ def test_sharded_advance_with_merged_stencil_passes_matches_single_gpu(p1, tau):
         assert got[k] == pytest.approx(getattr(rec, k), rel=1e-12), k
 
 
+@pytest.mark.parametrize("p1,p2,tau", [(2, 2, TAU), (4, 2, TAU), (4, 2, 1.7), (4, 3, TAU),
+                                        (2, 2, 0.0)])
+def test_sharded_advance_x1x2_stencil_passes_match_single_gpu(p1, p2, tau):
+    """x1 x x2 process grids (the north-star 4 x 2 layout at 8 GPUs):
+    advance() runs vpb_dg_sweep_xstencil2 -- x1 halos, then x2 halos with
+    the corner cells -- with the density epilogue, against the single-GPU
+    advance() ("fast" arithmetic)."""
+    prob, grid, solver, f0 = setup(p1, p2)
+    assert solver._stencil_ready(tau)
+    calls = []
+    orig = solver.ops.xstencil2
+    solver.ops.xstencil2 = lambda *a, **k: (calls.append(1), orig(*a, **k))[1]
+    solver.advance(tau, 4)
+    assert calls
+    f = vpb.advance(f0, tau, 4)
+    assert max_rel(solver.gather(), f.numpy()) <= 1e-13
+    got = solver.diagnostics(4 * tau)
+    rec = vpb.diagnostics(f, 4 * tau)
+    for k in ("mass", "l1_norm", "l2_norm", "kinetic_energy", "electric_energy"):
+        assert got[k] == pytest.approx(getattr(rec, k), rel=1e-12), k
+
+
 @pytest.mark.parametrize("p1", [3, 5])
 def test_sharded_advance_uneven_split_falls_back_to_halo_sweeps(p1):
     """Uneven x1 splits (16 cells over 3 or 5 ranks: shards of 5-6 / 3-4
