@@ -36,6 +36,8 @@ def main() -> None:
     ap.add_argument("--worlds", type=int, nargs="+", default=[1, 2, 4, 8])
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--vshard", action="store_true", help="v2-slab sharding (see doc)")
+    ap.add_argument("--grid2d", default=None,
+                    help="x-sharded process grid P1xP2 (e.g. 4x2): one run of that layout")
     args = ap.parse_args()
     import gc
 
@@ -49,6 +51,32 @@ def main() -> None:
     problem = vpb.problem_spec(prob)
     grid = vpb.make_grid(problem, "dg", dofs, dg_order=order)
     N = grid.total_dof
+    if args.grid2d:
+        p1, p2 = (int(x) for x in args.grid2d.split("x"))
+        w = p1 * p2
+        dec = dist.Decomposition(grid, p1, p2)
+        solver = dist.ShardedSolver(grid, dec, dist.VirtualComm(w), range(w))
+        solver.initialize(problem)
+        ready = solver._stencil_ready(tau)
+        merged = ready and solver._merged_halo_fits(tau)
+        solver.advance(tau, 2)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        solver._halo_bytes = 0
+        e0.record()
+        solver.advance(tau, args.steps)
+        e1.record()
+        torch.cuda.synchronize()
+        per_rank = e0.elapsed_time(e1) / args.steps / w
+        print(json.dumps({"config": args.config, "world": w, "layout": f"x1 x x2 {p1}x{p2}",
+                          "stencil_passes": ready, "merged_pass": merged,
+                          "per_rank_compute_ms_per_step": per_rank,
+                          "projected_dof_per_s_compute_only": N / (per_rank * 1e-3),
+                          "halo_bytes_per_rank_per_step": int(solver._halo_bytes
+                                                              / args.steps / w),
+                          "cells_per_shard": [grid.axes[0].count // p1,
+                                              grid.axes[1].count // p2]}), flush=True)
+        return
     for w in args.worlds:
         if args.vshard:
             solver = dist.VShardedSolver(grid, dist.VirtualComm(w), range(w), w)
