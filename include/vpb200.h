@@ -261,6 +261,21 @@ int vpb_dg_sweep_xstencil_rows(const double* src, double* dst, const int64_t dim
                                const double* wcell2_host, double volume, double* work,
                                double* rc_out, double* stats, int32_t phase, void* stream);
 
+/* The merged x pass with the density epilogue (vpb_dg_sweep_xcomp_density)
+ * on v2 rows [v2_0, v2_0 + v2_rows) of a field not sharded in x (a velocity
+ * shard); tables indexed by the field's v2 row.  The work buffer
+ * (vpb_dg_xcomp_density_work_len of `dims`) accumulates over the calls of
+ * one pass: phase bit 1 (first call) zeroes it, bit 2 (last) reduces it to
+ * rc_out / stats. */
+int vpb_dg_sweep_xcomp_rows(const double* src, double* dst, const int64_t dims[4], int32_t order,
+                            int64_t v2_0, int64_t v2_rows, const double* k1, const int64_t* q1,
+                            const double* alpha1, const double* k2, const int64_t* q2,
+                            const double* alpha2, int32_t* flag, const double* wv1,
+                            const double* wv2, const double* mid_host,
+                            const double* wcell1_host, const double* wcell2_host, double volume,
+                            double* work, double* rc_out, double* stats, int32_t phase,
+                            void* stream);
+
 /* The stencil pass on an x1 x x2 sharded field (the 4 x 2 process grid of
  * dist.ShardedSolver): x1 halos hl / hr as for vpb_dg_sweep_xstencil, and the
  * plane is not periodic in x2 either -- source x2 cells -wl2..-1 and

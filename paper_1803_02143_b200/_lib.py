@@ -101,6 +101,10 @@ SIGNATURES = {
                                       + [c_void_p] * 6
                                       + [c_int32, c_void_p, c_int32, c_void_p, c_int32]
                                       + [c_void_p] * 6 + [c_double] + [c_void_p] * 4),
+    "vpb_dg_sweep_xcomp_rows": (c_int, [c_void_p, c_void_p, POINTER(c_int64), c_int32,
+                                        c_int64, c_int64] + [c_void_p] * 6
+                                + [c_void_p] * 6 + [c_double] + [c_void_p] * 3
+                                + [c_int32, c_void_p]),
     "vpb_dg_sweep_xstencil2": (c_int, [c_void_p, c_void_p, POINTER(c_int64), c_int32]
                                + [c_void_p] * 6
                                + [c_int32, c_void_p, c_int32, c_void_p, c_int32]

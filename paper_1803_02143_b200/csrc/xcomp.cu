@@ -907,6 +907,52 @@ extern "C" int vpb_dg_sweep_xstencil_density(
   return launch_xdens_reduce(work, nblk, cc, volume, rc_out, stats, st);
 }
 
+// The merged x pass (composed stencils, density epilogue) on v2 rows
+// [v2_0, v2_0 + v2_rows) of an unsharded-in-x field (a velocity shard,
+// dist.VShardedSolver): the rows of one call are contiguous in src / dst;
+// k2 / q2 / alpha2 are indexed by the field's v2 row.  The CTA slabs of the
+// work buffer accumulate over the calls of one pass: phase bit 1 (first
+// call) zeroes them, bit 2 (last call) reduces them to rc_out / stats --
+// one reduction for the boundary-first blocks of the velocity-sharded step.
+extern "C" int vpb_dg_sweep_xcomp_rows(
+    const double* src, double* dst, const int64_t dims[4], int32_t order, int64_t v2_0,
+    int64_t v2_rows, const double* k1, const int64_t* q1, const double* alpha1, const double* k2,
+    const int64_t* q2, const double* alpha2, int32_t* flag, const double* wv1, const double* wv2,
+    const double* mid_host, const double* wcell1_host, const double* wcell2_host, double volume,
+    double* work, double* rc_out, double* stats, int32_t phase, void* stream) {
+  int rc = xplane_args_ok(src, dst, dims, order);
+  if (rc) return rc;
+  VPB_REQUIRE(k1 && q1 && alpha1 && k2 && q2 && alpha2 && rc_out && stats, "null pointer");
+  VPB_REQUIRE(v2_0 >= 0 && v2_rows >= 0 && v2_0 + v2_rows <= dims[3], "v2 rows outside the field");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t plane = dims[0] * dims[1];
+  const int64_t C2 = dims[1] / order;
+  const int64_t cc = (dims[0] / order) * C2;
+  const int64_t len = vpb_dg_xcomp_density_work_len(dims, order);
+  VPB_REQUIRE(len > 0, "cannot plan the composed x pass");
+  const int64_t nblk = len / (cc + 1);
+  XDensity dn;
+  rc = xdensity_setup(&dn, order, wv1, wv2, mid_host, wcell1_host, wcell2_host, work, nblk, cc);
+  if (rc) return rc;
+  if (phase & 1) {
+    if (cudaMemsetAsync(work, 0, (size_t)len * sizeof(double), st) != cudaSuccess)
+      return check_launch("cudaMemsetAsync");
+  }
+  const int64_t nitems = v2_rows * dims[2];
+  if (nitems) {
+    const XcMap mp{dims[2], 0, v2_0, dims[2], 1, (int)C2};
+    int64_t used = 0;
+    VPB_XPLANE_SWITCH(order, rc = (launch_xcomp<PP, true, false>(
+                                 src + v2_0 * dims[2] * plane, dst, dims, nitems, mp, k1, q1,
+                                 alpha1, k2, q2, alpha2, flag, dn, 1, st, &used)));
+    if (rc) return rc;
+    VPB_REQUIRE(used <= nblk, "x-plane launch plan exceeds the work buffer (%lld > %lld CTAs)",
+                (long long)used, (long long)nblk);
+  }
+  if (phase & 2) return launch_xdens_reduce(work, nblk, cc, volume, rc_out, stats, st);
+  return VPB_OK;
+}
+
 // The stencil pass on an x1 x x2 sharded field: x1 halos as above and x2
 // halos (x2l / x2r, three parts each, see XcStencil) of wl2 / wr2 cells; the
 // plane is not periodic in x2.  wv1 == nullptr: no density epilogue.

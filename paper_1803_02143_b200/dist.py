@@ -334,6 +334,21 @@ class CudaOps:
             wc2.ctypes.data, volume, work.data_ptr(), rc_out.data_ptr(), stats.data_ptr(),
             self._device.stream()), "vpb_dg_sweep_xstencil_density")
 
+    def xcomp_rows(self, src, dst, dims, order, v2_0, v2_rows, t1, t2, flag, dens, phase):
+        """Merged x pass with the density epilogue on v2 rows [v2_0, v2_0 +
+        v2_rows) of a shard (vpb_dg_sweep_xcomp_rows; t2 rows = the shard's
+        rows); the density accumulates over the calls of one pass (phase bit
+        1: first call, bit 2: last call, which reduces into rc / stats)."""
+        L = self._lib
+        wv1, wv2, mid, wc1, wc2, volume, work, rc_out, stats = dens
+        L.check(self.lib.vpb_dg_sweep_xcomp_rows(
+            src.data_ptr(), dst.data_ptr(), L.dims(dims), order, int(v2_0), int(v2_rows),
+            t1.composed().data_ptr(), t1.q.data_ptr(), t1.alpha.data_ptr(),
+            t2.composed().data_ptr(), t2.q.data_ptr(), t2.alpha.data_ptr(), flag.data_ptr(),
+            wv1.data_ptr(), wv2.data_ptr(), mid.ctypes.data, wc1.ctypes.data, wc2.ctypes.data,
+            volume, work.data_ptr(), rc_out.data_ptr(), stats.data_ptr(), int(phase),
+            self._device.stream()), "vpb_dg_sweep_xcomp_rows")
+
     def xstencil2(self, src, dst, dims, order, k1, t1, k2, t2, qmul, hl, wl, hr, wr, wl2, x2l,
                   wr2, x2r, flag, dens=None):
         """The stencil pass of an x1 x x2 shard (vpb_dg_sweep_xstencil2): x2l /
@@ -1360,6 +1375,17 @@ class SplineShardedSolver:
 KIND_VL, KIND_VR = 3, 4  # v2 halo messages: receiver's left / right halo
 
 
+class _RowsTab:
+    """Rows [r0, r1) of x2 tables, composed form included (views, no copy)."""
+
+    def __init__(self, t, r0: int, r1: int):
+        self.t, self.r0, self.r1 = t, r0, r1
+        self.q, self.alpha = t.q[r0:r1], t.alpha[r0:r1]
+
+    def composed(self):
+        return self.t.composed()[self.r0:self.r1]
+
+
 class VShardedSolver:
     """Strang steps of a 2x2v dG field split along v2 over W ranks.
 
@@ -1584,6 +1610,32 @@ class VShardedSolver:
             c0, c1 = self.cr[r]
             nl = c1 - c0
             blocks[r] = [(0, H), (nl - H, nl), (H, nl - H)] if split else [(0, nl)]
+        # merged pass with the density: the blocks of a shard accumulate into
+        # one set of CTA slabs (vpb_dg_sweep_xcomp_rows), one reduction
+        rows_dens = feeds_v and qmul == 2 and hasattr(self.ops, "xcomp_rows")
+        if rows_dens:
+            nb = len(blocks[self.ranks[0]])
+            acc = {}
+            for r in self.ranks:
+                c0, c1 = self.cr[r]
+                d = self.dims(r)
+                work = torch.empty(self.ops.xpass_work(d, p, 2), dtype=torch.float64,
+                                   device=self.device)
+                rc = torch.empty((self.n1 // p) * (self.n2 // p), dtype=torch.float64,
+                                 device=self.device)
+                st = torch.zeros(4, dtype=torch.float64, device=self.device)
+                wv2 = self.wv2[c0 * p:c1 * p].contiguous()
+                acc[r] = ((self.wv1, wv2, mid, wc1, wc2, volume, work, rc, st),
+                          _RowsTab(t2, c0 * p, c1 * p), [0])
+                parts[r].append((rc, st))
+
+            def run(r, a, b, with_dens, parts_r):  # noqa: F811 -- the accumulating form
+                dens, t2r, count = acc[r]
+                count[0] += 1
+                phase = (1 if count[0] == 1 else 0) | (2 if count[0] == nb else 0)
+                f1, _ = fl[r]
+                self.ops.xcomp_rows(self.local(self.f[r], r), self.local(self.buf[r], r),
+                                    self.dims(r), p, a * p, (b - a) * p, t1, t2r, f1, dens, phase)
         for r in self.ranks:
             for a, b in (blocks[r][:2] if split else blocks[r]):
                 run(r, a, b, feeds_v, parts[r])

@@ -130,6 +130,25 @@ class NumpyOps:
             mean = np.einsum("aibjvw,i,j,v,w->", o, wc1, wc2, wa, wb, optimize=False)
             stats[0] = float(mean) / volume
 
+    def xcomp_rows(self, src, dst, dims, order, v2_0, v2_rows, t1, t2r, flag, dens, phase):
+        """Merged pass on v2 rows [v2_0, v2_0 + v2_rows) of a shard (t2r: the
+        shard's rows of the global tables) with the density accumulated over
+        the calls of one pass (phase bit 1: reset, bit 2: last)."""
+        wv1, wv2, mid, wc1, wc2, volume, work, rc_out, stats = dens
+        n1, n2, nv1, _ = dims
+        plane = n1 * n2 * nv1
+        sub = (n1, n2, nv1, v2_rows)
+        a, b = v2_0 * plane, (v2_0 + v2_rows) * plane
+        rc_b = torch.empty_like(rc_out)
+        st_b = torch.zeros_like(stats)
+        self.xpass_rows(src[a:b], dst[a:b], sub, order, t1, t2r.t, t2r.r0 + v2_0, 2, flag, None,
+                        (wv1, wv2[v2_0:v2_0 + v2_rows], mid, wc1, wc2, volume, work, rc_b, st_b))
+        if phase & 1:
+            rc_out.zero_()
+            stats[0] = 0.0
+        rc_out += rc_b
+        stats[0] += st_b[0]
+
     def vplane_v2halo(self, src_ext, dst, dims, order, c2e, off, t1, t2, f1, f2, hflag):
         """v1 then v2 sweep of [halo | slab | halo]: swept periodically over
         the extended rows (whose wrap-around only reaches discarded cells when
