@@ -1579,8 +1579,9 @@ class VShardedSolver:
                                                                else ""))
         feeds_v = rc_parts is not None
 
-        def run(r, a, b, with_dens, parts):
-            """x pass on the shard's v2 cells [a, b) (local numbering)."""
+        def run_block(r, a, b, with_dens, parts):
+            """x pass on the shard's v2 cells [a, b) (local numbering), its own
+            density partial appended to parts."""
             c0, _ = self.cr[r]
             d = (self.n1, self.n2, self.nv1, (b - a) * p)
             off = a * p * self.row
@@ -1610,35 +1611,39 @@ class VShardedSolver:
             c0, c1 = self.cr[r]
             nl = c1 - c0
             blocks[r] = [(0, H), (nl - H, nl), (H, nl - H)] if split else [(0, nl)]
-        # merged pass with the density: the blocks of a shard accumulate into
-        # one set of CTA slabs (vpb_dg_sweep_xcomp_rows), one reduction
-        rows_dens = feeds_v and qmul == 2 and hasattr(self.ops, "xcomp_rows")
-        if rows_dens:
-            nb = len(blocks[self.ranks[0]])
-            acc = {}
+        # the merged pass with the density: the blocks of a shard accumulate
+        # into one set of CTA slabs (vpb_dg_sweep_xcomp_rows), one reduction
+        acc = {}
+        if feeds_v and qmul == 2 and hasattr(self.ops, "xcomp_rows"):
             for r in self.ranks:
                 c0, c1 = self.cr[r]
-                d = self.dims(r)
-                work = torch.empty(self.ops.xpass_work(d, p, 2), dtype=torch.float64,
-                                   device=self.device)
+                work = torch.empty(self.ops.xpass_work(self.dims(r), p, 2),
+                                   dtype=torch.float64, device=self.device)
                 rc = torch.empty((self.n1 // p) * (self.n2 // p), dtype=torch.float64,
                                  device=self.device)
                 st = torch.zeros(4, dtype=torch.float64, device=self.device)
                 wv2 = self.wv2[c0 * p:c1 * p].contiguous()
                 acc[r] = ((self.wv1, wv2, mid, wc1, wc2, volume, work, rc, st),
-                          _RowsTab(t2, c0 * p, c1 * p), [0])
+                          _RowsTab(t2, c0 * p, c1 * p), [0, len(blocks[r])])
                 parts[r].append((rc, st))
 
-            def run(r, a, b, with_dens, parts_r):  # noqa: F811 -- the accumulating form
-                dens, t2r, count = acc[r]
-                count[0] += 1
-                phase = (1 if count[0] == 1 else 0) | (2 if count[0] == nb else 0)
-                f1, _ = fl[r]
-                self.ops.xcomp_rows(self.local(self.f[r], r), self.local(self.buf[r], r),
-                                    self.dims(r), p, a * p, (b - a) * p, t1, t2r, f1, dens, phase)
+        def run_block_acc(r, a, b):
+            dens, t2r, count = acc[r]
+            count[0] += 1
+            phase = (1 if count[0] == 1 else 0) | (2 if count[0] == count[1] else 0)
+            self.ops.xcomp_rows(self.local(self.f[r], r), self.local(self.buf[r], r),
+                                self.dims(r), p, a * p, (b - a) * p, t1, t2r, fl[r][0], dens,
+                                phase)
+
+        def run(r, a, b, with_dens):
+            if acc:
+                run_block_acc(r, a, b)
+            else:
+                run_block(r, a, b, with_dens, parts[r])
+
         for r in self.ranks:
             for a, b in (blocks[r][:2] if split else blocks[r]):
-                run(r, a, b, feeds_v, parts[r])
+                run(r, a, b, feeds_v)
         reqs = []
         if feeds_v and not self.peer_halos:
             # the boundary cells of the new state are in buf: send them now
@@ -1647,7 +1652,7 @@ class VShardedSolver:
         if split:
             for r in self.ranks:
                 a, b = blocks[r][2]
-                run(r, a, b, True, parts[r])
+                run(r, a, b, True)
         if feeds_v:
             for r in self.ranks:  # fixed order: left block, right block, interior
                 rc = parts[r][0][0].clone()
