@@ -338,6 +338,19 @@ int vpb_spline_sweep_axis2(int32_t axis, const double* src, double* dst, const i
                            const double* values, double scale, double h, int32_t* flag,
                            void* stream);
 
+/* The x1 (contiguous axis) double sweep of vpb_spline_sweep_axis2 with the
+ * density of its output as an epilogue (compute_density, poisson.py:85-95,
+ * fused into the merged x half steps; the x2 double sweep runs first, the
+ * two commute): part[((iv2*(nv1/32) + b)*n2 + ix2)*n1 + ix1] = sum over the
+ * 32 v1 rows of block b of out * wv1[iv1], in row order.  vpb_density over
+ * dims {n1, n2, nv1/32, nv2} with unit v1 weights and wv2 reduces part to rho.
+ * Needs nv1 % 32 == 0, n1 % 8 == 0, n1 >= 64, 16-byte aligned buffers;
+ * vpb_spline_density_part_len(dims) doubles of part (0: unsupported). */
+int64_t vpb_spline_density_part_len(const int64_t dims[4]);
+int vpb_spline_sweep_x1dbl_density(const double* src, double* dst, const int64_t dims[4],
+                                   const double* values, double scale, double h, int32_t* flag,
+                                   const double* wv1, double* part, void* stream);
+
 /* rho[ix2*n1+ix1] = sum_v f * wv1[iv1] * wv2[iv2].  work: vpb_density_work_len doubles. */
 int64_t vpb_density_work_len(const int64_t dims[4]);
 int vpb_density(const double* f, const int64_t dims[4], const double* wv1, const double* wv2,

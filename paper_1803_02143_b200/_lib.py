@@ -127,6 +127,10 @@ SIGNATURES = {
                                       c_double, c_double, c_void_p, c_void_p]),
     "vpb_spline_sweep_axis2": (c_int, [c_int32, c_void_p, c_void_p, POINTER(c_int64), c_void_p,
                                        c_double, c_double, c_void_p, c_void_p]),
+    "vpb_spline_density_part_len": (c_int64, [POINTER(c_int64)]),
+    "vpb_spline_sweep_x1dbl_density": (c_int, [c_void_p, c_void_p, POINTER(c_int64), c_void_p,
+                                               c_double, c_double, c_void_p, c_void_p, c_void_p,
+                                               c_void_p]),
     "vpb_density_work_len": (c_int64, [POINTER(c_int64)]),
     "vpb_density": (c_int, [c_void_p, POINTER(c_int64), c_void_p, c_void_p, c_void_p, c_void_p,
                             c_void_p]),

@@ -164,6 +164,13 @@ struct SplineTileArgs {
   int use_tma;  // strided tiles: one TMA tensor copy per tile (tmap valid)
   int iir;      // fast path: recursive filters (n % 8 == 0, n >= 32) instead of PCR
   int dbl;      // two consecutive sweeps with the same shift in one pass (see below)
+  // density epilogue of the contiguous (x1) double sweep: a tile's 32 lines
+  // are 32 consecutive v1 rows at one (v2, x2) (line = ((iv2 nv1 + iv1) n2 +
+  // ix2)), and part[((iv2 (nv1/32) + blk) n2 + ix2) n + k] = sum over the
+  // tile's lines of out * w1[iv1] (fixed order); nullptr = no epilogue
+  double* part;
+  const double* pw1;
+  int64_t pn2, pnv1;
 };
 
 // Two sweeps by the same shift (the closing and opening x half steps of
@@ -284,16 +291,22 @@ __device__ __forceinline__ void iir_solve(double* y, const int YS, const int n, 
   }
 }
 
+constexpr int kDblWarm = 40;  // warm-up points of the double recursion (multiple of 8)
+
 // Two recursive-filter solves (the double sweep's (6 T^-1)^2 up to the gain)
 // in one causal and one anticausal pass: y1 <- u + z1 y1, y2 <- y1 + z1 y2
 // advance together, so every point is loaded and stored once per direction
-// and the two chains overlap.  The periodic start values come from a 64-point
-// warm-up over the wrapping end (y1 needs 32 terms, y2 32 terms of an
-// accurate y1: z1^32 ~ 5e-19).  Requires n >= 64 (else two iir_solve calls).
+// and the two chains overlap.  The periodic start values come from a
+// kDblWarm-point warm-up over the wrapping end: started J points back, the
+// pair of recursions computes exactly the truncated sums y1 = sum_{j<J} z1^j
+// u_{-j} and y2 = sum_{j<J} (j+1) z1^j u_{-j}, whose tails are below
+// (J+1) z1^J / (1-z1)^2 ~ 1e-21 of max|u| at J = 40 (z1^40 = 1.3e-23; the
+// round-1 warm-up of 64 points was 24 points longer than needed).
+// Requires n >= 64 (else two iir_solve calls).
 __device__ __forceinline__ void iir_solve2(double* y, const int YS, const int n, const double z1) {
   constexpr int U = 8;
   double p1 = 0.0, p2 = 0.0;
-  for (int k = n - 64; k < n; k += U) {
+  for (int k = n - kDblWarm; k < n; k += U) {
     double u[U];
 #pragma unroll
     for (int r = 0; r < U; ++r) u[r] = y[(k + r) * YS];
@@ -317,7 +330,7 @@ __device__ __forceinline__ void iir_solve2(double* y, const int YS, const int n,
     for (int r = 0; r < U; ++r) y[(k + r) * YS] = u[r];
   }
   double q1 = 0.0, q2 = 0.0;
-  for (int k = 64 - U; k >= 0; k -= U) {
+  for (int k = kDblWarm - U; k >= 0; k -= U) {
     double u[U];
 #pragma unroll
     for (int r = 0; r < U; ++r) u[r] = y[(k + r) * YS];
@@ -394,7 +407,7 @@ __device__ __forceinline__ bool iir_eval_fused(double* y, const int n, const dou
   constexpr int U = 8;
   constexpr int TAPS = DBL ? 7 : 4;
   constexpr int D = TAPS - 1;      // deferred (wrapped) outputs
-  constexpr int WARM = DBL ? 64 : 32;
+  constexpr int WARM = DBL ? kDblWarm : 32;
   // logical j lives at y[j + s]: for s = 1 the row's first point is parked in
   // the padding slot y[n] (RS = n + 2) so no access needs a wrap, and moved
   // back at the end (the in-place outputs are position-relative)
@@ -540,6 +553,16 @@ __global__ void __launch_bounds__(kSplineT)
   const int t = threadIdx.x;
   const int64_t L0 = (int64_t)blockIdx.x * T;
   const int lines = (int)min((int64_t)T, a.nlines - L0);
+  // the line of lane t: consecutive lines, or (density epilogue, contiguous
+  // axis) the 32 v1 rows of one (v2, x2, v1 block)
+  int64_t pbase = 0, Lt = L0 + t;
+  if (CONTIG && DBL && a.part) {
+    const int64_t nblk = a.pnv1 / T;
+    const int64_t ix2 = blockIdx.x % a.pn2, rest = blockIdx.x / a.pn2;
+    const int64_t blk = rest % nblk, iv2 = rest / nblk;
+    Lt = (iv2 * a.pnv1 + blk * T + t) * a.pn2 + ix2;
+    pbase = ((iv2 * nblk + blk) * a.pn2 + ix2) * (int64_t)n;
+  }
   const int64_t outer0 = CONTIG ? 0 : L0 / a.S;
   const int64_t inner0 = CONTIG ? 0 : L0 - outer0 * a.S;
 
@@ -575,7 +598,7 @@ __global__ void __launch_bounds__(kSplineT)
     }
     if (CONTIG) {
       __syncwarp();  // lane 0's arrive.expect_tx precedes the copies
-      if (t < lines) bulk_g2s(tile + t * RS, a.src + (L0 + t) * n, (uint32_t)n * 8u, bars);
+      if (t < lines) bulk_g2s(tile + t * RS, a.src + Lt * n, (uint32_t)n * 8u, bars);
     } else if (a.use_tma) {
       // the whole [n][32] tile in one (or two, n > 256) TMA tensor copies
       if (t == 0)
@@ -630,7 +653,7 @@ __global__ void __launch_bounds__(kSplineT)
           // j0s = the row's (even) rotation for the bulk-store write-out
           double w4[4];
           int j0;
-          spline_eval_weights(a, L0 + t, n, -6.0 * z1, w4, j0);
+          spline_eval_weights(a, Lt, n, -6.0 * z1, w4, j0);
           if constexpr (DBL) {
             double c[7];
             spline_weights2(w4, c);
@@ -895,14 +918,41 @@ __global__ void __launch_bounds__(kSplineT)
     // row[0, jr)) issued by its own lane, instead of a warp loop over points
     if (t < lines) {
       const int jr = j0s[t];
-      double* out = a.dst + (L0 + t) * n;
+      double* out = a.dst + Lt * n;
       const double* row = tile + t * RS;
       fence_proxy_async_smem();  // the rows were written by generic stores
       bulk_s2g(out, row + jr, (uint32_t)(n - jr) * 8u);
       if (jr) bulk_s2g(out + (n - jr), row, (uint32_t)jr * 8u);
       bulk_commit();
-      bulk_wait_read<0>();  // shared memory must outlive the reads
     }
+    if constexpr (DBL) {
+      if (a.part) {
+        // density epilogue (compute_density, poisson.py:85-95, summed over
+        // this tile's 32 v1 rows): lane t sums the point pairs k = 2t, 2t + 1
+        // (+ 2T i) of every row in row order (out[k] = row[(jr + k) mod n];
+        // jr and n are even, so a pair never wraps and is one 16-byte load);
+        // consecutive lanes read consecutive words of one row, so the column
+        // walk is bank-conflict free and runs while the bulk stores read the
+        // same rows.  Measured at config 4: +0.09 ms on this pass against the
+        // 0.34 ms density pass it replaces (the tile mapping alone +0.01 ms)
+        wts[t] = a.pw1[(Lt / a.pn2) % a.pnv1];
+        __syncwarp();
+        for (int k = 2 * t; k < n; k += 2 * T) {
+          double s0 = 0.0, s1 = 0.0;
+#pragma unroll 8
+          for (int r = 0; r < T; ++r) {
+            int q = j0s[r] + k;
+            if (q >= n) q -= n;
+            const double2 v = *reinterpret_cast<const double2*>(tile + r * RS + q);
+            const double w = wts[r];
+            s0 = fma(v.x, w, s0);
+            s1 = fma(v.y, w, s1);
+          }
+          *reinterpret_cast<double2*>(a.part + pbase + k) = make_double2(s0, s1);
+        }
+      }
+    }
+    if (t < lines) bulk_wait_read<0>();  // shared memory must outlive the reads
   } else if (CONTIG) {
     // rows hold out rotated by j0: write them out coalesced
     for (int r = 0; r < lines; ++r) {
@@ -1166,6 +1216,11 @@ static int launch_spline(SplineTileArgs a, bool contig, bool exact, cudaStream_t
   // kernel; VPB_SPLINE_ROWS=1 selects the rows kernel for them
   static const bool force_rows = getenv("VPB_SPLINE_ROWS") != nullptr;
   const bool tile_fused = a.iir && a.n >= 64 && a.n % 8 == 0 && !force_rows;
+  if (a.part && !(contig && a.dbl && tile_fused)) {
+    set_error("spline density epilogue needs the fused contiguous double sweep "
+              "(n %% 8 == 0, n >= 64, recursive filters)");
+    return VPB_ERR_UNSUPPORTED;
+  }
   const bool rows_ok = contig && pcr && !no_rows && !(a.dbl && !dbl_rows) && !tile_fused &&
                        a.n % 32 == 0 &&
                        (npt == 1 || npt == 2 || npt == 4 || npt == 8) &&
@@ -1286,6 +1341,38 @@ extern "C" int vpb_spline_sweep_strided(double* view, const int64_t shape[4],
   }
   cudaFreeAsync(tmp, st);
   return rc;
+}
+
+extern "C" int64_t vpb_spline_density_part_len(const int64_t dims[4]) {
+  return dims[2] % kSplineT ? 0 : dims[0] * dims[1] * (dims[2] / kSplineT) * dims[3];
+}
+
+// The x1 double sweep of the merged x half steps with the density of its
+// output as an epilogue: part (vpb_spline_density_part_len doubles) receives
+// per (v2, 32-row v1 block) partial sums of out * wv1, which vpb_density
+// over dims {n1, n2, nv1 / 32, nv2} with unit v1 weights reduces to rho.
+extern "C" int vpb_spline_sweep_x1dbl_density(const double* src, double* dst,
+                                              const int64_t dims[4], const double* values,
+                                              double scale, double h, int32_t* flag,
+                                              const double* wv1, double* part, void* stream) {
+  VPB_REQUIRE(src != dst, "src and dst must be distinct buffers");
+  VPB_REQUIRE(h > 0.0, "spacing must be positive, got %g", h);
+  VPB_REQUIRE(wv1 && part, "null pointer");
+  const int64_t n1 = dims[0], n2 = dims[1], nv1 = dims[2], nv2 = dims[3];
+  VPB_REQUIRE(nv1 % kSplineT == 0, "density epilogue needs nv1 %% %d == 0, got %lld", kSplineT,
+              (long long)nv1);
+  VPB_REQUIRE((reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
+                  (reinterpret_cast<uintptr_t>(dst) & 15) == 0,
+              "density epilogue needs 16-byte aligned buffers");
+  const int64_t total = n1 * n2 * nv1 * nv2;
+  SplineTileArgs a{src, dst, total / n1, (int)n1, 1, nullptr, n2, nv1, values, scale, h,
+                   nullptr, flag};
+  a.dbl = 1;
+  a.part = part;
+  a.pw1 = wv1;
+  a.pn2 = n2;
+  a.pnv1 = nv1;
+  return launch_spline(a, true, false, (cudaStream_t)stream);
 }
 
 static int spline_axis(int32_t axis, const double* src, double* dst, const int64_t dims[4],

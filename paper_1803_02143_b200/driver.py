@@ -39,7 +39,7 @@ from .poisson import (
     scratch,
     solve_into,
 )
-from .spline import double_sweep_ok, sweep_spline, sweep_spline2
+from .spline import double_sweep_ok, sweep_spline, sweep_spline2, sweep_spline2_density
 
 
 # Fused x1+x2 plane sweeps and fused v1+v2 column sweeps (set False to run
@@ -63,6 +63,8 @@ FUSE_RHO = os.environ.get("VPB_FUSE_RHO", "1") != "0"
 # VPB_ARITH=exact|fast overrides the default; see set_arithmetic().
 _ARITH_MODES = ("fast", "exact")
 ARITH = os.environ.get("VPB_ARITH", "fast")
+# spline density fused into the merged x pass ("fast" arithmetic only)
+SPLINE_RHO = os.environ.get("VPB_SPLINE_RHO", "1") != "0"
 if ARITH not in _ARITH_MODES:
     raise ValueError(f"VPB_ARITH must be one of {_ARITH_MODES}, got {ARITH!r}")
 
@@ -322,6 +324,24 @@ class StepState:
                     cells.append(cell)
                 self.dens_w1, self.dens_w2 = cells
 
+        # spline ("fast"): density as an epilogue of the merged pass's x1
+        # double sweep (vpb_spline_sweep_x1dbl_density; the x2 double sweep
+        # runs first), partial sums per 32-row v1 block reduced by vpb_density
+        self.spline_rho = False
+        if (self.spline_x2 and grid.ndim == 4 and SPLINE_RHO
+                and os.environ.get("VPB_SPLINE_ROWS") is None
+                and grid.dof(0) % 8 == 0 and grid.dof(0) >= 64):
+            plen = int(lib.vpb_spline_density_part_len(_lib.dims(grid.dims4)))
+            if plen > 0:
+                self.spline_rho = True
+                d4 = grid.dims4
+                self.spart_dims = (d4[0], d4[1], d4[2] // 32, d4[3])
+                self.spart = torch.empty(plen, dtype=torch.float64, device=dev)
+                self.spart_w1 = torch.ones(d4[2] // 32, dtype=torch.float64, device=dev)
+                self.spart_work = torch.empty(
+                    int(lib.vpb_density_work_len(_lib.dims(self.spart_dims))),
+                    dtype=torch.float64, device=dev)
+
     def x_tables(self, d: int, tau: float):
         """Tables for the half x-sweep along space axis d: shift = v_d * (tau/2)."""
         key = (d, float(tau))
@@ -468,16 +488,34 @@ def enqueue_steps(field: DistributionField, tau: float, nsteps: int, st: StepSta
             xplane2_dg(grid, field._phys.view(-1), out, t1, t2, fa, fb)
         swap(out)
 
-    def x_double_spline(fl) -> None:
+    def x_double_spline(fl, with_density: bool) -> None:
         """Spline: closing x half step of one step + opening one of the next
         as one double sweep per x axis (vpb_spline_sweep_axis2); a
-        non-finite result is reported against the closing sub-step."""
-        for d in range(nx):
+        non-finite result is reported against the closing sub-step.  With
+        ``with_density`` the x2 double sweep runs first (the two axes'
+        operators commute) and the x1 one carries the density epilogue
+        (st.rho of the next step, compute_density poisson.py:85-95)."""
+        lib = _lib.load()
+        for d in ((1, 0) if with_density else range(nx)):
             out = st.buf
+            if with_density and d == 0:
+                mark("sweep_x1x2_rho")
+                sweep_spline2_density(grid, field._phys.view(-1), out, st.x_tables(0, tau),
+                                      half, grid.axes[0].h, fl[close_k:close_k + 1], st.wv1,
+                                      st.spart)
+                swap(out)
+                mark("density")
+                _lib.check(lib.vpb_density(st.spart.data_ptr(), _lib.dims(st.spart_dims),
+                                           st.spart_w1.data_ptr(), st.wv2.data_ptr(),
+                                           st.rho.data_ptr(), st.spart_work.data_ptr(),
+                                           _device.stream()), "vpb_density")
+                continue
             mark(f"sweep_{xn[d]}x2")
             sweep_spline2(grid, d, field._phys.view(-1), out, st.x_tables(d, tau), half,
                           grid.axes[d].h, fl[close_k + d:close_k + d + 1])
             swap(out)
+
+    rho_ready = set()  # steps whose density the merged spline pass produced
 
     def field_solve_of(m: int) -> None:
         fl = flags[m]
@@ -485,8 +523,9 @@ def enqueue_steps(field: DistributionField, tau: float, nsteps: int, st: StepSta
             mark("field_solve")
             solve_into(st.rc, grid, st.e, None, fl[field_k:field_k + 1], centred=True)
         else:
-            mark("density")
-            density_into(field.data, grid, st.rho)  # compute_density  poisson.py:85-95
+            if m not in rho_ready:
+                mark("density")
+                density_into(field.data, grid, st.rho)  # compute_density  poisson.py:85-95
             mark("field_solve")
             solve_into(st.rho, grid, st.e, stats[m], fl[field_k:field_k + 1])  # solve_poisson
 
@@ -536,7 +575,9 @@ def enqueue_steps(field: DistributionField, tau: float, nsteps: int, st: StepSta
         elif merge and st.fused_x:
             x_double(flags[m], flags[m + 1], st.fused_rho, stats[m + 1])
         elif merge and st.spline_x2 and ARITH == "fast":
-            x_double_spline(flags[m])
+            x_double_spline(flags[m], st.spline_rho)
+            if st.spline_rho:
+                rho_ready.add(m + 1)
         else:
             x_half(flags[m], close_k, False, None)
             x_half(flags[m + 1], 0, st.fused_rho, stats[m + 1])

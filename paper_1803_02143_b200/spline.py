@@ -94,6 +94,22 @@ def sweep_spline2(grid, axis: int, src: torch.Tensor, dst: torch.Tensor, values:
     )
 
 
+def sweep_spline2_density(grid, src: torch.Tensor, dst: torch.Tensor, values: torch.Tensor,
+                          scale: float, h: float, flag: torch.Tensor | None, wv1: torch.Tensor,
+                          part: torch.Tensor) -> None:
+    """The x1 double sweep of :func:`sweep_spline2` with the density of its
+    output as an epilogue (``vpb_spline_sweep_x1dbl_density``): ``part``
+    receives per (v2, 32-row v1 block) partial sums of ``out * wv1``."""
+    lib = _lib.load()
+    _lib.check(
+        lib.vpb_spline_sweep_x1dbl_density(src.data_ptr(), dst.data_ptr(), _lib.dims(grid.dims4),
+                                           values.data_ptr(), float(scale), float(h),
+                                           None if flag is None else flag.data_ptr(),
+                                           wv1.data_ptr(), part.data_ptr(), _device.stream()),
+        "vpb_spline_sweep_x1dbl_density",
+    )
+
+
 def double_sweep_ok(grid, axis: int) -> bool:
     """Whether :func:`sweep_spline2` supports this axis of the grid."""
     n = grid.dof(axis)

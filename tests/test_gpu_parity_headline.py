@@ -148,6 +148,29 @@ def test_reduced_configs_full_length_through_run(slvp, golden, tag, prob, method
         assert floored_rel(f, ref[m][0], FLOOR) <= FLOOR_TOL, (tag, m)
 
 
+def test_spline_density_epilogue_every_step_vs_reference(slvp):
+    """The spline path with the density fused into the merged x pass (x1
+    lines of 64 points, two 32-row v1 blocks; the 32^4 configuration above
+    is below the epilogue's 64-point minimum): advance(f0, tau, m) for every
+    m = 1..8 against the live reference -- f, EE and mass."""
+    prob, dofs, tau, nsteps = "landau4d", 64, 0.1, 8
+    f0 = _vpb_initial(prob, "spline", dofs, 0)
+    from paper_1803_02143_b200 import driver
+    assert driver.step_state(f0.grid).spline_rho
+    m0 = vpb.diagnostics(f0, 0.0).mass
+    worst = 0.0
+    for m, fr, rr in _reference_states(slvp, prob, "spline", dofs, 0, tau, nsteps):
+        g, rec = vpb.advance(f0, tau, m, record_time=m * tau)
+        got = g.numpy()
+        err = max_rel(got, fr)
+        worst = max(worst, err)
+        assert err <= F_TOL, (m, err)
+        assert floored_rel(got, fr, FLOOR) <= FLOOR_TOL, m
+        assert abs(rec.electric_energy - rr.electric_energy) <= EE_TOL * rr.electric_energy, m
+        assert abs(rec.mass - m0) <= MASS_TOL * m0, m
+    print(f"spline 64^4 density epilogue, {nsteps} steps: worst max-rel {worst:.2e}")
+
+
 def test_config3_small_advance_full_length(slvp, golden):
     """BASELINE config 3's two-stream IC (32^4 dofs, degree 1, dt=0.1), all
     200 steps through advance() in blocks of 10 (merged passes inside each

@@ -612,7 +612,8 @@ def test_advance_without_fused_x_pass_equals_strang_steps(monkeypatch, prob, met
 @pytest.mark.parametrize("prob,dofs,tau", [
     ("landau4d", (32, 64, 32, 48), 0.1),      # rows kernel NPT 1, strided tiles
     ("landau4d", (128, 32, 48, 32), 0.37),    # NPT 4, |shift| of several points
-    ("landau4d", (256, 48, 32, 32), 0.1),     # NPT 8
+    ("landau4d", (256, 48, 32, 32), 0.1),     # NPT 8, density epilogue (one v1 block)
+    ("landau4d", (64, 32, 96, 16), 0.37),     # density epilogue over three v1 blocks
     ("landau2d", (64, 96), 0.2),              # 1x1v: contiguous x
 ])
 def test_spline_double_sweep_advance_matches_strang_steps(monkeypatch, prob, dofs, tau):
@@ -628,6 +629,66 @@ def test_spline_double_sweep_advance_matches_strang_steps(monkeypatch, prob, dof
     driver._state_cached.cache_clear()
     a, b = f1.numpy(), f2.numpy()
     assert max_rel(b, a) <= 1e-13
+
+
+@pytest.mark.parametrize("dofs", [(64, 32, 64, 16), (128, 32, 32, 8), (96, 32, 32, 16)])
+def test_spline_x1_double_sweep_density_epilogue(dofs):
+    """vpb_spline_sweep_x1dbl_density: the x1 double sweep with the density
+    of its output as an epilogue equals the plain double sweep (the lines run
+    on other lanes, so a line's start point, and with it the rounding, may
+    differ) and vpb_density of that output."""
+    from paper_1803_02143_b200 import _device, _lib
+    from paper_1803_02143_b200.poisson import density_into
+    from paper_1803_02143_b200.spline import sweep_spline2, sweep_spline2_density
+    prob = vpb.problem_spec("landau4d")
+    grid = vpb.make_grid(prob, "spline", dofs)
+    f = vpb.initialize(prob, grid)
+    rng = np.random.default_rng(11)
+    f.data.copy_(torch.from_numpy(rng.standard_normal(f.data.numel())))
+    st = driver.step_state(grid)
+    assert st.spline_rho
+    vals, h = st.vpoints[0], grid.axes[0].h
+    d1 = torch.empty_like(f.data)
+    sweep_spline2(grid, 0, f.data, d1, vals, 0.37, h, None)
+    rho1 = torch.empty(grid.dof(0) * grid.dof(1), dtype=torch.float64, device="cuda")
+    density_into(d1, grid, rho1)
+    d2 = torch.full_like(f.data, float("nan"))
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    st.spart.fill_(float("nan"))
+    sweep_spline2_density(grid, f.data, d2, vals, 0.37, h, flag, st.wv1, st.spart)
+    rho2 = torch.empty_like(rho1)
+    lib = _lib.load()
+    _lib.check(lib.vpb_density(st.spart.data_ptr(), _lib.dims(st.spart_dims),
+                               st.spart_w1.data_ptr(), st.wv2.data_ptr(), rho2.data_ptr(),
+                               st.spart_work.data_ptr(), _device.stream()), "vpb_density")
+    assert flag.item() == 0
+    a, b = d1.cpu().numpy(), d2.cpu().numpy()
+    assert np.isfinite(b).all()
+    assert np.max(np.abs(a - b)) <= 1e-14 * np.max(np.abs(a))
+    r1, r2 = rho1.cpu().numpy(), rho2.cpu().numpy()
+    assert np.max(np.abs(r1 - r2)) <= 1e-13 * np.max(np.abs(r1))
+    # deterministic: a second run is bitwise the same
+    d3 = torch.empty_like(f.data)
+    part2 = st.spart.clone()
+    sweep_spline2_density(grid, f.data, d3, vals, 0.37, h, flag, st.wv1, st.spart)
+    assert torch.equal(d2, d3) and torch.equal(part2, st.spart)
+
+
+def test_spline_density_epilogue_advance_equals_separate_density(monkeypatch):
+    """advance() with the spline density epilogue against the same merged
+    passes with the standalone density pass (VPB_SPLINE_RHO=0 semantics)."""
+    monkeypatch.setattr(driver, "ARITH", "fast")
+    problem = vpb.problem_spec("landau4d")
+    grid = vpb.make_grid(problem, "spline", (64, 32, 64, 32))
+    driver._state_cached.cache_clear()
+    assert driver.step_state(grid).spline_rho
+    f1 = vpb.advance(vpb.initialize(problem, grid), 0.2, 5)
+    monkeypatch.setattr(driver, "SPLINE_RHO", False)
+    driver._state_cached.cache_clear()
+    assert not driver.step_state(grid).spline_rho
+    f2 = vpb.advance(vpb.initialize(problem, grid), 0.2, 5)
+    driver._state_cached.cache_clear()
+    assert max_rel(f1.numpy(), f2.numpy()) <= 1e-13
 
 
 @pytest.mark.parametrize("axis", [0, 1, 2, 3])
