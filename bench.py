@@ -701,6 +701,8 @@ def run_vpb(args, cfg_name: str, cfg: dict) -> None:
         from paper_1803_02143_b200 import hoststep
 
         host = hoststep.HostField.from_field(field)
+        field = graph = None  # the device-resident field is done: free its copy (config 5)
+        torch.cuda.empty_cache()
         k_e2e = max(1, min(args.steps, args.e2e_steps))
         hoststep.host_steps(host, tau, 1, blocks=args.e2e_blocks)  # warm-up (buffers, tables)
         barrier(d, local)
