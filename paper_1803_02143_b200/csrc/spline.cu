@@ -356,11 +356,11 @@ __device__ __forceinline__ void iir_solve2(double* y, const int YS, const int n,
 }
 
 // Evaluation weights of one line (_kernels.pyx:62-87), the gain g folded in.
-__device__ __forceinline__ void spline_eval_weights_of(const double value, const double scale,
-                                                       const double h, int n, double g,
-                                                       double (&w)[4], int& j0) {
-  const double shift = __dmul_rn(value, scale);
-  const double sh = __ddiv_rn(shift, h);
+__device__ __forceinline__ void spline_eval_weights(const SplineTileArgs& a, int64_t L, int n,
+                                                    double g, double (&w)[4], int& j0) {
+  const int64_t trow = a.idx ? a.idx[L] : (L / a.tdiv) % a.tmod;
+  const double shift = __dmul_rn(a.values[trow], a.scale);
+  const double sh = __ddiv_rn(shift, a.h);
   double off = floor(-sh);
   double th = __dsub_rn(-sh, off);
   if (th >= 1.0) {
@@ -377,12 +377,6 @@ __device__ __forceinline__ void spline_eval_weights_of(const double value, const
                        6.0);
   w[3] = g * __ddiv_rn(__dmul_rn(__dmul_rn(th, th), th), 6.0);
   j0 = (int)wrap_mod((int64_t)off - 1, n);
-}
-
-__device__ __forceinline__ void spline_eval_weights(const SplineTileArgs& a, int64_t L, int n,
-                                                    double g, double (&w)[4], int& j0) {
-  const int64_t trow = a.idx ? a.idx[L] : (L / a.tdiv) % a.tmod;
-  spline_eval_weights_of(a.values[trow], a.scale, a.h, n, g, w, j0);
 }
 
 // Contiguous-axis sweep (single, or the double sweep of merged half steps),
@@ -406,14 +400,10 @@ __device__ __forceinline__ void spline_eval_weights(const SplineTileArgs& a, int
 // periodic start values are sums over the preceding points), so only the
 // rounding of the two half-warps' lines differs.  Requires n >= 64, n % 8 == 0.
 // Returns true when an output is not finite.
-// STR: the line's points are `ys` doubles apart (a column of a [row][RS] plane
-// tile, lanes along consecutive columns: conflict-free without the stagger;
-// s must be 0).
-template <bool DBL, bool STR = false>
+template <bool DBL>
 __device__ __forceinline__ bool iir_eval_fused(double* y, const int n, const double z1,
                                                const double (&c)[DBL ? 7 : 4], const int s,
-                                               const int sigma, const int ys = 1) {
-  const int YS = STR ? ys : 1;
+                                               const int sigma) {
   constexpr int U = 8;
   constexpr int TAPS = DBL ? 7 : 4;
   constexpr int D = TAPS - 1;      // deferred (wrapped) outputs
@@ -422,7 +412,7 @@ __device__ __forceinline__ bool iir_eval_fused(double* y, const int n, const dou
   // the padding slot y[n] (RS = n + 2) so no access needs a wrap, and moved
   // back at the end (the in-place outputs are position-relative)
   double* yb = y + s;
-  if (!STR && s) y[n] = y[0];
+  if (s) y[n] = y[0];
   auto eval = [&](double w, const double (&win)[D]) -> double {
     if constexpr (DBL) {
       double o = c[0] * w;
@@ -441,7 +431,7 @@ __device__ __forceinline__ bool iir_eval_fused(double* y, const int n, const dou
   for (int k = n - WARM; k < n; k += U) {
     double u[U];
 #pragma unroll
-    for (int r = 0; r < U; ++r) u[r] = yb[(k + r) * YS];
+    for (int r = 0; r < U; ++r) u[r] = yb[k + r];
 #pragma unroll
     for (int r = 0; r < U; ++r) {
       p1 = fma(z1, p1, u[r]);
@@ -451,7 +441,7 @@ __device__ __forceinline__ bool iir_eval_fused(double* y, const int n, const dou
   for (int k = 0; k < n; k += U) {
     double u[U];
 #pragma unroll
-    for (int r = 0; r < U; ++r) u[r] = yb[(k + r) * YS];
+    for (int r = 0; r < U; ++r) u[r] = yb[k + r];
 #pragma unroll
     for (int r = 0; r < U; ++r) {
       p1 = fma(z1, p1, u[r]);
@@ -463,14 +453,14 @@ __device__ __forceinline__ bool iir_eval_fused(double* y, const int n, const dou
       }
     }
 #pragma unroll
-    for (int r = 0; r < U; ++r) yb[(k + r) * YS] = u[r];
+    for (int r = 0; r < U; ++r) yb[k + r] = u[r];
   }
   // ---- anticausal pass, periodic start from the WARM points after n - 1
   double q1 = 0.0, q2 = 0.0;
   for (int k = WARM - U; k >= 0; k -= U) {
     double u[U];
 #pragma unroll
-    for (int r = 0; r < U; ++r) u[r] = yb[(k + r) * YS];
+    for (int r = 0; r < U; ++r) u[r] = yb[k + r];
 #pragma unroll
     for (int r = U - 1; r >= 0; --r) {
       q1 = fma(z1, q1, u[r]);
@@ -494,7 +484,7 @@ __device__ __forceinline__ bool iir_eval_fused(double* y, const int n, const dou
     const int k = n - U;
     double u[U];
 #pragma unroll
-    for (int r = 0; r < U; ++r) u[r] = yb[(k + r) * YS];
+    for (int r = 0; r < U; ++r) u[r] = yb[k + r];
 #pragma unroll
     for (int r = U - 1; r >= 0; --r) u[r] = chain(u[r]);  // w_{k+r}
 #pragma unroll
@@ -509,14 +499,14 @@ __device__ __forceinline__ bool iir_eval_fused(double* y, const int n, const dou
       em.add(o[r]);
     }
 #pragma unroll
-    for (int r = 0; r < U - D; ++r) yb[(k + r + sigma) * YS] = o[r];
+    for (int r = 0; r < U - D; ++r) yb[k + r + sigma] = o[r];
 #pragma unroll
     for (int m = 0; m < D; ++m) win[m] = u[m];  // w_{n-8} .. w_{n-8+D-1}
   }
   for (int k = n - 2 * U; k >= 0; k -= U) {
     double u[U], o[U];
 #pragma unroll
-    for (int r = 0; r < U; ++r) u[r] = yb[(k + r) * YS];
+    for (int r = 0; r < U; ++r) u[r] = yb[k + r];
 #pragma unroll
     for (int r = U - 1; r >= 0; --r) {
       const double w = chain(u[r]);  // w_{k+r}; window w_{k+r+1 ..} in win
@@ -527,7 +517,7 @@ __device__ __forceinline__ bool iir_eval_fused(double* y, const int n, const dou
       em.add(o[r]);
     }
 #pragma unroll
-    for (int r = 0; r < U; ++r) yb[(k + r + sigma) * YS] = o[r];
+    for (int r = 0; r < U; ++r) yb[k + r + sigma] = o[r];
   }
   // win = w_0 .. w_{D-1}: the wrapped outputs j = n-D .. n-1
 #pragma unroll
@@ -541,9 +531,9 @@ __device__ __forceinline__ bool iir_eval_fused(double* y, const int n, const dou
     const double o = eval(tail[r], wv);
     em.add(o);
     const int slot = n - D + r + sigma;
-    yb[(slot >= n ? slot - n : slot) * YS] = o;
+    yb[slot >= n ? slot - n : slot] = o;
   }
-  if (!STR && s) y[0] = y[n];
+  if (s) y[0] = y[n];
   return em.bad();
 }
 
