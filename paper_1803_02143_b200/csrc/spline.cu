@@ -641,6 +641,12 @@ __global__ void __launch_bounds__(kSplineT)
     const double mc = a.fac[4 * n + 4], dc = a.fac[4 * n + 5], rc = a.fac[4 * n + 6];
     double* y = CONTIG ? tile + t * RS : tile + t;
     double wscale = 1.0;
+    // The line's evaluation weights first (unscaled; _kernels.pyx:62-87): their
+    // ~900 instructions (five fp64 divisions, 64-bit index arithmetic) run
+    // while the tile's copies are still in flight instead of after the wait.
+    double ew[4];
+    int ej0;
+    spline_eval_weights(a, Lt, n, 1.0, ew, ej0);
     if constexpr (PCR) {
       // parallel cyclic reduction in shared memory: no serial chain per line
       if (bulk)
@@ -651,9 +657,9 @@ __global__ void __launch_bounds__(kSplineT)
         if (fused_eval) {
           // solve + evaluation in one pass pair over the row (iir_eval_fused);
           // j0s = the row's (even) rotation for the bulk-store write-out
-          double w4[4];
-          int j0;
-          spline_eval_weights(a, Lt, n, -6.0 * z1, w4, j0);
+          const double g = -6.0 * z1;
+          const double w4[4] = {g * ew[0], g * ew[1], g * ew[2], g * ew[3]};
+          const int j0 = ej0;
           if constexpr (DBL) {
             double c[7];
             spline_weights2(w4, c);
@@ -756,33 +762,16 @@ __global__ void __launch_bounds__(kSplineT)
     }  // Thomas
 
     if (!fused_eval) {
-    // evaluation weights (_kernels.pyx:62-87)
+    // evaluation weights (computed above, before the tile landed)
     const int64_t L = L0 + t;
-    const int64_t row = a.idx ? a.idx[L] : (L / a.tdiv) % a.tmod;
-    const double shift = __dmul_rn(a.values[row], a.scale);
-    const double s = __ddiv_rn(shift, a.h);
-    double off = floor(-s);
-    double th = __dsub_rn(-s, off);
-    if (th >= 1.0) {
-      off = __dadd_rn(off, 1.0);
-      th = 0.0;
-    }
-    const double omt = __dsub_rn(1.0, th);
-    double w0 = __ddiv_rn(__dmul_rn(__dmul_rn(omt, omt), omt), 6.0);
-    double w1 = __ddiv_rn(__dadd_rn(__dsub_rn(4.0, __dmul_rn(__dmul_rn(6.0, th), th)),
-                                          __dmul_rn(__dmul_rn(__dmul_rn(3.0, th), th), th)),
-                                6.0);
-    double w2 = __ddiv_rn(__dadd_rn(__dsub_rn(4.0, __dmul_rn(__dmul_rn(6.0, omt), omt)),
-                                          __dmul_rn(__dmul_rn(__dmul_rn(3.0, omt), omt), omt)),
-                                6.0);
-    double w3 = __ddiv_rn(__dmul_rn(__dmul_rn(th, th), th), 6.0);
+    double w0 = ew[0], w1 = ew[1], w2 = ew[2], w3 = ew[3];
     if constexpr (PCR) {
       w0 *= wscale;
       w1 *= wscale;
       w2 *= wscale;
       w3 *= wscale;
     }
-    const int j0 = (int)wrap_mod((int64_t)off - 1, n);
+    const int j0 = ej0;
     j0s[t] = j0;
     if constexpr (DBL) {
       // out_i = sum_m c_m w2[2 j0 + i + m], m = 0..6: a 7-value sliding window
