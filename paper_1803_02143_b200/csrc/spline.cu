@@ -628,6 +628,7 @@ __global__ void __launch_bounds__(kSplineT)
 
   // ---- per-line solve (Thomas + Sherman-Morrison) and evaluation -----------
   bool bad = false;
+  double pw_early = 0.0;  // the line's density weight (epilogue), loaded before the wait
   // contiguous recursive-filter sweeps: evaluated inside the solve
   // (iir_eval_fused); uniform over the warp (template flags and arguments)
   const bool fused_eval = CONTIG && PCR && a.iir && n >= 64 && n % 8 == 0;
@@ -647,13 +648,19 @@ __global__ void __launch_bounds__(kSplineT)
     double ew[4];
     int ej0;
     spline_eval_weights(a, Lt, n, 1.0, ew, ej0);
+    // likewise the filter pole and the line's density weight: global loads
+    // whose latency would otherwise follow the wait
+    const double z1_early = PCR ? __ldg(a.fac + 4 * n + 7 + kPcrLevels + 2) : 0.0;
+    if constexpr (CONTIG && DBL) {
+      if (a.part) pw_early = __ldg(a.pw1 + (Lt / a.pn2) % a.pnv1);
+    }
     if constexpr (PCR) {
       // parallel cyclic reduction in shared memory: no serial chain per line
       if (bulk)
         for (int bb = 0; bb < nbars; ++bb) mbar_wait(bars + bb, 0);
       const double* pk = a.fac + 4 * n + 7;
       if (a.iir) {
-        const double z1 = pk[kPcrLevels + 2];  // z1^1 of the power table
+        const double z1 = z1_early;  // z1^1 of the power table
         if (fused_eval) {
           // solve + evaluation in one pass pair over the row (iir_eval_fused);
           // j0s = the row's (even) rotation for the bulk-store write-out
@@ -924,7 +931,7 @@ __global__ void __launch_bounds__(kSplineT)
         // walk is bank-conflict free and runs while the bulk stores read the
         // same rows.  Measured at config 4: +0.09 ms on this pass against the
         // 0.34 ms density pass it replaces (the tile mapping alone +0.01 ms)
-        wts[t] = a.pw1[(Lt / a.pn2) % a.pnv1];
+        wts[t] = pw_early;
         __syncwarp();
         for (int k = 2 * t; k < n; k += 2 * T) {
           double s0 = 0.0, s1 = 0.0;
