@@ -556,12 +556,15 @@ __global__ void __launch_bounds__(kSplineT)
   // the line of lane t: consecutive lines, or (density epilogue, contiguous
   // axis) the 32 v1 rows of one (v2, x2, v1 block)
   int64_t pbase = 0, Lt = L0 + t;
+  int tc1 = (int)L0, tc2 = 0;  // contiguous tiles by TMA: box coordinates {0, tc1, tc2}
   if (CONTIG && DBL && a.part) {
     const int64_t nblk = a.pnv1 / T;
     const int64_t ix2 = blockIdx.x % a.pn2, rest = blockIdx.x / a.pn2;
     const int64_t blk = rest % nblk, iv2 = rest / nblk;
     Lt = (iv2 * a.pnv1 + blk * T + t) * a.pn2 + ix2;
     pbase = ((iv2 * nblk + blk) * a.pn2 + ix2) * (int64_t)n;
+    tc1 = (int)ix2;
+    tc2 = (int)(iv2 * a.pnv1 + blk * T);
   }
   const int64_t outer0 = CONTIG ? 0 : L0 / a.S;
   const int64_t inner0 = CONTIG ? 0 : L0 - outer0 * a.S;
@@ -588,7 +591,8 @@ __global__ void __launch_bounds__(kSplineT)
       for (int b = 0; b < nbars; ++b) mbar_init(bars + b, 1);
       fence_mbar_init();
       if (CONTIG) {
-        mbar_arrive_expect_tx(bars, (uint32_t)lines * n * 8u);
+        // TMA: the whole box counts, zero-filled padding columns and rows included
+        mbar_arrive_expect_tx(bars, a.use_tma ? (uint32_t)T * RS * 8u : (uint32_t)lines * n * 8u);
       } else {
         for (int b = 0; b < nbars; ++b) {
           const int rows = min(rows_per_bar, n - b * rows_per_bar);
@@ -596,7 +600,11 @@ __global__ void __launch_bounds__(kSplineT)
         }
       }
     }
-    if (CONTIG) {
+    if (CONTIG && a.use_tma) {
+      // one tensor copy for the tile: the box is n + 2 points wide, two more
+      // than the tensor, so the rows land RS apart (the padding is zero-filled)
+      if (t == 0) tma_load_3d(tile, &tmap, 0, tc1, tc2, bars);
+    } else if (CONTIG) {
       __syncwarp();  // lane 0's arrive.expect_tx precedes the copies
       if (t < lines) bulk_g2s(tile + t * RS, a.src + Lt * n, (uint32_t)n * 8u, bars);
     } else if (a.use_tma) {
@@ -1199,6 +1207,28 @@ static int launch_spline(SplineTileArgs a, bool contig, bool exact, cudaStream_t
                                (uint32_t)std::min(a.n, 256), 1)
                     ? 1
                     : 0;
+  }
+  // fused contiguous sweeps: the [32 lines][n + 2] tile in one tensor copy
+  // (rows of a 2-D view of the lines, or -- density epilogue -- the 32 v1 rows
+  // of one (v2, x2) in the 3-D view {x1, x2, v}); VPB_SPLINE_CONTIG_TMA=0: one
+  // bulk copy per line, issued by its lane
+  static const bool contig_tma = !(getenv("VPB_SPLINE_CONTIG_TMA") &&
+                                   atoi(getenv("VPB_SPLINE_CONTIG_TMA")) == 0);
+  if (contig && contig_tma && a.iir && a.n >= 64 && a.n % 8 == 0 && a.n + 2 <= 256 &&
+      getenv("VPB_SPLINE_ROWS") == nullptr &&
+      (reinterpret_cast<uintptr_t>(a.src) & 15) == 0) {
+    const uint64_t nn = (uint64_t)a.n;
+    if (a.part)
+      a.use_tma = encode_tmap_3d(&tmap, a.src, nn, (uint64_t)a.pn2,
+                                 (uint64_t)(a.nlines / a.pn2), nn * 8, nn * a.pn2 * 8,
+                                 (uint32_t)a.n + 2, 1, kSplineT)
+                      ? 1
+                      : 0;
+    else
+      a.use_tma = encode_tmap_3d(&tmap, a.src, nn, (uint64_t)a.nlines, 1, nn * 8,
+                                 nn * a.nlines * 8, (uint32_t)a.n + 2, kSplineT, 1)
+                      ? 1
+                      : 0;
   }
   static const bool no_rows = getenv("VPB_SPLINE_TILES") != nullptr;
   const int npt = a.n / 32;
