@@ -415,10 +415,13 @@ __device__ __forceinline__ bool iir_eval_fused(double* y, const int n, const dou
   if (s) y[n] = y[0];
   auto eval = [&](double w, const double (&win)[D]) -> double {
     if constexpr (DBL) {
-      double o = c[0] * w;
+      // oldest value first, the value just solved (w) last: only one fma of
+      // the 7-term chain waits for the recursion step that produced w, the
+      // rest can issue while earlier points' chains are in flight
+      double o = c[TAPS - 1] * win[TAPS - 2];
 #pragma unroll
-      for (int m = 1; m < TAPS; ++m) o = fma(c[m], win[m - 1], o);
-      return o;
+      for (int m = TAPS - 2; m >= 1; --m) o = fma(c[m], win[m - 1], o);
+      return fma(c[0], w, o);
     } else {  // out = w0 w_j + w1 w_{j+1} + w2 w_{j+2} + w3 w_{j+3}, left to right
       double o = __dmul_rn(c[0], w);
       o = __dadd_rn(o, __dmul_rn(c[1], win[0]));
