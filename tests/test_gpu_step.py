@@ -709,6 +709,56 @@ def test_spline_double_sweep_rows_kernel_equals_two_sweeps(monkeypatch):
     assert r.returncode == 0, r.stderr[-2000:]
 
 
+def _contig_tile_digest():
+    """sha256 of the contiguous-axis spline sweeps of one random field: the
+    single sweep, the double sweep and the double sweep with the density
+    epilogue (f and the partial densities), on full and on partial tiles."""
+    import hashlib
+    from paper_1803_02143_b200.spline import sweep_spline, sweep_spline2, sweep_spline2_density
+    h = hashlib.sha256()
+    for dofs in ((128, 32, 32, 8), (72, 24, 32, 4), (64, 20, 5, 4)):
+        prob = vpb.problem_spec("landau4d")
+        grid = vpb.make_grid(prob, "spline", dofs)
+        f = vpb.initialize(prob, grid)
+        rng = np.random.default_rng(31)
+        f.data.copy_(torch.from_numpy(rng.standard_normal(f.data.numel())))
+        st = driver.step_state(grid)
+        vals, hx = st.vpoints[0], grid.axes[0].h
+        flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+        out = torch.empty_like(f.data)
+        sweep_spline(grid, 0, f.data, out, vals, 0.41, hx, flag)
+        h.update(out.cpu().numpy().tobytes())
+        if grid.dof(0) % 16 == 0:
+            sweep_spline2(grid, 0, f.data, out, vals, 0.41, hx, flag)
+            h.update(out.cpu().numpy().tobytes())
+        if st.spline_rho:
+            sweep_spline2_density(grid, f.data, out, vals, 0.41, hx, flag, st.wv1, st.spart)
+            h.update(out.cpu().numpy().tobytes())
+            h.update(st.spart.cpu().numpy().tobytes())
+        assert flag.item() == 0
+    return h.hexdigest()
+
+
+def test_spline_contiguous_tiles_tma_equals_per_lane_copies():
+    """The fused contiguous-axis sweeps load their [32 lines][n + 2] tile by
+    one TMA tensor copy whose box is two points wider than the tensor (the
+    zero-filled padding columns give the row pitch); VPB_SPLINE_CONTIG_TMA=0
+    selects one bulk copy per line.  Both must give the same bits (the
+    switch is read once per process, so each side runs in a child)."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, 'tests'); import test_gpu_step as t; "
+            "print('DIGEST', t._contig_tile_digest())")
+    got = {}
+    for tma in ("1", "0"):
+        env = dict(__import__("os").environ, VPB_SPLINE_CONTIG_TMA=tma)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True,
+                           text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        got[tma] = [ln for ln in r.stdout.splitlines() if ln.startswith("DIGEST")][-1]
+    assert got["1"] == got["0"]
+
+
 def _double_vs_two(axis):
     from paper_1803_02143_b200.spline import sweep_spline, sweep_spline2
     prob = vpb.problem_spec("landau4d")
